@@ -1,0 +1,177 @@
+/*
+ * epd.h -- C ABI of the B200-native EPD encode-stage hot path.
+ *
+ * This is the drop-in boundary for the encode path of the EPD reference
+ * simulator (`disaggsim`, /root/reference/pkg/src/disaggsim). The reference
+ * has no FFI of its own: its encode worker, multimodal-token cache and stage
+ * handoff are Python calls inside `engine._Sim`. Each group below names the
+ * reference interface it stands behind (file:line, relative to
+ * /root/reference/pkg/src/disaggsim/). Signatures use plain pointers, sizes and
+ * opaque handles only; device pointers are caller-owned unless stated, and
+ * `stream` is a cudaStream_t passed as void*. All work is asynchronous on
+ * `stream`; nothing synchronises the host except where documented.
+ *
+ * Errors: every call returns an epd_status_t. The Python host maps each code
+ * to the exception class the reference raises for the same condition.
+ */
+#ifndef EPD_H_
+#define EPD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EPD_ABI_VERSION 1
+
+typedef enum {
+  EPD_OK = 0,
+  EPD_ERR_VALUE = 1,       /* ValueError: irp_shard width<1 / patches<0 (engine.py:57-60),
+                              negative counts (costs.py:85-86), bad shapes */
+  EPD_ERR_RUNTIME = 2,     /* RuntimeError: cache misuse / overcommit (blocks.py:47-60) */
+  EPD_ERR_CAPACITY = 4,    /* CapacityExceeded (simconfig.py:19-20): table or cache full */
+  EPD_ERR_CUDA = 5,        /* RuntimeError carrying the CUDA error string */
+  EPD_ERR_UNSUPPORTED = 6  /* ValueError: configuration outside what the kernels implement */
+} epd_status_t;
+
+int32_t epd_abi_version(void);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* epd_last_error(void);
+
+/* ------------------------------------------------------------------ routing
+ * Replaces engine.irp_shard (engine.py:55-62): balanced partition of one
+ * request's tiles across `width` encode workers; the first `patches % width`
+ * workers get one extra tile. counts[width] is written.
+ */
+epd_status_t epd_irp_shard(int64_t patches, int32_t width, int64_t* counts);
+
+/* Contiguous tile ranges implied by the shard order in engine._start_encode
+ * (engine.py:589-602): worker k owns [first[k], first[k] + counts[k]). */
+epd_status_t epd_irp_ranges(int64_t patches, int32_t width, int64_t* first, int64_t* counts);
+
+/* ------------------------------------------------------------------ encoder
+ * Replaces the modeled cost costs.encode_latency (costs.py:78-90) with the
+ * real vision encoder + resampler/projector. One encoder per GPU process.
+ */
+typedef struct epd_encoder epd_encoder_t;
+
+enum {
+  EPD_FAMILY_SIGLIP_RESAMPLER = 1, /* MiniCPM-V 2.6: SigLIP ViT + 2D-sincos perceiver resampler */
+  EPD_FAMILY_INTERNVIT_MLP = 2     /* InternVL2: InternViT (CLS, layer scale) + pixel shuffle + MLP */
+};
+
+typedef struct {
+  int32_t family;
+  int32_t image_size;  /* tile side in pixels (448) */
+  int32_t patch_size;  /* 14 */
+  int32_t channels;    /* 3 */
+  int32_t hidden;      /* ViT width */
+  int32_t layers;
+  int32_t heads;
+  int32_t mlp;         /* ViT MLP width */
+  int32_t out_tokens;  /* MM tokens per tile (models.cfg tokens_per_patch) */
+  int32_t out_dim;     /* MM token width (models.cfg hidden_dim) */
+  int32_t out_heads;   /* resampler attention heads (family 1) */
+  int32_t max_tiles;   /* workspace bound for one epd_encode_tiles call */
+  float ln_eps;
+  float mean[3];
+  float std[3];
+} epd_encoder_desc_t;
+
+epd_status_t epd_encoder_create(const epd_encoder_desc_t* desc, int32_t device, epd_encoder_t** out);
+void epd_encoder_destroy(epd_encoder_t* enc);
+/* Canonical (framework-layout, fp32) weight schema; index order is stable. */
+int32_t epd_encoder_num_weights(const epd_encoder_t* enc);
+epd_status_t epd_encoder_weight_info(const epd_encoder_t* enc, int32_t index, const char** name,
+                                     int32_t* ndim, int64_t* shape /* [4] */);
+/* Host fp32 values for weight `index`; the library converts to bf16 and to
+ * its own B200 layout (head padding, fused QKV, transposes) at finalize. */
+epd_status_t epd_encoder_set_weight(epd_encoder_t* enc, int32_t index, const float* host_values,
+                                    int64_t numel);
+/* Uploads weights and precomputes weight-only constants. Synchronises. */
+epd_status_t epd_encoder_finalize(epd_encoder_t* enc, void* stream);
+/* tiles: device uint8 [n][S][S][C] (HWC); out: device bf16 [n][out_tokens][out_dim]. */
+epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t n, void* out,
+                              void* stream);
+/* Algorithmic FLOPs of one tile (roofline numerator). */
+double epd_encoder_flops_per_tile(const epd_encoder_t* enc);
+/* Kernel launches issued by one epd_encode_tiles call over n tiles. */
+int32_t epd_encoder_launches(const epd_encoder_t* enc, int32_t n);
+
+/* ------------------------------------------------------------------ MM-token cache
+ * Stands behind blocks.BlockManager(CacheKind.MM) (blocks.py:14-61) as the
+ * encode-side multimodal cache; adds the content-hash lookup the reference
+ * lacks so repeated images skip encoding. Keys are 2 x u64 per record.
+ */
+typedef struct epd_mmcache epd_mmcache_t;
+
+/* keys[n][2] <- content hash of n records of rec_bytes each (pitch rec_stride).
+ * scratch: device buffer of >= 16*n bytes. */
+epd_status_t epd_hash_records(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
+                              uint64_t* keys, void* scratch, void* stream);
+/* Table with at least 2*capacity slots (power of two). */
+epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t** out);
+void epd_mmcache_destroy(epd_mmcache_t* cache);
+/* entry[i] = value stored for keys[i] or -1; dup[i] = first j < i with the same
+ * key among misses, else -1 (in-batch repeats). */
+epd_status_t epd_mmcache_lookup(epd_mmcache_t* cache, const uint64_t* keys, int32_t n,
+                                int32_t* entry, int32_t* dup, void* stream);
+/* Insert absent, batch-unique keys with their entry ids. */
+epd_status_t epd_mmcache_insert(epd_mmcache_t* cache, const uint64_t* keys, const int32_t* entries,
+                                int32_t n, void* stream);
+epd_status_t epd_mmcache_erase(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, void* stream);
+epd_status_t epd_mmcache_clear(epd_mmcache_t* cache, void* stream);
+/* Synchronises `stream`; EPD_ERR_CAPACITY if any insert found no free slot. */
+epd_status_t epd_mmcache_check(epd_mmcache_t* cache, void* stream);
+
+/* ------------------------------------------------------------------ packing / handoff
+ * MM-token packing (implicit in engine._send_ready_shards, engine.py:521-526):
+ * dst[i] = src[index[i]] for records of rec_bytes (16-byte multiples). */
+epd_status_t epd_gather_records(const void* src, const int32_t* index, int32_t n, int64_t rec_bytes,
+                                void* dst, void* stream);
+/* dst[index[i]] = src[i]. */
+epd_status_t epd_scatter_records(const void* src, const int32_t* index, int32_t n, int64_t rec_bytes,
+                                 void* dst, void* stream);
+/* Paged KV handoff (engine._try_reserve_decode / _on_transfer_end("pd"),
+ * engine.py:542-555, 436-439). The cache holds `segments` (= 2 x layers)
+ * arrays of fixed-size blocks: block b of segment s starts at
+ * cache + s*segment_stride + b*block_bytes. pack: out[i][s] = cache[s][ids[i]];
+ * unpack: cache[s][ids[i]] = in[i][s]. */
+epd_status_t epd_kv_pack(const void* cache, int32_t segments, int64_t segment_stride,
+                         int64_t block_bytes, const int32_t* block_ids, int32_t nblocks, void* out,
+                         void* stream);
+epd_status_t epd_kv_unpack(const void* in, int32_t segments, int64_t segment_stride,
+                           int64_t block_bytes, const int32_t* block_ids, int32_t nblocks, void* cache,
+                           void* stream);
+
+/* ------------------------------------------------------------------ kernel-level ops
+ * The building blocks epd_encode_tiles is made of, exported for per-kernel
+ * parity tests and profiling. All tensors are device bf16 unless stated.
+ *
+ * out[M,N] = act(A[M,K] W[N,K]^T + bias) ; if resid: out = resid[row % r_mod] + lscale * out
+ * act: 0 none, 1 GELU (tanh approximation), 2 GELU (erf). bias/resid/lscale may be NULL.
+ * bn: N tile (0 = auto, else 128/192/256). */
+epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
+                             int32_t K, const void* bias, int32_t act, const void* resid, int32_t ldr,
+                             int32_t r_mod, const void* lscale, void* out, int32_t ldo, int32_t bn,
+                             void* stream);
+/* O = softmax(Q K^T * scale) V per (batch, head); see csrc/kernels.h AttnParams.
+ * q: [q_shared ? H : B*H][Tq][Dp], k: [B*H][Tk][Dp], vt: [B*H][Dp][Tkpad],
+ * out[(b*Tq + i)*ldo + h*Dv + d]. Dp in {64, 80, 128}. */
+epd_status_t epd_attention_bf16(const void* q, const void* k, const void* vt, void* out, int32_t B,
+                                int32_t H, int32_t Tq, int32_t Tk, int32_t Tkpad, int32_t Dp, int32_t Dv,
+                                int32_t ldo, int32_t q_shared, float scale, void* stream);
+epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
+                                const void* beta, int32_t rows, int32_t D, float eps, void* stream);
+/* uint8 HWC tiles [n][S][S][C] -> bf16 rows [n*rows_per_tile][Kpad], patch rows start at
+ * row_offset within each tile's block; columns in (c, ky, kx) order, zero padded. */
+epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t S, int32_t C, int32_t p, int32_t Kpad,
+                             int32_t row_offset, int32_t rows_per_tile, const float* mean3, const float* std3,
+                             void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EPD_H_ */

@@ -1,0 +1,365 @@
+// extern "C" surface declared in include/epd.h: argument checking, error
+// strings, and thin forwarding to the kernels / encoder executor.
+#include <cstring>
+#include <string>
+
+#include "../../include/epd.h"
+#include "encoder.h"
+#include "kernels.h"
+#include "mmcache.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+epd_status_t fail(epd_status_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+epd_status_t cuda_status(int rc, const char* what) {
+  if (rc == 0) return EPD_OK;
+  std::string m = std::string(what) + ": ";
+  if (rc < 1000)
+    m += cudaGetErrorString((cudaError_t)rc);
+  else
+    m += "invalid shape/alignment (code " + std::to_string(rc) + ")";
+  return fail(rc < 1000 ? EPD_ERR_CUDA : EPD_ERR_VALUE, m);
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Two-level record copy used by the KV handoff:
+//   pack:   out[i][s] = cache[s][ids[i]]
+//   unpack: cache[s][ids[i]] = in[i][s]
+__global__ void kv_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int segments,
+                               long long seg_stride, long long block_bytes, const int32_t* __restrict__ ids,
+                               int pack) {
+  const int i = blockIdx.z;
+  const int s = blockIdx.y;
+  const long long cache_off = (long long)s * seg_stride + (long long)ids[i] * block_bytes;
+  const long long packed_off = ((long long)i * segments + s) * block_bytes;
+  const uint4* a = reinterpret_cast<const uint4*>(src + (pack ? cache_off : packed_off));
+  uint4* b = reinterpret_cast<uint4*>(dst + (pack ? packed_off : cache_off));
+  const long long vecs = block_bytes / 16;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < vecs;
+       v += (long long)gridDim.x * blockDim.x)
+    b[v] = a[v];
+}
+
+__global__ void scatter_records_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ index,
+                                       size_t vecs, uint4* __restrict__ dst) {
+  const int rec = blockIdx.y;
+  const uint4* s = src + (size_t)rec * vecs;
+  uint4* d = dst + (size_t)index[rec] * vecs;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < vecs;
+       i += (size_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+epd_status_t kv_copy(const void* src, void* dst, int32_t segments, int64_t seg_stride, int64_t block_bytes,
+                     const int32_t* ids, int32_t nblocks, int pack, void* stream) {
+  if (segments < 1 || block_bytes <= 0 || nblocks < 0 || seg_stride < block_bytes)
+    return fail(EPD_ERR_VALUE, "kv handoff: bad geometry");
+  if (block_bytes % 16 || seg_stride % 16 ||
+      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15))
+    return fail(EPD_ERR_VALUE, "kv handoff: blocks must be 16-byte aligned");
+  if (nblocks == 0) return EPD_OK;
+  if (segments > 65535 || nblocks > 65535) return fail(EPD_ERR_VALUE, "kv handoff: too many blocks");
+  long long vecs = block_bytes / 16;
+  int bx = (int)((vecs + 255) / 256);
+  if (bx > 8) bx = 8;
+  dim3 grid(bx, segments, nblocks);
+  kv_copy_kernel<<<grid, 256, 0, S(stream)>>>(reinterpret_cast<const uint8_t*>(src),
+                                              reinterpret_cast<uint8_t*>(dst), segments, seg_stride,
+                                              block_bytes, ids, pack);
+  return cuda_status((int)cudaGetLastError(), "kv handoff");
+}
+
+}  // namespace
+
+struct epd_encoder {
+  epd::Encoder impl;
+  epd_encoder(const epd_encoder_desc_t& d, int dev) : impl(d, dev) {}
+};
+
+struct epd_mmcache {
+  epd::DeviceTable t;
+  void* mem = nullptr;
+  int device = 0;
+};
+
+extern "C" {
+
+int32_t epd_abi_version(void) { return EPD_ABI_VERSION; }
+const char* epd_last_error(void) { return g_err.c_str(); }
+
+epd_status_t epd_irp_shard(int64_t patches, int32_t width, int64_t* counts) {
+  // engine.py:55-62
+  if (width < 1) return fail(EPD_ERR_VALUE, "shard width must be >= 1");
+  if (patches < 0) return fail(EPD_ERR_VALUE, "patch count must be non-negative");
+  if (!counts) return fail(EPD_ERR_VALUE, "counts is null");
+  const int64_t base = patches / width, rem = patches % width;
+  for (int32_t k = 0; k < width; ++k) counts[k] = base + (k < rem ? 1 : 0);
+  return EPD_OK;
+}
+
+epd_status_t epd_irp_ranges(int64_t patches, int32_t width, int64_t* first, int64_t* counts) {
+  epd_status_t st = epd_irp_shard(patches, width, counts);
+  if (st != EPD_OK) return st;
+  if (!first) return fail(EPD_ERR_VALUE, "first is null");
+  int64_t acc = 0;
+  for (int32_t k = 0; k < width; ++k) {
+    first[k] = acc;
+    acc += counts[k];
+  }
+  return EPD_OK;
+}
+
+// ------------------------------------------------------------------ encoder
+
+epd_status_t epd_encoder_create(const epd_encoder_desc_t* desc, int32_t device, epd_encoder_t** out) {
+  if (!desc || !out) return fail(EPD_ERR_VALUE, "null argument");
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(EPD_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  auto* enc = new epd_encoder(*desc, device);
+  std::string msg = enc->impl.validate_and_build_schema();
+  if (!msg.empty()) {
+    delete enc;
+    return fail(EPD_ERR_UNSUPPORTED, msg);
+  }
+  *out = enc;
+  return EPD_OK;
+}
+
+void epd_encoder_destroy(epd_encoder_t* enc) { delete enc; }
+
+int32_t epd_encoder_num_weights(const epd_encoder_t* enc) {
+  return enc ? (int32_t)enc->impl.slots.size() : 0;
+}
+
+epd_status_t epd_encoder_weight_info(const epd_encoder_t* enc, int32_t index, const char** name,
+                                     int32_t* ndim, int64_t* shape) {
+  if (!enc || index < 0 || index >= (int32_t)enc->impl.slots.size())
+    return fail(EPD_ERR_VALUE, "weight index out of range");
+  const auto& s = enc->impl.slots[index];
+  if (name) *name = s.name.c_str();
+  if (ndim) *ndim = (int32_t)s.shape.size();
+  if (shape)
+    for (size_t i = 0; i < 4; ++i) shape[i] = i < s.shape.size() ? s.shape[i] : 1;
+  return EPD_OK;
+}
+
+epd_status_t epd_encoder_set_weight(epd_encoder_t* enc, int32_t index, const float* host_values,
+                                    int64_t numel) {
+  if (!enc || index < 0 || index >= (int32_t)enc->impl.slots.size())
+    return fail(EPD_ERR_VALUE, "weight index out of range");
+  if (enc->impl.finalized) return fail(EPD_ERR_RUNTIME, "encoder already finalized");
+  if (!host_values || numel != enc->impl.numel(index))
+    return fail(EPD_ERR_VALUE, "weight " + enc->impl.slots[index].name + ": numel mismatch");
+  auto& s = enc->impl.slots[index];
+  s.host.assign(host_values, host_values + numel);
+  s.set = true;
+  return EPD_OK;
+}
+
+epd_status_t epd_encoder_finalize(epd_encoder_t* enc, void* stream) {
+  if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
+  if (enc->impl.finalized) return fail(EPD_ERR_RUNTIME, "encoder already finalized");
+  cudaSetDevice(enc->impl.dev);
+  std::string err;
+  int rc = enc->impl.finalize(S(stream), err);
+  if (rc) return fail((epd_status_t)rc, err);
+  return EPD_OK;
+}
+
+epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t n, void* out, void* stream) {
+  if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
+  if (n > 0 && (!tiles || !out)) return fail(EPD_ERR_VALUE, "null tile or output buffer");
+  std::string err;
+  int rc = enc->impl.encode(tiles, n, reinterpret_cast<epd::bf16*>(out), S(stream), err);
+  if (rc) return fail((epd_status_t)rc, err);
+  return EPD_OK;
+}
+
+double epd_encoder_flops_per_tile(const epd_encoder_t* enc) { return enc ? enc->impl.flops_per_tile() : 0.0; }
+int32_t epd_encoder_launches(const epd_encoder_t* enc, int32_t n) { return enc ? enc->impl.launches(n) : 0; }
+
+// ------------------------------------------------------------------ cache
+
+epd_status_t epd_hash_records(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
+                              uint64_t* keys, void* scratch, void* stream) {
+  if (n < 0 || rec_bytes < 0 || rec_stride < rec_bytes) return fail(EPD_ERR_VALUE, "hash: bad geometry");
+  if (rec_bytes % 8) return fail(EPD_ERR_VALUE, "hash: record length must be a multiple of 8 bytes");
+  if (n == 0) return EPD_OK;
+  if (!data || !keys || !scratch) return fail(EPD_ERR_VALUE, "hash: null buffer");
+  if (n > 65535) return fail(EPD_ERR_VALUE, "hash: at most 65535 records per call");
+  int rc = epd::hash_records(data, n, (size_t)rec_bytes, (size_t)rec_stride,
+                             reinterpret_cast<unsigned long long*>(scratch),
+                             reinterpret_cast<unsigned long long*>(keys), S(stream));
+  return cuda_status(rc, "hash_records");
+}
+
+epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t** out) {
+  if (!out || capacity < 1) return fail(EPD_ERR_VALUE, "cache capacity must be >= 1");
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) return fail(EPD_ERR_CUDA, "cudaSetDevice failed");
+  unsigned long long slots = 16;
+  while (slots < 2ull * (unsigned long long)capacity) slots <<= 1;
+  auto* c = new epd_mmcache();
+  c->device = device;
+  const size_t bytes = slots * 16 + slots * 4 + 256;
+  cudaError_t e = cudaMalloc(&c->mem, bytes);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(EPD_ERR_CUDA, std::string("cudaMalloc(cache table): ") + cudaGetErrorString(e));
+  }
+  cudaMemset(c->mem, 0, bytes);
+  c->t.capacity = slots;
+  c->t.keys = reinterpret_cast<unsigned long long*>(c->mem);
+  c->t.vals = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->mem) + slots * 16);
+  c->t.status = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->mem) + slots * 20);
+  *out = c;
+  return EPD_OK;
+}
+
+void epd_mmcache_destroy(epd_mmcache_t* cache) {
+  if (!cache) return;
+  if (cache->mem) cudaFree(cache->mem);
+  delete cache;
+}
+
+epd_status_t epd_mmcache_lookup(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, int32_t* entry,
+                                int32_t* dup, void* stream) {
+  if (!cache || n < 0) return fail(EPD_ERR_VALUE, "lookup: bad arguments");
+  if (n == 0) return EPD_OK;
+  auto k = reinterpret_cast<const unsigned long long*>(keys);
+  int rc = epd::table_lookup(cache->t, k, n, entry, S(stream));
+  if (!rc && dup) rc = epd::table_dedup(k, entry, n, dup, S(stream));
+  return cuda_status(rc, "mmcache_lookup");
+}
+
+epd_status_t epd_mmcache_insert(epd_mmcache_t* cache, const uint64_t* keys, const int32_t* entries, int32_t n,
+                                void* stream) {
+  if (!cache || n < 0) return fail(EPD_ERR_VALUE, "insert: bad arguments");
+  if (n == 0) return EPD_OK;
+  int rc = epd::table_insert(cache->t, reinterpret_cast<const unsigned long long*>(keys), entries, n, S(stream));
+  return cuda_status(rc, "mmcache_insert");
+}
+
+epd_status_t epd_mmcache_erase(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, void* stream) {
+  if (!cache || n < 0) return fail(EPD_ERR_VALUE, "erase: bad arguments");
+  if (n == 0) return EPD_OK;
+  int rc = epd::table_erase(cache->t, reinterpret_cast<const unsigned long long*>(keys), n, S(stream));
+  return cuda_status(rc, "mmcache_erase");
+}
+
+epd_status_t epd_mmcache_clear(epd_mmcache_t* cache, void* stream) {
+  if (!cache) return fail(EPD_ERR_VALUE, "clear: null cache");
+  int rc = (int)cudaMemsetAsync(cache->mem, 0, cache->t.capacity * 20 + 256, S(stream));
+  return cuda_status(rc, "mmcache_clear");
+}
+
+epd_status_t epd_mmcache_check(epd_mmcache_t* cache, void* stream) {
+  if (!cache) return fail(EPD_ERR_VALUE, "check: null cache");
+  int32_t st = 0;
+  cudaError_t e = cudaMemcpyAsync(&st, cache->t.status, 4, cudaMemcpyDeviceToHost, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e != cudaSuccess) return cuda_status((int)e, "mmcache_check");
+  if (st) return fail(EPD_ERR_CAPACITY, "multimodal cache table is full");
+  return EPD_OK;
+}
+
+// ------------------------------------------------------------------ packing / handoff
+
+epd_status_t epd_gather_records(const void* src, const int32_t* index, int32_t n, int64_t rec_bytes, void* dst,
+                                void* stream) {
+  if (n < 0 || rec_bytes <= 0) return fail(EPD_ERR_VALUE, "gather: bad geometry");
+  if (n > 65535) return fail(EPD_ERR_VALUE, "gather: at most 65535 records per call");
+  return cuda_status(epd::gather_records(src, index, n, (size_t)rec_bytes, dst, S(stream)), "gather_records");
+}
+
+epd_status_t epd_scatter_records(const void* src, const int32_t* index, int32_t n, int64_t rec_bytes, void* dst,
+                                 void* stream) {
+  if (n < 0 || rec_bytes <= 0) return fail(EPD_ERR_VALUE, "scatter: bad geometry");
+  if (n == 0) return EPD_OK;
+  if (n > 65535) return fail(EPD_ERR_VALUE, "scatter: at most 65535 records per call");
+  if (rec_bytes % 16 || ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15))
+    return fail(EPD_ERR_VALUE, "scatter: records must be 16-byte aligned");
+  const size_t vecs = (size_t)rec_bytes / 16;
+  int bx = (int)((vecs + 255) / 256);
+  if (bx > 64) bx = 64;
+  scatter_records_kernel<<<dim3(bx, n), 256, 0, S(stream)>>>(reinterpret_cast<const uint4*>(src), index, vecs,
+                                                               reinterpret_cast<uint4*>(dst));
+  return cuda_status((int)cudaGetLastError(), "scatter_records");
+}
+
+epd_status_t epd_kv_pack(const void* cache, int32_t segments, int64_t segment_stride, int64_t block_bytes,
+                         const int32_t* block_ids, int32_t nblocks, void* out, void* stream) {
+  return kv_copy(cache, out, segments, segment_stride, block_bytes, block_ids, nblocks, 1, stream);
+}
+
+epd_status_t epd_kv_unpack(const void* in, int32_t segments, int64_t segment_stride, int64_t block_bytes,
+                           const int32_t* block_ids, int32_t nblocks, void* cache, void* stream) {
+  return kv_copy(in, cache, segments, segment_stride, block_bytes, block_ids, nblocks, 0, stream);
+}
+
+// ------------------------------------------------------------------ kernel-level ops
+
+epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
+                             int32_t K, const void* bias, int32_t act, const void* resid, int32_t ldr,
+                             int32_t r_mod, const void* lscale, void* out, int32_t ldo, int32_t bn,
+                             void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return fail(EPD_ERR_VALUE, "linear: empty shape");
+  if (act < 0 || act > 2) return fail(EPD_ERR_VALUE, "linear: unknown activation");
+  if (ldo % 8 || (resid && ldr % 8) || ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(bias) |
+                                          reinterpret_cast<uintptr_t>(resid) | reinterpret_cast<uintptr_t>(lscale)) & 15))
+    return fail(EPD_ERR_VALUE, "linear: epilogue tensors must be 16-byte aligned");
+  epd::EpiParams ep;
+  ep.act = act;
+  ep.bias = reinterpret_cast<const epd::bf16*>(bias);
+  ep.resid = reinterpret_cast<const epd::bf16*>(resid);
+  ep.ldr = ldr;
+  ep.r_mod = r_mod > 0 ? r_mod : 0x7fffffff;
+  ep.lscale = reinterpret_cast<const epd::bf16*>(lscale);
+  ep.out = reinterpret_cast<epd::bf16*>(out);
+  ep.ldo = ldo;
+  int rc = epd::gemm_bf16(reinterpret_cast<const epd::bf16*>(A), lda, reinterpret_cast<const epd::bf16*>(W), ldw,
+                          M, N, K, ep, S(stream), bn);
+  return cuda_status(rc, "linear_bf16");
+}
+
+epd_status_t epd_attention_bf16(const void* q, const void* k, const void* vt, void* out, int32_t B, int32_t H,
+                                int32_t Tq, int32_t Tk, int32_t Tkpad, int32_t Dp, int32_t Dv, int32_t ldo,
+                                int32_t q_shared, float scale, void* stream) {
+  epd::AttnParams p;
+  p.q = reinterpret_cast<const epd::bf16*>(q);
+  p.k = reinterpret_cast<const epd::bf16*>(k);
+  p.vt = reinterpret_cast<const epd::bf16*>(vt);
+  p.out = reinterpret_cast<epd::bf16*>(out);
+  p.B = B; p.H = H; p.Tq = Tq; p.Tk = Tk; p.Tkpad = Tkpad; p.Dp = Dp; p.Dv = Dv; p.ldo = ldo;
+  p.q_shared = q_shared;
+  p.scale = scale;
+  return cuda_status(epd::attention_bf16(p, S(stream)), "attention_bf16");
+}
+
+epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
+                                const void* beta, int32_t rows, int32_t D, float eps, void* stream) {
+  return cuda_status(epd::layernorm_bf16(reinterpret_cast<const epd::bf16*>(in), ld_in,
+                                         reinterpret_cast<epd::bf16*>(out), ld_out,
+                                         reinterpret_cast<const epd::bf16*>(gamma),
+                                         reinterpret_cast<const epd::bf16*>(beta), rows, D, eps, S(stream)),
+                     "layernorm_bf16");
+}
+
+epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t Sz, int32_t C, int32_t p, int32_t Kpad,
+                             int32_t row_offset, int32_t rows_per_tile, const float* mean3, const float* std3,
+                             void* out, void* stream) {
+  if (!mean3 || !std3) return fail(EPD_ERR_VALUE, "patchify: null mean/std");
+  return cuda_status(epd::patchify_u8(tiles, n, Sz, C, p, Kpad, row_offset, rows_per_tile, mean3, std3,
+                                      reinterpret_cast<epd::bf16*>(out), S(stream)),
+                     "patchify_u8");
+}
+
+}  // extern "C"

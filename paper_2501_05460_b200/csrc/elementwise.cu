@@ -1,0 +1,192 @@
+// HBM-bound kernels: LayerNorm (warp per row, vectorised 16 B accesses,
+// shuffle reductions), patchify (uint8 HWC tiles -> normalised bf16 im2col
+// rows for the conv-as-GEMM patch embedding), record gather (MM-token
+// packing) and the pixel-shuffle gather used by the InternVL projector.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace epd {
+
+namespace {
+
+// One warp per row; each lane holds up to MAXV 8-element vectors in registers.
+// Optional row gather: logical row o = concat over seg of src rows
+// gidx[o*segs + seg] (each D/segs wide) -- fuses the InternVL pixel shuffle.
+template <int MAXV>
+__global__ void __launch_bounds__(256) layernorm_kernel(const bf16* __restrict__ in, int ld_in,
+                                                        bf16* __restrict__ out, int ld_out,
+                                                        const bf16* __restrict__ gamma,
+                                                        const bf16* __restrict__ beta, int rows,
+                                                        int D, float eps,
+                                                        const int32_t* __restrict__ gidx, int segs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (row >= rows) return;
+  const int nvec = D >> 3;
+  const int seg_vec = gidx ? nvec / segs : nvec;
+  float x[MAXV][8];
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int v = lane + i * 32;
+    if (v < nvec) {
+      const bf16* src;
+      if (gidx) {
+        const int seg = v / seg_vec;
+        src = in + (size_t)gidx[(size_t)row * segs + seg] * ld_in + (v - seg * seg_vec) * 8;
+      } else {
+        src = in + (size_t)row * ld_in + v * 8;
+      }
+      uint4 u = *reinterpret_cast<const uint4*>(src);
+      float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z),
+             d = unpack_bf16x2(u.w);
+      x[i][0] = a.x; x[i][1] = a.y; x[i][2] = b.x; x[i][3] = b.y;
+      x[i][4] = c.x; x[i][5] = c.y; x[i][6] = d.x; x[i][7] = d.y;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum += x[i][j];
+    }
+  }
+  const float mean = warp_sum(sum) / (float)D;
+  float var = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int v = lane + i * 32;
+    if (v < nvec) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float t = x[i][j] - mean;
+        var += t * t;
+      }
+    }
+  }
+  const float rstd = rsqrtf(warp_sum(var) / (float)D + eps);
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int v = lane + i * 32;
+    if (v < nvec) {
+      float g[8], bb[8];
+      uint4 ug = *reinterpret_cast<const uint4*>(gamma + v * 8);
+      uint4 ub = *reinterpret_cast<const uint4*>(beta + v * 8);
+      float2 t;
+      t = unpack_bf16x2(ug.x); g[0] = t.x; g[1] = t.y;
+      t = unpack_bf16x2(ug.y); g[2] = t.x; g[3] = t.y;
+      t = unpack_bf16x2(ug.z); g[4] = t.x; g[5] = t.y;
+      t = unpack_bf16x2(ug.w); g[6] = t.x; g[7] = t.y;
+      t = unpack_bf16x2(ub.x); bb[0] = t.x; bb[1] = t.y;
+      t = unpack_bf16x2(ub.y); bb[2] = t.x; bb[3] = t.y;
+      t = unpack_bf16x2(ub.z); bb[4] = t.x; bb[5] = t.y;
+      t = unpack_bf16x2(ub.w); bb[6] = t.x; bb[7] = t.y;
+      float y[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) y[j] = (x[i][j] - mean) * rstd * g[j] + bb[j];
+      uint4 o;
+      o.x = pack_bf16x2(y[0], y[1]);
+      o.y = pack_bf16x2(y[2], y[3]);
+      o.z = pack_bf16x2(y[4], y[5]);
+      o.w = pack_bf16x2(y[6], y[7]);
+      *reinterpret_cast<uint4*>(out + (size_t)row * ld_out + v * 8) = o;
+    }
+  }
+}
+
+// One block per (tile, patch row). Stage p image rows in smem, then emit
+// S/p patches x Kpad columns in (c, ky, kx) order.
+__global__ void patchify_kernel(const uint8_t* __restrict__ tiles, int S, int C, int p, int Kpad,
+                                int row_offset, int rows_per_tile, float m0, float m1, float m2,
+                                float s0, float s1, float s2, bf16* __restrict__ out) {
+  extern __shared__ uint8_t strip[];  // p * S * C bytes
+  const int tile = blockIdx.y;
+  const int py = blockIdx.x;
+  const int np = S / p;
+  const size_t strip_bytes = (size_t)p * S * C;
+  const uint8_t* src = tiles + (size_t)tile * S * S * C + (size_t)py * strip_bytes;
+  for (size_t i = threadIdx.x * 16; i < strip_bytes; i += blockDim.x * 16) {
+    if (i + 16 <= strip_bytes && ((reinterpret_cast<uintptr_t>(src + i) & 15) == 0))
+      *reinterpret_cast<uint4*>(strip + i) = *reinterpret_cast<const uint4*>(src + i);
+    else
+      for (size_t j = i; j < i + 16 && j < strip_bytes; ++j) strip[j] = src[j];
+  }
+  __syncthreads();
+  const float mean[3] = {m0, m1, m2};
+  const float inv[3] = {1.f / s0, 1.f / s1, 1.f / s2};
+  const int kreal = C * p * p;
+  const int total = np * Kpad;
+  bf16* dst = out + ((size_t)tile * rows_per_tile + row_offset + (size_t)py * np) * Kpad;
+  for (int o = threadIdx.x; o < total; o += blockDim.x) {
+    const int px = o / Kpad;
+    const int col = o - px * Kpad;
+    float v = 0.f;
+    if (col < kreal) {
+      const int c = col / (p * p);
+      const int r = col - c * p * p;
+      const int ky = r / p, kx = r - ky * p;
+      const float u = (float)strip[((size_t)ky * S + px * p + kx) * C + c];
+      v = (u * (1.f / 255.f) - mean[c]) * inv[c];
+    }
+    dst[o] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void gather_records_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ index,
+                                      int n, size_t vecs, uint4* __restrict__ dst) {
+  const int rec = blockIdx.y;
+  const uint4* s = src + (size_t)index[rec] * vecs;
+  uint4* d = dst + (size_t)rec * vecs;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < vecs;
+       i += (size_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+}
+
+}  // namespace
+
+int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                          const bf16* beta, int rows, int D, float eps, const int32_t* gidx,
+                          int segs, cudaStream_t stream) {
+  if (rows <= 0) return 0;
+  if (D % 8 || ld_in % 8 || ld_out % 8) return 1002;
+  const int nvec = D / 8;
+  const dim3 block(256);
+  const dim3 grid((rows + 7) / 8);
+  if (nvec <= 32 * 5)
+    layernorm_kernel<5><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
+  else if (nvec <= 32 * 16)
+    layernorm_kernel<16><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
+  else
+    return 1004;
+  return (int)cudaGetLastError();
+}
+
+int layernorm_bf16(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                   const bf16* beta, int rows, int D, float eps, cudaStream_t stream) {
+  return layernorm_bf16_gather(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, nullptr, 1, stream);
+}
+
+int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int row_offset,
+                int rows_per_tile, const float* mean, const float* stdv, bf16* out,
+                cudaStream_t stream) {
+  if (n <= 0) return 0;
+  if (S % p || C > 3 || Kpad < C * p * p) return 1002;
+  const size_t smem = (size_t)p * S * C;
+  dim3 grid(S / p, n);
+  patchify_kernel<<<grid, 256, smem, stream>>>(tiles, S, C, p, Kpad, row_offset, rows_per_tile,
+                                               mean[0], C > 1 ? mean[1] : 0.f, C > 2 ? mean[2] : 0.f,
+                                               stdv[0], C > 1 ? stdv[1] : 1.f, C > 2 ? stdv[2] : 1.f,
+                                               out);
+  return (int)cudaGetLastError();
+}
+
+int gather_records(const void* src_base, const int32_t* index, int n, size_t bytes, void* dst,
+                   cudaStream_t stream) {
+  if (n <= 0) return 0;
+  if (bytes % 16 || (reinterpret_cast<uintptr_t>(src_base) | reinterpret_cast<uintptr_t>(dst)) & 15)
+    return 1002;
+  const size_t vecs = bytes / 16;
+  int bx = (int)((vecs + 255) / 256);
+  if (bx > 64) bx = 64;
+  dim3 grid(bx, n);
+  gather_records_kernel<<<grid, 256, 0, stream>>>(reinterpret_cast<const uint4*>(src_base), index, n,
+                                                  vecs, reinterpret_cast<uint4*>(dst));
+  return (int)cudaGetLastError();
+}
+
+}  // namespace epd

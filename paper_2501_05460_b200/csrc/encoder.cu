@@ -1,0 +1,625 @@
+// Vision encoder + resampler/projector executor (host C++ driving the sm_100a
+// kernels). Owns the bf16 weights in the B200 layout and the activation
+// workspace; one instance per GPU process.
+//
+// Families (public model definitions restated in oracle/encoders.py):
+//   1  MiniCPM-V 2.6: SigLIP-so400m ViT (pre-LN, GELU-tanh, post-LN)
+//      + perceiver resampler (kv_proj, ln_kv, 64 learned queries, MHA with
+//        2-D sincos key positions, ln_post, proj)
+//   2  InternVL2: InternViT-300M (CLS token, layer scale, GELU-erf, no post-LN)
+//      + pixel shuffle 0.5 + mlp1 (LN, Linear, GELU, Linear)
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "encoder.h"
+#include "kernels.h"
+#include "tmap.h"
+
+namespace epd {
+
+namespace {
+
+uint16_t f2bf(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace
+
+Encoder::Encoder(const epd_encoder_desc_t& desc, int device) : d(desc), dev(device) {}
+
+Encoder::~Encoder() {
+  if (blob) cudaFree(blob);
+  if (work) cudaFree(work);
+}
+
+int Encoder::add(const std::string& name, std::vector<int64_t> shape) {
+  WeightSlot s;
+  s.name = name;
+  s.shape = std::move(shape);
+  slots.push_back(std::move(s));
+  return (int)slots.size() - 1;
+}
+
+int64_t Encoder::numel(int i) const {
+  int64_t n = 1;
+  for (auto v : slots[i].shape) n *= v;
+  return n;
+}
+
+std::string Encoder::validate_and_build_schema() {
+  const auto& x = d;
+  if (x.family != EPD_FAMILY_SIGLIP_RESAMPLER && x.family != EPD_FAMILY_INTERNVIT_MLP)
+    return "unknown encoder family";
+  if (x.image_size <= 0 || x.patch_size <= 0 || x.image_size % x.patch_size)
+    return "image_size must be a positive multiple of patch_size";
+  if (x.channels < 1 || x.channels > 3) return "channels must be 1..3";
+  if (x.hidden <= 0 || x.heads <= 0 || x.hidden % x.heads) return "hidden must divide into heads";
+  if (x.hidden % 8 || x.mlp % 8 || x.out_dim % 8) return "hidden, mlp and out_dim must be multiples of 8";
+  if (x.layers < 0 || x.max_tiles <= 0) return "layers >= 0 and max_tiles > 0 required";
+  grid = x.image_size / x.patch_size;
+  npatch = grid * grid;
+  D = x.hidden;
+  H = x.heads;
+  dh = D / H;
+  Dp = dh <= 64 ? 64 : (dh <= 80 ? 80 : (dh <= 128 ? 128 : 0));
+  if (!Dp) return "head_dim > 128 is not supported";
+  if (dh % 8) return "head_dim must be a multiple of 8";
+  Kreal = x.channels * x.patch_size * x.patch_size;
+  Kpad = (Kreal + 63) / 64 * 64;
+  F = x.mlp;
+  if (x.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    T = npatch;
+    E = x.out_dim;
+    Q = x.out_tokens;
+    if (x.out_heads <= 0 || E % x.out_heads) return "out_dim must divide into out_heads";
+    RH = x.out_heads;
+    rdh = E / RH;
+    RDp = rdh <= 64 ? 64 : (rdh <= 80 ? 80 : (rdh <= 128 ? 128 : 0));
+    if (!RDp || rdh % 8) return "resampler head_dim must be a multiple of 8 and <= 128";
+  } else {
+    T = npatch + 1;
+    E = x.out_dim;
+    if (grid % 2) return "pixel shuffle needs an even patch grid";
+    Q = npatch / 4;
+    if (x.out_tokens != Q) return "InternVL out_tokens must equal (grid/2)^2";
+  }
+  Tpad = (T + 7) / 8 * 8;
+
+  const int L = x.layers;
+  w_pe = add("patch_embed.weight", {D, x.channels, x.patch_size, x.patch_size});
+  b_pe = add("patch_embed.bias", {D});
+  if (x.family == EPD_FAMILY_INTERNVIT_MLP) w_cls = add("cls_token", {D});
+  w_pos = add("pos_embed", {T, D});
+  for (int l = 0; l < L; ++l) {
+    LayerSlots ls;
+    const std::string p = "layers." + std::to_string(l) + ".";
+    ls.ln1w = add(p + "ln1.weight", {D});
+    ls.ln1b = add(p + "ln1.bias", {D});
+    if (x.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+      ls.qw = add(p + "attn.q.weight", {D, D});
+      ls.qb = add(p + "attn.q.bias", {D});
+      ls.kw = add(p + "attn.k.weight", {D, D});
+      ls.kb = add(p + "attn.k.bias", {D});
+      ls.vw = add(p + "attn.v.weight", {D, D});
+      ls.vb = add(p + "attn.v.bias", {D});
+    } else {
+      ls.qw = add(p + "attn.qkv.weight", {3 * D, D});
+      ls.qb = add(p + "attn.qkv.bias", {3 * D});
+    }
+    ls.ow = add(p + "attn.o.weight", {D, D});
+    ls.ob = add(p + "attn.o.bias", {D});
+    if (x.family == EPD_FAMILY_INTERNVIT_MLP) ls.ls1 = add(p + "ls1", {D});
+    ls.ln2w = add(p + "ln2.weight", {D});
+    ls.ln2b = add(p + "ln2.bias", {D});
+    ls.f1w = add(p + "mlp.fc1.weight", {F, D});
+    ls.f1b = add(p + "mlp.fc1.bias", {F});
+    ls.f2w = add(p + "mlp.fc2.weight", {D, F});
+    ls.f2b = add(p + "mlp.fc2.bias", {D});
+    if (x.family == EPD_FAMILY_INTERNVIT_MLP) ls.ls2 = add(p + "ls2", {D});
+    lslots.push_back(ls);
+  }
+  if (x.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    w_post_w = add("post_ln.weight", {D});
+    w_post_b = add("post_ln.bias", {D});
+    r_query = add("rs.query", {Q, E});
+    r_kv = add("rs.kv_proj.weight", {E, D});
+    r_lnq_w = add("rs.ln_q.weight", {E});
+    r_lnq_b = add("rs.ln_q.bias", {E});
+    r_lnkv_w = add("rs.ln_kv.weight", {E});
+    r_lnkv_b = add("rs.ln_kv.bias", {E});
+    r_qw = add("rs.attn.q.weight", {E, E});
+    r_qb = add("rs.attn.q.bias", {E});
+    r_kw = add("rs.attn.k.weight", {E, E});
+    r_kb = add("rs.attn.k.bias", {E});
+    r_vw = add("rs.attn.v.weight", {E, E});
+    r_vb = add("rs.attn.v.bias", {E});
+    r_ow = add("rs.attn.o.weight", {E, E});
+    r_ob = add("rs.attn.o.bias", {E});
+    r_lnp_w = add("rs.ln_post.weight", {E});
+    r_lnp_b = add("rs.ln_post.bias", {E});
+    r_proj = add("rs.proj", {E, E});
+    r_pos = add("rs.pos_embed", {T, E});
+  } else {
+    const int C4 = 4 * D;
+    m_ln_w = add("mlp1.ln.weight", {C4});
+    m_ln_b = add("mlp1.ln.bias", {C4});
+    m_f1w = add("mlp1.fc1.weight", {E, C4});
+    m_f1b = add("mlp1.fc1.bias", {E});
+    m_f2w = add("mlp1.fc2.weight", {E, E});
+    m_f2b = add("mlp1.fc2.bias", {E});
+  }
+  return "";
+}
+
+const float* Encoder::host(int i) const { return slots[i].host.data(); }
+
+// ------------------------------------------------------------ finalize
+
+namespace {
+
+struct Arena {
+  uint8_t* base = nullptr;
+  size_t off = 0, cap = 0;
+  void* take(size_t bytes) {
+    void* p = base + off;
+    off += align256(bytes);
+    return p;
+  }
+};
+
+}  // namespace
+
+int Encoder::finalize(cudaStream_t stream, std::string& err) {
+  for (size_t i = 0; i < slots.size(); ++i)
+    if (!slots[i].set) {
+      err = "weight not set: " + slots[i].name;
+      return EPD_ERR_VALUE;
+    }
+  // ---- build the bf16 device images on the host (B200 layouts)
+  std::vector<std::pair<bf16**, std::vector<uint16_t>>> images;
+  auto plain = [&](bf16** dst, int slot) {
+    std::vector<uint16_t> v(numel(slot));
+    const float* h = host(slot);
+    for (size_t i = 0; i < v.size(); ++i) v[i] = f2bf(h[i]);
+    images.emplace_back(dst, std::move(v));
+  };
+  auto transposed = [&](bf16** dst, int slot, int rows, int cols) {  // out[c][r] = in[r][c]
+    std::vector<uint16_t> v((size_t)rows * cols);
+    const float* h = host(slot);
+    for (int r = 0; r < rows; ++r)
+      for (int c = 0; c < cols; ++c) v[(size_t)c * rows + r] = f2bf(h[(size_t)r * cols + c]);
+    images.emplace_back(dst, std::move(v));
+  };
+  // head-padded projection rows: sections s (source slot, row offset), heads nh of dim hd -> pad hp
+  auto headpad_w = [&](bf16** dst, const std::vector<std::pair<int, int>>& secs, int nh, int hd, int hp,
+                       int K) {
+    std::vector<uint16_t> v((size_t)secs.size() * nh * hp * K, 0);
+    for (size_t s = 0; s < secs.size(); ++s) {
+      const float* h = host(secs[s].first) + (size_t)secs[s].second * K;
+      for (int hh = 0; hh < nh; ++hh)
+        for (int dd = 0; dd < hd; ++dd) {
+          const float* src = h + (size_t)(hh * hd + dd) * K;
+          uint16_t* o = v.data() + ((s * nh + hh) * (size_t)hp + dd) * K;
+          for (int k = 0; k < K; ++k) o[k] = f2bf(src[k]);
+        }
+    }
+    images.emplace_back(dst, std::move(v));
+  };
+  auto headpad_b = [&](bf16** dst, const std::vector<std::pair<int, int>>& secs, int nh, int hd, int hp) {
+    std::vector<uint16_t> v((size_t)secs.size() * nh * hp, 0);
+    for (size_t s = 0; s < secs.size(); ++s) {
+      const float* h = host(secs[s].first) + secs[s].second;
+      for (int hh = 0; hh < nh; ++hh)
+        for (int dd = 0; dd < hd; ++dd) v[(s * nh + hh) * hp + dd] = f2bf(h[hh * hd + dd]);
+    }
+    images.emplace_back(dst, std::move(v));
+  };
+
+  // patch embedding [D][C*p*p] padded to Kpad columns
+  {
+    std::vector<uint16_t> v((size_t)D * Kpad, 0);
+    const float* h = host(w_pe);
+    for (int r = 0; r < D; ++r)
+      for (int k = 0; k < Kreal; ++k) v[(size_t)r * Kpad + k] = f2bf(h[(size_t)r * Kreal + k]);
+    images.emplace_back(&dw.pe, std::move(v));
+  }
+  plain(&dw.pe_b, b_pe);
+  {
+    // additive table applied in the patch-embed epilogue as resid[row % T]:
+    // rows carry the position embedding; InternViT's CLS row (whose patch row
+    // is zero, so the GEMM yields just the bias) carries cls + pos0 - bias.
+    std::vector<float> pos(host(w_pos), host(w_pos) + (size_t)T * D);
+    if (d.family == EPD_FAMILY_INTERNVIT_MLP)
+      for (int c = 0; c < D; ++c) pos[c] += host(w_cls)[c] - host(b_pe)[c];
+    std::vector<uint16_t> v(pos.size());
+    for (size_t i = 0; i < pos.size(); ++i) v[i] = f2bf(pos[i]);
+    images.emplace_back(&dw.pos, std::move(v));
+  }
+  dl.resize(lslots.size());
+  for (size_t l = 0; l < lslots.size(); ++l) {
+    const auto& s = lslots[l];
+    auto& o = dl[l];
+    plain(&o.ln1w, s.ln1w);
+    plain(&o.ln1b, s.ln1b);
+    if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+      headpad_w(&o.qkv, {{s.qw, 0}, {s.kw, 0}, {s.vw, 0}}, H, dh, Dp, D);
+      headpad_b(&o.qkvb, {{s.qb, 0}, {s.kb, 0}, {s.vb, 0}}, H, dh, Dp);
+    } else {
+      headpad_w(&o.qkv, {{s.qw, 0}, {s.qw, D}, {s.qw, 2 * D}}, H, dh, Dp, D);
+      headpad_b(&o.qkvb, {{s.qb, 0}, {s.qb, D}, {s.qb, 2 * D}}, H, dh, Dp);
+    }
+    plain(&o.ow, s.ow);
+    plain(&o.ob, s.ob);
+    plain(&o.ln2w, s.ln2w);
+    plain(&o.ln2b, s.ln2b);
+    plain(&o.f1w, s.f1w);
+    plain(&o.f1b, s.f1b);
+    plain(&o.f2w, s.f2w);
+    plain(&o.f2b, s.f2b);
+    if (d.family == EPD_FAMILY_INTERNVIT_MLP) {
+      plain(&o.ls1, s.ls1);
+      plain(&o.ls2, s.ls2);
+    }
+  }
+  bf16 *rs_query = nullptr, *rs_lnq_w = nullptr, *rs_lnq_b = nullptr, *rs_qw = nullptr, *rs_qb = nullptr,
+       *rs_kw = nullptr, *rs_pos = nullptr;
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    plain(&dw.post_w, w_post_w);
+    plain(&dw.post_b, w_post_b);
+    plain(&dw.r_kv, r_kv);
+    plain(&dw.r_lnkv_w, r_lnkv_w);
+    plain(&dw.r_lnkv_b, r_lnkv_b);
+    headpad_w(&dw.r_kvin, {{r_kw, 0}, {r_vw, 0}}, RH, rdh, RDp, E);
+    headpad_b(&dw.r_kvin_b, {{r_kb, 0}, {r_vb, 0}}, RH, rdh, RDp);
+    plain(&dw.r_ow, r_ow);
+    plain(&dw.r_ob, r_ob);
+    plain(&dw.r_lnp_w, r_lnp_w);
+    plain(&dw.r_lnp_b, r_lnp_b);
+    transposed(&dw.r_projT, r_proj, E, E);
+    // inputs for the weight-only precomputations below
+    plain(&rs_query, r_query);
+    plain(&rs_lnq_w, r_lnq_w);
+    plain(&rs_lnq_b, r_lnq_b);
+    headpad_w(&rs_qw, {{r_qw, 0}}, RH, rdh, RDp, E);
+    headpad_b(&rs_qb, {{r_qb, 0}}, RH, rdh, RDp);
+    headpad_w(&rs_kw, {{r_kw, 0}}, RH, rdh, RDp, E);
+    plain(&rs_pos, r_pos);
+  } else {
+    plain(&dw.m_ln_w, m_ln_w);
+    plain(&dw.m_ln_b, m_ln_b);
+    plain(&dw.m_f1w, m_f1w);
+    plain(&dw.m_f1b, m_f1b);
+    plain(&dw.m_f2w, m_f2w);
+    plain(&dw.m_f2b, m_f2b);
+  }
+
+  // ---- derived device tensors and workspace sizes
+  const size_t nt = d.max_tiles;
+  const size_t M = nt * T;
+  size_t derived = 0;
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    derived += align256((size_t)RH * Q * RDp * 2);            // q heads
+    derived += align256((size_t)T * 2 * RH * RDp * 2);        // pos_k table
+  } else {
+    derived += align256(nt * Q * 4 * sizeof(int32_t));        // pixel-shuffle gather index
+  }
+  size_t wbytes = derived;
+  for (auto& im : images) wbytes += align256(im.second.size() * 2);
+  cudaError_t e = cudaMalloc(&blob, wbytes);
+  if (e != cudaSuccess) {
+    err = std::string("cudaMalloc(weights): ") + cudaGetErrorString(e);
+    return EPD_ERR_CUDA;
+  }
+  Arena a{reinterpret_cast<uint8_t*>(blob), 0, wbytes};
+  for (auto& im : images) {
+    void* p = a.take(im.second.size() * 2);
+    e = cudaMemcpy(p, im.second.data(), im.second.size() * 2, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      err = std::string("cudaMemcpy(weights): ") + cudaGetErrorString(e);
+      return EPD_ERR_CUDA;
+    }
+    *im.first = reinterpret_cast<bf16*>(p);
+  }
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    dw.r_qheads = reinterpret_cast<bf16*>(a.take((size_t)RH * Q * RDp * 2));
+    dw.r_posk = reinterpret_cast<bf16*>(a.take((size_t)T * 2 * RH * RDp * 2));
+  } else {
+    dw.ps_idx = reinterpret_cast<int32_t*>(a.take(nt * Q * 4 * sizeof(int32_t)));
+    // InternVL pixel_shuffle(0.5), ps_version v2, after dropping CLS:
+    // out token (a2, b2), channel segment s <- patch (2*a2 + s/2, 2*b2 + s%2)
+    std::vector<int32_t> idx(nt * Q * 4);
+    const int g2 = grid / 2;
+    for (size_t t = 0; t < nt; ++t)
+      for (int a2 = 0; a2 < g2; ++a2)
+        for (int b2 = 0; b2 < g2; ++b2)
+          for (int s = 0; s < 4; ++s) {
+            const int pa = 2 * a2 + s / 2, pb = 2 * b2 + s % 2;
+            idx[((t * Q) + a2 * g2 + b2) * 4 + s] = (int32_t)(t * T + 1 + pa * grid + pb);
+          }
+    cudaMemcpy(dw.ps_idx, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  }
+
+  // workspace
+  size_t wsz = 0;
+  auto plan = [&](size_t bytes) {
+    size_t o = wsz;
+    wsz += align256(bytes);
+    return o;
+  };
+  const size_t o_xp = plan(M * Kpad * 2);
+  const size_t o_h = plan(M * D * 2);
+  const size_t o_xn = plan(M * D * 2);
+  const size_t o_ao = plan(M * D * 2);
+  const size_t o_q = plan(nt * H * T * Dp * 2);
+  const size_t o_k = plan(nt * H * T * Dp * 2);
+  const size_t o_vt = plan(nt * H * Dp * Tpad * 2);
+  size_t big = M * F * 2;
+  size_t o_r1 = 0, o_r2 = 0, o_rk = 0, o_rvt = 0, o_rao = 0, o_rr = 0;
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    big = std::max(big, M * (size_t)E * 2);
+  }
+  const size_t o_f = plan(big);
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    o_r2 = plan(M * (size_t)E * 2);  // ln_kv output
+    o_rk = plan(nt * RH * T * RDp * 2);
+    o_rvt = plan(nt * RH * RDp * Tpad * 2);
+    o_rao = plan(nt * Q * (size_t)E * 2);
+    o_rr = plan(nt * Q * (size_t)E * 2);
+    o_r1 = o_f;  // kv_proj output reuses the MLP buffer
+  } else {
+    o_r2 = plan(nt * Q * (size_t)4 * D * 2);  // shuffled + LN rows
+    o_rr = plan(nt * Q * (size_t)E * 2);      // fc1 output
+  }
+  e = cudaMalloc(&work, wsz);
+  if (e != cudaSuccess) {
+    err = std::string("cudaMalloc(workspace): ") + cudaGetErrorString(e);
+    return EPD_ERR_CUDA;
+  }
+  uint8_t* wb = reinterpret_cast<uint8_t*>(work);
+  ws.xp = reinterpret_cast<bf16*>(wb + o_xp);
+  ws.h = reinterpret_cast<bf16*>(wb + o_h);
+  ws.xn = reinterpret_cast<bf16*>(wb + o_xn);
+  ws.ao = reinterpret_cast<bf16*>(wb + o_ao);
+  ws.q = reinterpret_cast<bf16*>(wb + o_q);
+  ws.k = reinterpret_cast<bf16*>(wb + o_k);
+  ws.vt = reinterpret_cast<bf16*>(wb + o_vt);
+  ws.f = reinterpret_cast<bf16*>(wb + o_f);
+  ws.r1 = reinterpret_cast<bf16*>(wb + o_r1);
+  ws.r2 = reinterpret_cast<bf16*>(wb + o_r2);
+  ws.rk = reinterpret_cast<bf16*>(wb + o_rk);
+  ws.rvt = reinterpret_cast<bf16*>(wb + o_rvt);
+  ws.rao = reinterpret_cast<bf16*>(wb + o_rao);
+  ws.rr = reinterpret_cast<bf16*>(wb + o_rr);
+  // Padded head dims / key padding are read by the attention TMA and must be finite.
+  cudaMemsetAsync(work, 0, wsz, stream);
+
+  // ---- weight-only precomputation (resampler queries and key positions)
+  int rc = 0;
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    // temporaries live in the (not yet used) MLP buffer
+    bf16* qn = ws.f;
+    rc = layernorm_bf16(rs_query, E, qn, E, rs_lnq_w, rs_lnq_b, Q, E, 1e-6f, stream);
+    if (!rc) {
+      EpiParams ep;
+      ep.mode = EPI_HEADS;
+      ep.bias = rs_qb;
+      ep.H = RH; ep.Dp = RDp; ep.T = Q; ep.Tpad = Q; ep.sec_cols = RH * RDp;
+      ep.sec_out[0] = dw.r_qheads;
+      rc = gemm_bf16(qn, E, rs_qw, E, Q, RH * RDp, E, ep, stream);
+    }
+    if (!rc) {
+      // pos_k[t][0:RH*RDp] = pos[t] @ Wk^T (head padded); second half (V section) = 0
+      cudaMemsetAsync(dw.r_posk, 0, (size_t)T * 2 * RH * RDp * 2, stream);
+      EpiParams ep;
+      ep.out = dw.r_posk;
+      ep.ldo = 2 * RH * RDp;
+      rc = gemm_bf16(rs_pos, E, rs_kw, E, T, RH * RDp, E, ep, stream);
+    }
+  }
+  if (!rc) rc = (int)cudaStreamSynchronize(stream);
+  if (rc) {
+    err = "finalize precompute failed (code " + std::to_string(rc) + "): " +
+          (rc < 1000 ? cudaGetErrorString((cudaError_t)rc) : "argument");
+    return EPD_ERR_CUDA;
+  }
+  for (auto& s : slots) std::vector<float>().swap(s.host);
+  finalized = true;
+  return EPD_OK;
+}
+
+// ------------------------------------------------------------ forward
+
+int Encoder::launches(int n) const {
+  if (n <= 0) return 0;
+  const int chunks = (n + d.max_tiles - 1) / d.max_tiles;
+  int per = 1 /*patchify*/ + 1 /*patch GEMM*/ + 7 * d.layers;
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER)
+    per += 1 /*post LN*/ + 1 /*kv_proj*/ + 1 /*ln_kv*/ + 1 /*kv in-proj*/ + 1 /*attn*/ + 1 /*o*/ +
+           1 /*ln_post*/ + 1 /*proj*/;
+  else
+    per += 1 /*memset CLS rows*/ + 1 /*shuffle+LN*/ + 2 /*fc1, fc2*/;
+  return chunks * per;
+}
+
+double Encoder::flops_per_tile() const {
+  const double t = npatch, Dd = D, Ff = F;
+  double f = 2.0 * npatch * Kreal * Dd;  // patch embedding
+  const double tt = T;
+  const double layer = 2.0 * tt * Dd * 3 * Dd + 2.0 * 2.0 * tt * tt * Dd + 2.0 * tt * Dd * Dd +
+                       2.0 * 2.0 * tt * Dd * Ff;
+  f += d.layers * layer;
+  const double Ee = E, Qq = Q;
+  if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    f += 2.0 * t * Dd * Ee;             // kv_proj
+    f += 2.0 * 2.0 * t * Ee * Ee;       // k, v in-projections
+    f += 2.0 * Qq * Ee * Ee;            // q in-projection (weight-only; precomputed once here)
+    f += 2.0 * 2.0 * Qq * t * Ee;       // cross attention
+    f += 2.0 * 2.0 * Qq * Ee * Ee;      // out-proj + proj
+  } else {
+    f += 2.0 * Qq * 4 * Dd * Ee + 2.0 * Qq * Ee * Ee;  // mlp1
+  }
+  return f;
+}
+
+int Encoder::encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std::string& err) {
+  if (!finalized) {
+    err = "encoder not finalized";
+    return EPD_ERR_RUNTIME;
+  }
+  if (n < 0) {
+    err = "tile count must be non-negative";
+    return EPD_ERR_VALUE;
+  }
+  const size_t tile_bytes = (size_t)d.image_size * d.image_size * d.channels;
+  for (int c0 = 0; c0 < n; c0 += d.max_tiles) {
+    const int nt = std::min(d.max_tiles, n - c0);
+    int rc = forward_chunk(tiles + (size_t)c0 * tile_bytes, nt, out + (size_t)c0 * Q * E, s);
+    if (rc) {
+      err = "kernel launch failed (code " + std::to_string(rc) + "): " +
+            (rc < 1000 ? cudaGetErrorString((cudaError_t)rc) : "argument/shape");
+      return EPD_ERR_CUDA;
+    }
+  }
+  return EPD_OK;
+}
+
+#define EPD_TRY(x)            \
+  do {                        \
+    int _rc = (x);            \
+    if (_rc) return _rc;      \
+  } while (0)
+
+int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s) {
+  const int M = nt * T;
+  const float eps = d.ln_eps;
+  const bool internvl = d.family == EPD_FAMILY_INTERNVIT_MLP;
+  // 1. patchify (+ zero CLS rows) and patch-embedding GEMM (+bias +pos)
+  if (internvl)
+    EPD_TRY((int)cudaMemsetAsync(ws.xp, 0, (size_t)M * Kpad * 2, s));
+  EPD_TRY(patchify_u8(tiles, nt, d.image_size, d.channels, d.patch_size, Kpad, internvl ? 1 : 0, T,
+                      d.mean, d.std, ws.xp, s));
+  {
+    EpiParams ep;
+    ep.bias = dw.pe_b;
+    ep.resid = dw.pos;
+    ep.ldr = D;
+    ep.r_mod = T;
+    ep.out = ws.h;
+    ep.ldo = D;
+    EPD_TRY(gemm_bf16(ws.xp, Kpad, dw.pe, Kpad, M, D, Kpad, ep, s));
+  }
+  // 2. transformer blocks
+  const int act = internvl ? ACT_GELU_ERF : ACT_GELU_TANH;
+  for (size_t l = 0; l < dl.size(); ++l) {
+    const auto& w = dl[l];
+    EPD_TRY(layernorm_bf16(ws.h, D, ws.xn, D, w.ln1w, w.ln1b, M, D, eps, s));
+    {
+      EpiParams ep;
+      ep.mode = EPI_HEADS;
+      ep.bias = w.qkvb;
+      ep.H = H; ep.Dp = Dp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = H * Dp;
+      ep.sec_out[0] = ws.q; ep.sec_out[1] = ws.k; ep.sec_out[2] = ws.vt;
+      ep.sec_trans[2] = 1;
+      EPD_TRY(gemm_bf16(ws.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
+    }
+    {
+      AttnParams ap;
+      ap.q = ws.q; ap.k = ws.k; ap.vt = ws.vt; ap.out = ws.ao;
+      ap.B = nt; ap.H = H; ap.Tq = T; ap.Tk = T; ap.Tkpad = Tpad; ap.Dp = Dp; ap.Dv = dh;
+      ap.ldo = D;
+      ap.scale = 1.f / std::sqrt((float)dh);
+      EPD_TRY(attention_bf16(ap, s));
+    }
+    {
+      EpiParams ep;
+      ep.bias = w.ob;
+      ep.resid = ws.h; ep.ldr = D; ep.lscale = w.ls1;
+      ep.out = ws.h; ep.ldo = D;
+      EPD_TRY(gemm_bf16(ws.ao, D, w.ow, D, M, D, D, ep, s));
+    }
+    EPD_TRY(layernorm_bf16(ws.h, D, ws.xn, D, w.ln2w, w.ln2b, M, D, eps, s));
+    {
+      EpiParams ep;
+      ep.bias = w.f1b;
+      ep.act = act;
+      ep.out = ws.f; ep.ldo = F;
+      EPD_TRY(gemm_bf16(ws.xn, D, w.f1w, D, M, F, D, ep, s));
+    }
+    {
+      EpiParams ep;
+      ep.bias = w.f2b;
+      ep.resid = ws.h; ep.ldr = D; ep.lscale = w.ls2;
+      ep.out = ws.h; ep.ldo = D;
+      EPD_TRY(gemm_bf16(ws.f, F, w.f2w, F, M, D, F, ep, s));
+    }
+  }
+  // 3. resampler / projector
+  if (!internvl) {
+    EPD_TRY(layernorm_bf16(ws.h, D, ws.xn, D, dw.post_w, dw.post_b, M, D, eps, s));
+    {
+      EpiParams ep;
+      ep.out = ws.r1; ep.ldo = E;
+      EPD_TRY(gemm_bf16(ws.xn, D, dw.r_kv, D, M, E, D, ep, s));
+    }
+    EPD_TRY(layernorm_bf16(ws.r1, E, ws.r2, E, dw.r_lnkv_w, dw.r_lnkv_b, M, E, 1e-6f, s));
+    {
+      // k = (x + pos) Wk^T + bk  ==  x Wk^T + bk + (pos Wk^T)   [pos_k table, rows % T]
+      EpiParams ep;
+      ep.mode = EPI_HEADS;
+      ep.bias = dw.r_kvin_b;
+      ep.resid = dw.r_posk; ep.ldr = 2 * RH * RDp; ep.r_mod = T;
+      ep.H = RH; ep.Dp = RDp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = RH * RDp;
+      ep.sec_out[0] = ws.rk; ep.sec_out[1] = ws.rvt;
+      ep.sec_trans[1] = 1;
+      EPD_TRY(gemm_bf16(ws.r2, E, dw.r_kvin, E, M, 2 * RH * RDp, E, ep, s));
+    }
+    {
+      AttnParams ap;
+      ap.q = dw.r_qheads; ap.k = ws.rk; ap.vt = ws.rvt; ap.out = ws.rao;
+      ap.B = nt; ap.H = RH; ap.Tq = Q; ap.Tk = T; ap.Tkpad = Tpad; ap.Dp = RDp; ap.Dv = rdh;
+      ap.ldo = E; ap.q_shared = 1;
+      ap.scale = 1.f / std::sqrt((float)rdh);
+      EPD_TRY(attention_bf16(ap, s));
+    }
+    {
+      EpiParams ep;
+      ep.bias = dw.r_ob;
+      ep.out = ws.rr; ep.ldo = E;
+      EPD_TRY(gemm_bf16(ws.rao, E, dw.r_ow, E, nt * Q, E, E, ep, s));
+    }
+    EPD_TRY(layernorm_bf16(ws.rr, E, ws.rao, E, dw.r_lnp_w, dw.r_lnp_b, nt * Q, E, 1e-6f, s));
+    {
+      EpiParams ep;
+      ep.out = out; ep.ldo = E;
+      EPD_TRY(gemm_bf16(ws.rao, E, dw.r_projT, E, nt * Q, E, E, ep, s));
+    }
+  } else {
+    const int C4 = 4 * D;
+    EPD_TRY(layernorm_bf16_gather(ws.h, D, ws.r2, C4, dw.m_ln_w, dw.m_ln_b, nt * Q, C4, 1e-5f,
+                                  dw.ps_idx, 4, s));
+    {
+      EpiParams ep;
+      ep.bias = dw.m_f1b;
+      ep.act = ACT_GELU_ERF;
+      ep.out = ws.rr; ep.ldo = E;
+      EPD_TRY(gemm_bf16(ws.r2, C4, dw.m_f1w, C4, nt * Q, E, C4, ep, s));
+    }
+    {
+      EpiParams ep;
+      ep.bias = dw.m_f2b;
+      ep.out = out; ep.ldo = E;
+      EPD_TRY(gemm_bf16(ws.rr, E, dw.m_f2w, E, nt * Q, E, E, ep, s));
+    }
+  }
+  return 0;
+}
+
+}  // namespace epd

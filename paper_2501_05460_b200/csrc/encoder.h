@@ -1,0 +1,86 @@
+// Encoder executor object behind the epd_encoder_* C ABI (see encoder.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <string>
+#include <vector>
+
+#include "../../include/epd.h"
+#include "kernels.h"
+
+namespace epd {
+
+struct WeightSlot {
+  std::string name;
+  std::vector<int64_t> shape;
+  std::vector<float> host;
+  bool set = false;
+};
+
+struct LayerSlots {
+  int ln1w = -1, ln1b = -1, qw = -1, qb = -1, kw = -1, kb = -1, vw = -1, vb = -1, ow = -1, ob = -1;
+  int ls1 = -1, ln2w = -1, ln2b = -1, f1w = -1, f1b = -1, f2w = -1, f2b = -1, ls2 = -1;
+};
+
+struct LayerW {
+  bf16 *ln1w = nullptr, *ln1b = nullptr, *qkv = nullptr, *qkvb = nullptr, *ow = nullptr, *ob = nullptr;
+  bf16 *ls1 = nullptr, *ln2w = nullptr, *ln2b = nullptr, *f1w = nullptr, *f1b = nullptr;
+  bf16 *f2w = nullptr, *f2b = nullptr, *ls2 = nullptr;
+};
+
+struct GlobalW {
+  bf16 *pe = nullptr, *pe_b = nullptr, *pos = nullptr, *post_w = nullptr, *post_b = nullptr;
+  bf16 *r_kv = nullptr, *r_lnkv_w = nullptr, *r_lnkv_b = nullptr, *r_kvin = nullptr, *r_kvin_b = nullptr;
+  bf16 *r_ow = nullptr, *r_ob = nullptr, *r_lnp_w = nullptr, *r_lnp_b = nullptr, *r_projT = nullptr;
+  bf16 *r_qheads = nullptr, *r_posk = nullptr;
+  bf16 *m_ln_w = nullptr, *m_ln_b = nullptr, *m_f1w = nullptr, *m_f1b = nullptr, *m_f2w = nullptr,
+       *m_f2b = nullptr;
+  int32_t* ps_idx = nullptr;
+};
+
+struct Workspace {
+  bf16 *xp = nullptr, *h = nullptr, *xn = nullptr, *ao = nullptr, *q = nullptr, *k = nullptr,
+       *vt = nullptr, *f = nullptr;
+  bf16 *r1 = nullptr, *r2 = nullptr, *rk = nullptr, *rvt = nullptr, *rao = nullptr, *rr = nullptr;
+};
+
+class Encoder {
+ public:
+  Encoder(const epd_encoder_desc_t& desc, int device);
+  ~Encoder();
+  std::string validate_and_build_schema();
+  int finalize(cudaStream_t stream, std::string& err);
+  int encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std::string& err);
+  int launches(int n) const;
+  double flops_per_tile() const;
+  int64_t numel(int i) const;
+
+  epd_encoder_desc_t d;
+  int dev;
+  std::vector<WeightSlot> slots;
+  bool finalized = false;
+
+ private:
+  int add(const std::string& name, std::vector<int64_t> shape);
+  const float* host(int i) const;
+  int forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
+
+  // geometry
+  int grid = 0, npatch = 0, T = 0, Tpad = 0, D = 0, H = 0, dh = 0, Dp = 0, F = 0;
+  int Kreal = 0, Kpad = 0, E = 0, Q = 0, RH = 0, rdh = 0, RDp = 0;
+  // schema indices
+  int w_pe = -1, b_pe = -1, w_cls = -1, w_pos = -1, w_post_w = -1, w_post_b = -1;
+  int r_query = -1, r_kv = -1, r_lnq_w = -1, r_lnq_b = -1, r_lnkv_w = -1, r_lnkv_b = -1;
+  int r_qw = -1, r_qb = -1, r_kw = -1, r_kb = -1, r_vw = -1, r_vb = -1, r_ow = -1, r_ob = -1;
+  int r_lnp_w = -1, r_lnp_b = -1, r_proj = -1, r_pos = -1;
+  int m_ln_w = -1, m_ln_b = -1, m_f1w = -1, m_f1b = -1, m_f2w = -1, m_f2b = -1;
+  std::vector<LayerSlots> lslots;
+  // device state
+  void* blob = nullptr;
+  void* work = nullptr;
+  GlobalW dw;
+  std::vector<LayerW> dl;
+  Workspace ws;
+};
+
+}  // namespace epd

@@ -1,0 +1,84 @@
+// Internal (C++) launch interface of the sm_100a kernels. The public, C-ABI
+// surface lives in include/epd.h and csrc/capi.cu; nothing here crosses the
+// shared-library boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace epd {
+
+using bf16 = __nv_bfloat16;
+
+enum EpiMode : int { EPI_ROWS = 0, EPI_HEADS = 1 };
+enum Act : int { ACT_NONE = 0, ACT_GELU_TANH = 1, ACT_GELU_ERF = 2 };
+
+// Epilogue of C = A[M,K] * B[N,K]^T, fused on the TMEM accumulator:
+//   x = act(acc + bias[n]);  if (resid) x = resid[row % r_mod][n] + lscale[n] * x
+// EPI_ROWS : out[row * ldo + n] = x
+// EPI_HEADS: column n splits into section s = n / sec_cols (q/k/v), head
+//   h = (n % sec_cols) / Dp, dim d = n % Dp; row = b * T + t. Section s writes
+//   sec_out[s][((b*H + h)*T + t)*Dp + d]            (sec_trans[s] == 0)
+//   sec_out[s][((b*H + h)*Dp + d)*Tpad + t]         (sec_trans[s] == 1, keys-major V^T)
+struct EpiParams {
+  int mode = EPI_ROWS;
+  int act = ACT_NONE;
+  const bf16* bias = nullptr;
+  const bf16* resid = nullptr;
+  int ldr = 0;
+  int r_mod = 0x7fffffff;
+  const bf16* lscale = nullptr;
+  bf16* out = nullptr;
+  int ldo = 0;
+  int H = 0, Dp = 0, T = 0, Tpad = 0, sec_cols = 0;
+  bf16* sec_out[3] = {nullptr, nullptr, nullptr};
+  int sec_trans[3] = {0, 0, 0};
+};
+
+// Returns a cudaError_t-compatible code (0 = success); 1000+ for argument errors.
+int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
+              const EpiParams& ep, cudaStream_t stream, int bn_hint = 0);
+
+// Fused multi-head attention O = softmax(Q K^T * scale) V on tcgen05.
+//   Q  : [Bq][Tq][Dp]   (q batch index = b * H + h, or h when q_shared)
+//   K  : [B*H][Tk][Dp]
+//   Vt : [B*H][Dp][Tkpad]  (keys contiguous)
+//   O  : out[(b * Tq + q) * ldo + h * Dv + d] for d < Dv
+// Dp in {64, 80, 128}; zero-padded head dims contribute nothing.
+struct AttnParams {
+  const bf16* q = nullptr;
+  const bf16* k = nullptr;
+  const bf16* vt = nullptr;
+  bf16* out = nullptr;
+  int B = 0, H = 0, Tq = 0, Tk = 0, Tkpad = 0, Dp = 0, Dv = 0, ldo = 0;
+  int q_shared = 0;
+  float scale = 1.f;
+};
+int attention_bf16(const AttnParams& p, cudaStream_t stream);
+
+// Row-wise LayerNorm over D (bf16 in/out, fp32 statistics), optional fused
+// residual-free affine (gamma, beta). in/out may alias. Rows are contiguous
+// with stride ld (elements).
+int layernorm_bf16(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                   const bf16* beta, int rows, int D, float eps, cudaStream_t stream);
+// Same, but logical row o is the concatenation of `segs` source rows
+// gidx[o*segs + s] (each D/segs wide, pitch ld_in): fuses a row gather such
+// as the InternVL pixel shuffle into the normalisation.
+int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                          const bf16* beta, int rows, int D, float eps, const int32_t* gidx,
+                          int segs, cudaStream_t stream);
+
+// uint8 HWC tiles [n][S][S][C] -> normalized bf16 patch rows
+// [n*(S/p)^2 (+cls)][Kpad] (im2col of the conv-as-GEMM patch embedding).
+// Column order = (c, ky, kx) to match Conv2d weight.view(D, C*p*p).
+// Normalization: x = (u8 / 255 - mean[c]) / std[c].
+int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int row_offset,
+                int rows_per_tile, const float* mean, const float* stdv, bf16* out,
+                cudaStream_t stream);
+
+// Gather equal-sized byte records: dst[i] = src_base[index[i]] (record = bytes).
+int gather_records(const void* src_base, const int32_t* index, int n, size_t bytes, void* dst,
+                   cudaStream_t stream);
+
+}  // namespace epd

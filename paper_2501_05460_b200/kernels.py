@@ -1,0 +1,82 @@
+"""Torch-tensor front ends for the kernel-level C-ABI ops (libepd.so).
+
+PyTorch supplies device memory and the current stream; all arithmetic runs in
+the sm_100a kernels. Every function requires CUDA tensors and fails loudly
+otherwise -- there is no CPU path.
+"""
+from __future__ import annotations
+
+import torch
+
+from ._lib import call
+
+ACT = {"none": 0, "gelu_tanh": 1, "gelu_erf": 2}
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _need_cuda(*ts: torch.Tensor | None) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("libepd ops take CUDA tensors only (no CPU fallback)")
+
+
+def linear(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, act: str = "none",
+           resid: torch.Tensor | None = None, r_mod: int = 0, lscale: torch.Tensor | None = None,
+           out: torch.Tensor | None = None, bn: int = 0) -> torch.Tensor:
+    """out = act(a @ w.T + bias); if resid: out = resid[row % r_mod] + lscale * out (bf16)."""
+    _need_cuda(a, w, bias, resid, lscale, out)
+    M, K = a.shape
+    N = w.shape[0]
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device=a.device)
+    call("epd_linear_bf16", a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K, _ptr(bias),
+         ACT[act], _ptr(resid), resid.stride(0) if resid is not None else 0, r_mod, _ptr(lscale),
+         out.data_ptr(), out.stride(0), bn, _stream(a))
+    return out
+
+
+def attention(q: torch.Tensor, k: torch.Tensor, vt: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
+              Dv: int, scale: float, q_shared: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Fused MHA; q [Bq,Tq,Dp], k [B*H,Tk,Dp], vt [B*H,Dp,Tkpad] -> out [B*Tq, H*Dv]."""
+    _need_cuda(q, k, vt, out)
+    Dp = q.shape[-1]
+    Tkpad = vt.shape[-1]
+    if out is None:
+        out = torch.empty(B * Tq, H * Dv, dtype=torch.bfloat16, device=q.device)
+    call("epd_attention_bf16", q.data_ptr(), k.data_ptr(), vt.data_ptr(), out.data_ptr(), B, H, Tq, Tk, Tkpad,
+         Dp, Dv, out.stride(0), int(q_shared), float(scale), _stream(q))
+    return out
+
+
+def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    _need_cuda(x, gamma, beta, out)
+    rows, D = x.shape
+    if out is None:
+        out = torch.empty_like(x)
+    call("epd_layernorm_bf16", x.data_ptr(), x.stride(0), out.data_ptr(), out.stride(0), gamma.data_ptr(),
+         beta.data_ptr(), rows, D, float(eps), _stream(x))
+    return out
+
+
+def patchify(tiles: torch.Tensor, patch: int, kpad: int, mean, std, row_offset: int = 0,
+             rows_per_tile: int | None = None) -> torch.Tensor:
+    """uint8 [n,S,S,C] -> bf16 [n*rows_per_tile, kpad] normalised im2col rows."""
+    _need_cuda(tiles)
+    import ctypes
+    n, S, _, Cc = tiles.shape
+    npatch = (S // patch) ** 2
+    rpt = rows_per_tile or npatch + row_offset
+    out = torch.zeros(n * rpt, kpad, dtype=torch.bfloat16, device=tiles.device)
+    m = (ctypes.c_float * 3)(*mean)
+    s = (ctypes.c_float * 3)(*std)
+    call("epd_patchify_u8", tiles.data_ptr(), n, S, Cc, patch, kpad, row_offset, rpt,
+         ctypes.cast(m, ctypes.c_void_p), ctypes.cast(s, ctypes.c_void_p), out.data_ptr(), _stream(tiles))
+    return out
