@@ -121,8 +121,7 @@ epd_status_t epd_irp_ranges(int64_t patches, int32_t width, int64_t* first, int6
 epd_status_t epd_encoder_create(const epd_encoder_desc_t* desc, int32_t device, epd_encoder_t** out) {
   if (!desc || !out) return fail(EPD_ERR_VALUE, "null argument");
   *out = nullptr;
-  cudaError_t e = cudaSetDevice(device);
-  if (e != cudaSuccess) return fail(EPD_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  // Schema construction is host-only; device memory is touched from finalize on.
   auto* enc = new epd_encoder(*desc, device);
   std::string msg = enc->impl.validate_and_build_schema();
   if (!msg.empty()) {
@@ -167,7 +166,8 @@ epd_status_t epd_encoder_set_weight(epd_encoder_t* enc, int32_t index, const flo
 epd_status_t epd_encoder_finalize(epd_encoder_t* enc, void* stream) {
   if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
   if (enc->impl.finalized) return fail(EPD_ERR_RUNTIME, "encoder already finalized");
-  cudaSetDevice(enc->impl.dev);
+  cudaError_t e = cudaSetDevice(enc->impl.dev);
+  if (e != cudaSuccess) return fail(EPD_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
   std::string err;
   int rc = enc->impl.finalize(S(stream), err);
   if (rc) return fail((epd_status_t)rc, err);

@@ -12,8 +12,25 @@ namespace {
 // One warp per row; each lane holds up to MAXV 8-element vectors in registers.
 // Optional row gather: logical row o = concat over seg of src rows
 // gidx[o*segs + seg] (each D/segs wide) -- fuses the InternVL pixel shuffle.
-template <int MAXV>
-__global__ void __launch_bounds__(256) layernorm_kernel(const bf16* __restrict__ in, int ld_in,
+template <typename Tin>
+EPD_DEVICE void load_row8(const Tin* src, float* x);
+template <>
+EPD_DEVICE void load_row8<bf16>(const bf16* src, float* x) {
+  uint4 u = *reinterpret_cast<const uint4*>(src);
+  float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z), d = unpack_bf16x2(u.w);
+  x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+  x[4] = c.x; x[5] = c.y; x[6] = d.x; x[7] = d.y;
+}
+template <>
+EPD_DEVICE void load_row8<float>(const float* src, float* x) {
+  const float4 a = *reinterpret_cast<const float4*>(src);
+  const float4 b = *reinterpret_cast<const float4*>(src + 4);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+  x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+
+template <int MAXV, typename Tin>
+__global__ void __launch_bounds__(256) layernorm_kernel(const Tin* __restrict__ in, int ld_in,
                                                         bf16* __restrict__ out, int ld_out,
                                                         const bf16* __restrict__ gamma,
                                                         const bf16* __restrict__ beta, int rows,
@@ -30,18 +47,14 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const bf16* __restrict__
   for (int i = 0; i < MAXV; ++i) {
     const int v = lane + i * 32;
     if (v < nvec) {
-      const bf16* src;
+      const Tin* src;
       if (gidx) {
         const int seg = v / seg_vec;
         src = in + (size_t)gidx[(size_t)row * segs + seg] * ld_in + (v - seg * seg_vec) * 8;
       } else {
         src = in + (size_t)row * ld_in + v * 8;
       }
-      uint4 u = *reinterpret_cast<const uint4*>(src);
-      float2 a = unpack_bf16x2(u.x), b = unpack_bf16x2(u.y), c = unpack_bf16x2(u.z),
-             d = unpack_bf16x2(u.w);
-      x[i][0] = a.x; x[i][1] = a.y; x[i][2] = b.x; x[i][3] = b.y;
-      x[i][4] = c.x; x[i][5] = c.y; x[i][6] = d.x; x[i][7] = d.y;
+      load_row8<Tin>(src, x[i]);
 #pragma unroll
       for (int j = 0; j < 8; ++j) sum += x[i][j];
     }
@@ -139,21 +152,35 @@ __global__ void gather_records_kernel(const uint4* __restrict__ src, const int32
 
 }  // namespace
 
-int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
-                          const bf16* beta, int rows, int D, float eps, const int32_t* gidx,
-                          int segs, cudaStream_t stream) {
+template <typename Tin>
+int layernorm_any(const Tin* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                  const bf16* beta, int rows, int D, float eps, const int32_t* gidx,
+                  int segs, cudaStream_t stream) {
   if (rows <= 0) return 0;
   if (D % 8 || ld_in % 8 || ld_out % 8) return 1002;
+  if (gidx && (segs <= 0 || (D / 8) % segs)) return 1002;
   const int nvec = D / 8;
   const dim3 block(256);
   const dim3 grid((rows + 7) / 8);
   if (nvec <= 32 * 5)
-    layernorm_kernel<5><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
+    layernorm_kernel<5, Tin><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
   else if (nvec <= 32 * 16)
-    layernorm_kernel<16><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
+    layernorm_kernel<16, Tin><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
   else
     return 1004;
   return (int)cudaGetLastError();
+}
+
+int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                          const bf16* beta, int rows, int D, float eps, const int32_t* gidx,
+                          int segs, cudaStream_t stream) {
+  return layernorm_any<bf16>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs, stream);
+}
+
+int layernorm_f32in(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                    const bf16* beta, int rows, int D, float eps, const int32_t* gidx, int segs,
+                    cudaStream_t stream) {
+  return layernorm_any<float>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs, stream);
 }
 
 int layernorm_bf16(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,

@@ -355,7 +355,7 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
     return o;
   };
   const size_t o_xp = plan(M * Kpad * 2);
-  const size_t o_h = plan(M * D * 2);
+  const size_t o_h = plan(M * D * 4);
   const size_t o_xn = plan(M * D * 2);
   const size_t o_ao = plan(M * D * 2);
   const size_t o_q = plan(nt * H * T * Dp * 2);
@@ -385,7 +385,7 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   }
   uint8_t* wb = reinterpret_cast<uint8_t*>(work);
   ws.xp = reinterpret_cast<bf16*>(wb + o_xp);
-  ws.h = reinterpret_cast<bf16*>(wb + o_h);
+  ws.h = reinterpret_cast<float*>(wb + o_h);
   ws.xn = reinterpret_cast<bf16*>(wb + o_xn);
   ws.ao = reinterpret_cast<bf16*>(wb + o_ao);
   ws.q = reinterpret_cast<bf16*>(wb + o_q);
@@ -512,7 +512,7 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     ep.resid = dw.pos;
     ep.ldr = D;
     ep.r_mod = T;
-    ep.out = ws.h;
+    ep.out_f = ws.h;
     ep.ldo = D;
     EPD_TRY(gemm_bf16(ws.xp, Kpad, dw.pe, Kpad, M, D, Kpad, ep, s));
   }
@@ -520,7 +520,7 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
   const int act = internvl ? ACT_GELU_ERF : ACT_GELU_TANH;
   for (size_t l = 0; l < dl.size(); ++l) {
     const auto& w = dl[l];
-    EPD_TRY(layernorm_bf16(ws.h, D, ws.xn, D, w.ln1w, w.ln1b, M, D, eps, s));
+    EPD_TRY(layernorm_f32in(ws.h, D, ws.xn, D, w.ln1w, w.ln1b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
       ep.mode = EPI_HEADS;
@@ -541,11 +541,11 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     {
       EpiParams ep;
       ep.bias = w.ob;
-      ep.resid = ws.h; ep.ldr = D; ep.lscale = w.ls1;
-      ep.out = ws.h; ep.ldo = D;
+      ep.resid_f = ws.h; ep.ldr = D; ep.lscale = w.ls1;
+      ep.out_f = ws.h; ep.ldo = D;
       EPD_TRY(gemm_bf16(ws.ao, D, w.ow, D, M, D, D, ep, s));
     }
-    EPD_TRY(layernorm_bf16(ws.h, D, ws.xn, D, w.ln2w, w.ln2b, M, D, eps, s));
+    EPD_TRY(layernorm_f32in(ws.h, D, ws.xn, D, w.ln2w, w.ln2b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
       ep.bias = w.f1b;
@@ -556,14 +556,14 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     {
       EpiParams ep;
       ep.bias = w.f2b;
-      ep.resid = ws.h; ep.ldr = D; ep.lscale = w.ls2;
-      ep.out = ws.h; ep.ldo = D;
+      ep.resid_f = ws.h; ep.ldr = D; ep.lscale = w.ls2;
+      ep.out_f = ws.h; ep.ldo = D;
       EPD_TRY(gemm_bf16(ws.f, F, w.f2w, F, M, D, F, ep, s));
     }
   }
   // 3. resampler / projector
   if (!internvl) {
-    EPD_TRY(layernorm_bf16(ws.h, D, ws.xn, D, dw.post_w, dw.post_b, M, D, eps, s));
+    EPD_TRY(layernorm_f32in(ws.h, D, ws.xn, D, dw.post_w, dw.post_b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
       ep.out = ws.r1; ep.ldo = E;
@@ -603,8 +603,8 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     }
   } else {
     const int C4 = 4 * D;
-    EPD_TRY(layernorm_bf16_gather(ws.h, D, ws.r2, C4, dw.m_ln_w, dw.m_ln_b, nt * Q, C4, 1e-5f,
-                                  dw.ps_idx, 4, s));
+    EPD_TRY(layernorm_f32in(ws.h, D, ws.r2, C4, dw.m_ln_w, dw.m_ln_b, nt * Q, C4, 1e-5f,
+                            dw.ps_idx, 4, s));
     {
       EpiParams ep;
       ep.bias = dw.m_f1b;

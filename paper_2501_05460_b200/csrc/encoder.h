@@ -39,7 +39,8 @@ struct GlobalW {
 };
 
 struct Workspace {
-  bf16 *xp = nullptr, *h = nullptr, *xn = nullptr, *ao = nullptr, *q = nullptr, *k = nullptr,
+  float* h = nullptr;  // fp32 residual stream
+  bf16 *xp = nullptr, *xn = nullptr, *ao = nullptr, *q = nullptr, *k = nullptr,
        *vt = nullptr, *f = nullptr;
   bf16 *r1 = nullptr, *r2 = nullptr, *rk = nullptr, *rvt = nullptr, *rao = nullptr, *rr = nullptr;
 };

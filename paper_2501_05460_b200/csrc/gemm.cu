@@ -68,7 +68,7 @@ EPD_DEVICE void epilogue_chunk(const EpiParams& ep, int row, int n, int N, const
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[j] = gelu_erf(x[j]);
     }
-    if (ep.resid) {
+    if (ep.resid || ep.resid_f) {
       if (ep.lscale) {
         float s[8];
         load8(ep.lscale + col, s);
@@ -76,12 +76,26 @@ EPD_DEVICE void epilogue_chunk(const EpiParams& ep, int row, int n, int N, const
         for (int j = 0; j < 8; ++j) x[j] *= s[j];
       }
       float r[8];
-      load8(ep.resid + (size_t)(row % ep.r_mod) * ep.ldr + col, r);
+      const size_t roff = (size_t)(row % ep.r_mod) * ep.ldr + col;
+      if (ep.resid_f) {
+        const float4 r0 = *reinterpret_cast<const float4*>(ep.resid_f + roff);
+        const float4 r1 = *reinterpret_cast<const float4*>(ep.resid_f + roff + 4);
+        r[0] = r0.x; r[1] = r0.y; r[2] = r0.z; r[3] = r0.w;
+        r[4] = r1.x; r[5] = r1.y; r[6] = r1.z; r[7] = r1.w;
+      } else {
+        load8(ep.resid + roff, r);
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) x[j] += r[j];
     }
     if (ep.mode == EPI_ROWS) {
-      store8(ep.out + (size_t)row * ep.ldo + col, x);
+      if (ep.out_f) {
+        float* o = ep.out_f + (size_t)row * ep.ldo + col;
+        *reinterpret_cast<float4*>(o) = make_float4(x[0], x[1], x[2], x[3]);
+        *reinterpret_cast<float4*>(o + 4) = make_float4(x[4], x[5], x[6], x[7]);
+      } else {
+        store8(ep.out + (size_t)row * ep.ldo + col, x);
+      }
     } else {
       const int s = col / ep.sec_cols;
       const int within = col - s * ep.sec_cols;

@@ -29,7 +29,9 @@ struct EpiParams {
   int ldr = 0;
   int r_mod = 0x7fffffff;
   const bf16* lscale = nullptr;
+  const float* resid_f = nullptr;  // fp32 residual stream (takes precedence over resid)
   bf16* out = nullptr;
+  float* out_f = nullptr;          // fp32 output (takes precedence over out)
   int ldo = 0;
   int H = 0, Dp = 0, T = 0, Tpad = 0, sec_cols = 0;
   bf16* sec_out[3] = {nullptr, nullptr, nullptr};
@@ -65,6 +67,10 @@ int layernorm_bf16(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16*
 // Same, but logical row o is the concatenation of `segs` source rows
 // gidx[o*segs + s] (each D/segs wide, pitch ld_in): fuses a row gather such
 // as the InternVL pixel shuffle into the normalisation.
+// fp32-input variant (the residual stream is kept in fp32).
+int layernorm_f32in(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
+                    const bf16* beta, int rows, int D, float eps, const int32_t* gidx, int segs,
+                    cudaStream_t stream);
 int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
                           const bf16* beta, int rows, int D, float eps, const int32_t* gidx,
                           int segs, cudaStream_t stream);

@@ -1,0 +1,76 @@
+"""End-to-end encoder parity on the B200: the sm_100a encode path (through the
+C ABI) against the fp32 CPU oracle on identical random-init weights and
+synthetic uint8 tiles.
+
+Tolerance (BASELINE.json north_star): max|y - y_ref| / max|y_ref| <= 1e-2 (bf16 compute).
+"""
+import pytest
+import torch
+
+from paper_2501_05460_b200.configs import INTERNVIT_300M, SEED, SIGLIP_MINICPM, TINY_VIT
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 1e-2
+
+_cache = {}
+
+
+def _setup(cfg, cuda, max_tiles=4):
+    key = (cfg.name, max_tiles)
+    if key not in _cache:
+        from paper_2501_05460_b200.encoder import VisionEncoder, canonical_weights
+        w = canonical_weights(cfg, SEED)
+        enc = VisionEncoder(cfg, cuda, max_tiles=max_tiles, weights=w)
+        _cache[key] = (w, enc)
+    return _cache[key]
+
+
+def _tiles(cfg, n, seed):
+    g = torch.Generator().manual_seed(seed)
+    return torch.randint(0, 256, (n, cfg.image_size, cfg.image_size, cfg.channels), dtype=torch.uint8,
+                         generator=g)
+
+
+@pytest.mark.parametrize("cfg,n", [
+    (TINY_VIT, 4),                         # PR1 config: 1 request x 4 tiles
+    (SIGLIP_MINICPM.with_layers(2), 2),
+    (INTERNVIT_300M.with_layers(2), 2),
+    (SIGLIP_MINICPM, 1),                   # full 27-layer SigLIP + resampler
+    (INTERNVIT_300M, 1),                   # full 24-layer InternViT + mlp1
+])
+def test_encoder_matches_oracle(cuda, cfg, n):
+    import oracle.encoders as oe
+    w, enc = _setup(cfg, cuda)
+    tiles = _tiles(cfg, n, seed=SEED + n)
+    y = enc.encode(tiles.to(cuda))
+    torch.cuda.synchronize()
+    # The deployed weights are bf16: the oracle computes the same (bf16-valued) weights in fp32.
+    ref = oe.encode(cfg, oe.bf16_weights(w), tiles)
+    assert y.shape == (n, cfg.out_tokens, cfg.out_dim)
+    err = oe.relerr(y, ref)
+    err32 = oe.relerr(y, oe.encode(cfg, w, tiles))
+    print(f"{cfg.name}: n={n} relerr={err:.3e} (vs fp32-valued weights {err32:.3e})")
+    assert err <= TOL_BF16
+
+
+def test_encoder_chunking_and_tile_independence(cuda):
+    """Tiles are independent sequences: encoding [a, b, c] in one call (split across
+    max_tiles chunks) equals encoding each alone, bit for bit."""
+    cfg = SIGLIP_MINICPM.with_layers(2)
+    w, enc = _setup(cfg, cuda, max_tiles=2)
+    tiles = _tiles(cfg, 3, seed=7).to(cuda)
+    together = enc.encode(tiles)
+    alone = torch.cat([enc.encode(tiles[i:i + 1].contiguous()) for i in range(3)])
+    torch.cuda.synchronize()
+    assert torch.equal(together, alone)
+
+
+def test_encoder_rejects_bad_input(cuda):
+    cfg = TINY_VIT
+    _, enc = _setup(cfg, cuda)
+    with pytest.raises(ValueError):
+        enc.encode(torch.zeros(1, 8, 8, 3, dtype=torch.uint8, device=cuda))
+    with pytest.raises(ValueError):
+        enc.encode_latency(None, -1)
+    assert enc.encode_latency(None, 0) == 0.0
