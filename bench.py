@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Encode-stage hot-path benchmark (BASELINE.json metric: encoded image tiles/s and
+p50 TTFT at 1/2/4/8 B200 vs the host-CPU reference).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c4|c5]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1; one process per GPU)
+
+One step = one request through the encode stage: its tiles are IRP-sharded over the
+N encode ranks (irp_shard, engine.py:55-62), encoded by the sm_100a kernels, and the
+MM tokens are gathered (NCCL P2P) in request order onto the prefill rank (rank 0).
+Default workload (c2): MiniCPM-V 2.6-shaped SigLIP-400M + resampler, 10 tiles of
+448x448 per request, bf16, random-init weights, synthetic uint8 tiles.
+
+Prints ONE JSON line on rank 0 (see the task contract): `value` = whole-job tiles/s
+with tiles resident in HBM; `e2e` = same through the public API with host buffers
+(pinned H2D of the tiles + D2H of the packed MM tokens inside the timed region);
+`p50_ttft_ms` = encode-side TTFT (tile upload -> MM tokens packed on the prefill GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "encoded image tiles/sec & p50 TTFT at 1/2/4/8 B200 vs host-CPU reference"
+
+# reference synthetic prefill calibration for MiniCPM-V 2.6 / InternVL2-8B (presets.py:53-61),
+# used only for the labelled "modeled prefill" add-on to the measured encode-side TTFT.
+PREFILL_COST = {"minicpm-v-2.6": (0.05, 2e-4, 1e-8), "internvl2-8b": (0.05, 8e-5, 1e-9)}
+PROMPT_TOKENS = 22
+
+
+def modeled_prefill_s(model: str, total_tokens: int) -> float:
+    """costs.prefill_latency (costs.py:93-99) at tp = pp = 1."""
+    b, a, q = PREFILL_COST[model]
+    return b + a * total_tokens + q * total_tokens * total_tokens
+
+
+def workload(name: str):
+    from paper_2501_05460_b200.configs import INTERNVIT_300M, SIGLIP_MINICPM
+    if name == "c2":
+        return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False,
+                    desc="C2: MiniCPM-V 2.6-shaped SigLIP-400M + resampler, 10 tiles (448x448) per request")
+    if name == "c4":
+        return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True,
+                    desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
+    if name == "c5":
+        return dict(cfg=INTERNVIT_300M, tiles=12, repeat=None, cache=False,
+                    desc="C5: InternVL2-8B-shaped InternViT-300M + pixel shuffle + mlp1, 12 tiles per request")
+    raise SystemExit(f"unknown workload {name}")
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]
+                          and not s[3 + i].startswith("Not")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def init_dist(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus and world != 1:
+        raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def reference_arm(args, wl, world, rank):
+    """--impl reference: the reference's CPU path for the encode stage = the fp32 CPU
+    oracle (the reference ships no encoder), on all host cores."""
+    if rank != 0:
+        return
+    import oracle.encoders as oe
+    from paper_2501_05460_b200.encoder import canonical_weights
+    from paper_2501_05460_b200.stage import tiles_for_request
+    cfg = wl["cfg"]
+    torch.set_num_threads(os.cpu_count())
+    w = canonical_weights(cfg)
+    tiles = tiles_for_request(wl["tiles"], cfg, seed=20260808)
+    per_step = 1  # bounded sample: one tile of the request per step
+    for i in range(args.warmup):
+        oe.encode(cfg, w, tiles[i % tiles.shape[0]:i % tiles.shape[0] + per_step])
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        j = (args.warmup + i) % tiles.shape[0]
+        oe.encode(cfg, w, tiles[j:j + per_step])
+    dt = time.perf_counter() - t0
+    v = args.steps * per_step / dt
+    line = {"metric": METRIC, "value": v, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": wl["desc"], "tiles_per_request": wl["tiles"], "sample_tiles_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "tiles/s", "cores": torch.get_num_threads(), "kind": "port",
+                             "sample": f"{per_step} tile per step, fp32 PyTorch CPU oracle (oracle/encoders.py)"},
+            "e2e": {"value": v, "unit": "tiles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warm-up raised to the minimum of 3", file=sys.stderr)
+        args.warmup = 3
+    wl = workload(args.workload)
+    world, rank, local = init_dist(args.gpus) if args.impl == "ours" else (
+        int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
+    if args.impl == "reference":
+        reference_arm(args, wl, world, rank)
+        return
+    run_ours(args, wl, world, rank, local)
+
+
+def run_ours(args, wl, world, rank, local):
+    import torch.distributed as dist
+
+    from paper_2501_05460_b200 import _lib
+    from paper_2501_05460_b200.encoder import VisionEncoder, canonical_weights
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    from paper_2501_05460_b200.stage import EncodeStage, tiles_for_request
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = wl["cfg"]
+    n = wl["tiles"]
+    weights = canonical_weights(cfg)
+    max_tiles = 32 if n > 32 else max(1, n)
+    enc = VisionEncoder(cfg, dev, max_tiles=max_tiles, weights=weights)
+    cache = None
+    if wl["cache"] and rank == 0:
+        cache = MMTokenCache(capacity=max(n, 750), tokens_per_tile=cfg.out_tokens, hidden=cfg.out_dim, device=dev)
+    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache)
+
+    tiles_host = tiles_for_request(n, cfg, seed=20260808, repeat_period=wl["repeat"]).pin_memory()
+    tiles_dev = tiles_host.to(dev)
+    out_host = torch.empty(n, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16).pin_memory()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def reset_cache():
+        if cache is not None:
+            cache.clear()
+
+    def step_resident():
+        reset_cache()
+        return stage.process(None, tiles_dev=tiles_dev)
+
+    def step_e2e():
+        reset_cache()
+        res = stage.process(tiles_host)
+        if res.tokens is not None:
+            out_host.copy_(res.tokens, non_blocking=True)
+        return res
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        barrier()
+        torch.cuda.synchronize()
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all0.record()
+        last = None
+        for i in range(k):
+            evs[i][0].record()
+            last = fn()
+            evs[i][1].record()
+        t_all1.record()
+        torch.cuda.synchronize()
+        barrier()
+        total_ms = max_over_ranks(t_all0.elapsed_time(t_all1))
+        per = [max_over_ranks(a.elapsed_time(b)) for a, b in evs]
+        return total_ms, per, last
+
+    for _ in range(args.warmup):
+        step_resident()
+        step_e2e()
+    torch.cuda.synchronize()
+
+    with ClockSampler(local) as clk:
+        total_ms, per_ms, last = timed(step_resident, args.steps)
+        e2e_ms, e2e_per, last_e2e = timed(step_e2e, args.steps)
+
+    # profiled pass (same workload, after the timed region): per-kernel-class device times
+    _lib.call("epd_encoder_profile", enc._h, 1)
+    prof_steps = 2
+    for _ in range(prof_steps):
+        step_resident()
+    torch.cuda.synchronize()
+    import ctypes as C
+    nc = 5
+    ms = (C.c_double * nc)()
+    fl = (C.c_double * nc)()
+    by = (C.c_double * nc)()
+    cnt = (C.c_int64 * nc)()
+    _lib.call("epd_encoder_profile_read", enc._h, ms, fl, by, cnt, nc)
+    _lib.call("epd_encoder_profile", enc._h, 0)
+
+    encoded_tiles = n  # tiles that complete the request per step (cache hits count as served)
+    value = encoded_tiles * args.steps / (total_ms / 1e3)
+    e2e_value = encoded_tiles * args.steps / (e2e_ms / 1e3)
+    p50_ttft = _percentile(e2e_per, 0.5)
+    p50_resident = _percentile(per_ms, 0.5)
+    if rank != 0:
+        return
+
+    peaks, peak_src = measured_peaks()
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    gemm_tflops = fl[1] / (ms[1] / 1e3) / 1e12 if ms[1] > 0 else None
+    flops_tile = enc.flops_per_tile()
+    classes = ["patchify", "gemm", "attention", "layernorm", "other"]
+    kernels = {classes[c]: {"ms_per_step": ms[c] / prof_steps, "launches_per_step": cnt[c] / prof_steps,
+                            "share": ms[c] / max(sum(ms), 1e-9),
+                            "tflops": (fl[c] / (ms[c] / 1e3) / 1e12) if ms[c] > 0 and fl[c] > 0 else None,
+                            "gbs": (by[c] / (ms[c] / 1e3) / 1e9) if ms[c] > 0 and by[c] > 0 else None}
+               for c in range(nc) if cnt[c]}
+    traffic = None
+    tj = ROOT / "profiles" / "ncu_traffic.json"
+    if tj.exists():
+        traffic = json.loads(tj.read_text()).get(wl["cfg"].name, {}).get("gemm_dram_bytes_per_launch")
+
+    launches_per_step = enc.launches(stage_tiles_per_rank(n, world, rank)) + (2 if cache is not None else 0)
+    model = cfg.geometry.name
+    total_tokens = n * cfg.out_tokens + PROMPT_TOKENS
+    prefill_ms = modeled_prefill_s(model, total_tokens) * 1e3 if model in PREFILL_COST else None
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, weights, tiles_host)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": wl["desc"], "encoder": cfg.name, "tiles_per_request": n,
+                   "irp_width": world, "prefill_rank": 0, "parallelism": f"irp{world}",
+                   "l2": "working set > L2 (0.97 GB bf16 weights + ~0.5 GB activations streamed per step)",
+                   "weights": "random-init N(0,0.02), seed 20260808"},
+        "p50_ttft_ms": p50_ttft,
+        "p50_ttft_ms_resident": p50_resident,
+        "p50_ttft_ms_with_modeled_prefill": (p50_ttft + prefill_ms) if prefill_ms is not None else None,
+        "ttft_note": "encode-side TTFT measured on B200 (H2D of the request's tiles -> MM tokens packed on the "
+                     "prefill GPU -> D2H); modeled prefill = reference costs.prefill_latency with "
+                     "SYNTHETIC_COSTS (presets.py:53-61), labelled 'modeled'",
+        "e2e": {"value": e2e_value, "unit": "tiles/s",
+                "h2d_bytes_per_step": int(n * cfg.tile_bytes),  # summed over ranks (each uploads its shard)
+                "d2h_bytes_per_step": int(out_host.numel() * 2)},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all encoder GEMM launches, profiled pass)",
+                     "achieved": gemm_tflops, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (gemm_tflops / peak) if gemm_tflops else None, "traffic": traffic,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "encoder_achieved": value * flops_tile / world / 1e12,
+                     "encoder_frac": value * flops_tile / world / 1e12 / peak,
+                     "flops_per_tile": flops_tile},
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    if cache is not None and last is not None and last.kinds is not None:
+        line["cache"] = {"hits": last.kinds.count("hit"), "misses": last.kinds.count("miss"),
+                         "dups": last.kinds.count("dup")}
+    print(json.dumps(line), flush=True)
+
+
+def stage_tiles_per_rank(n: int, world: int, rank: int) -> int:
+    from paper_2501_05460_b200.routing import shard_ranges
+    return shard_ranges(n, world)[rank][1]
+
+
+def _percentile(values, q):
+    """metrics._percentile (metrics.py:103-108): nearest rank, banker's round."""
+    o = sorted(values)
+    if not o:
+        return 0.0
+    return o[min(len(o) - 1, max(0, round(q * (len(o) - 1))))]
+
+
+def cpu_baseline(cfg, weights, tiles_host):
+    """fp32 CPU oracle on the host cores: 1 warm-up tile + 2 timed tiles (bounded sample)."""
+    import oracle.encoders as oe
+    torch.set_num_threads(os.cpu_count())
+    t = tiles_host[:3].clone()
+    oe.encode(cfg, weights, t[:1])
+    t0 = time.perf_counter()
+    oe.encode(cfg, weights, t[1:3])
+    dt = time.perf_counter() - t0
+    return {"value": 2 / dt, "unit": "tiles/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": "2 tiles of the request (after 1 warm-up tile), fp32 PyTorch CPU oracle "
+                      "(oracle/encoders.py), rank 0"}
+
+
+if __name__ == "__main__":
+    main()

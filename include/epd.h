@@ -98,6 +98,13 @@ epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t 
 double epd_encoder_flops_per_tile(const epd_encoder_t* enc);
 /* Kernel launches issued by one epd_encode_tiles call over n tiles. */
 int32_t epd_encoder_launches(const epd_encoder_t* enc, int32_t n);
+/* Per-launch CUDA-event profiling of subsequent encode calls (on = 1/0). */
+epd_status_t epd_encoder_profile(epd_encoder_t* enc, int32_t on);
+/* Drain the profile (synchronises on the last recorded event). Per kernel class
+ * c in {0 patchify, 1 gemm, 2 attention, 3 layernorm, 4 other}: summed device
+ * milliseconds, algorithmic FLOPs, algorithmic bytes and launch counts. */
+epd_status_t epd_encoder_profile_read(epd_encoder_t* enc, double* ms, double* flops, double* bytes,
+                                      int64_t* launches, int32_t nclass);
 
 /* ------------------------------------------------------------------ MM-token cache
  * Stands behind blocks.BlockManager(CacheKind.MM) (blocks.py:14-61) as the

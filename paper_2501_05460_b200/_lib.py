@@ -56,6 +56,8 @@ _SIGS = {
     "epd_encode_tiles": (_i32, [_vp, _vp, _i32, _vp, _vp]),
     "epd_encoder_flops_per_tile": (C.c_double, [_vp]),
     "epd_encoder_launches": (_i32, [_vp, _i32]),
+    "epd_encoder_profile": (_i32, [_vp, _i32]),
+    "epd_encoder_profile_read": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32]),
     "epd_hash_records": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "epd_mmcache_create": (_i32, [_i64, _i32, C.POINTER(_vp)]),
     "epd_mmcache_destroy": (None, [_vp]),

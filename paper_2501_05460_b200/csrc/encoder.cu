@@ -38,6 +38,7 @@ Encoder::Encoder(const epd_encoder_desc_t& desc, int device) : d(desc), dev(devi
 Encoder::~Encoder() {
   if (blob) cudaFree(blob);
   if (work) cudaFree(work);
+  for (auto e : prof_events) cudaEventDestroy(e);
 }
 
 int Encoder::add(const std::string& name, std::vector<int64_t> shape) {
@@ -445,7 +446,7 @@ int Encoder::launches(int n) const {
     per += 1 /*post LN*/ + 1 /*kv_proj*/ + 1 /*ln_kv*/ + 1 /*kv in-proj*/ + 1 /*attn*/ + 1 /*o*/ +
            1 /*ln_post*/ + 1 /*proj*/;
   else
-    per += 1 /*memset CLS rows*/ + 1 /*shuffle+LN*/ + 2 /*fc1, fc2*/;
+    per += 1 /*shuffle+LN*/ + 2 /*fc1, fc2*/;  // (+ a cudaMemset of the CLS rows, not a kernel of ours)
   return chunks * per;
 }
 
@@ -497,15 +498,68 @@ int Encoder::encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std:
     if (_rc) return _rc;      \
   } while (0)
 
+// Launch with optional per-launch CUDA-event profiling (class, algorithmic FLOPs, bytes).
+#define EPD_LAUNCH(cls, flops, bytes, x)        \
+  do {                                          \
+    const int _ev = prof_begin(s);              \
+    int _rc = (x);                              \
+    if (_rc) return _rc;                        \
+    prof_end(s, _ev, (cls), (flops), (bytes));  \
+  } while (0)
+
+int Encoder::prof_begin(cudaStream_t s) {
+  if (!prof_on) return -1;
+  if (prof_used + 2 > prof_events.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      prof_events.push_back(e);
+    }
+  }
+  const int i = (int)prof_used;
+  cudaEventRecord(prof_events[i], s);
+  prof_used += 2;
+  return i;
+}
+
+void Encoder::prof_end(cudaStream_t s, int ev, int cls, double flops, double bytes) {
+  if (ev < 0) return;
+  cudaEventRecord(prof_events[ev + 1], s);
+  prof_recs.push_back({cls, ev, flops, bytes});
+}
+
+int Encoder::prof_read(double* ms, double* flops, double* bytes, int64_t* count, int nclass) {
+  for (int c = 0; c < nclass; ++c) ms[c] = flops[c] = bytes[c] = 0, count[c] = 0;
+  if (!prof_recs.empty()) {
+    cudaError_t e = cudaEventSynchronize(prof_events[prof_recs.back().ev + 1]);
+    if (e != cudaSuccess) return (int)e;
+  }
+  for (const auto& r : prof_recs) {
+    if (r.cls < 0 || r.cls >= nclass) continue;
+    float t = 0.f;
+    cudaEventElapsedTime(&t, prof_events[r.ev], prof_events[r.ev + 1]);
+    ms[r.cls] += t;
+    flops[r.cls] += r.flops;
+    bytes[r.cls] += r.bytes;
+    count[r.cls] += 1;
+  }
+  prof_recs.clear();
+  prof_used = 0;
+  return 0;
+}
+
 int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s) {
   const int M = nt * T;
   const float eps = d.ln_eps;
   const bool internvl = d.family == EPD_FAMILY_INTERNVIT_MLP;
+  const double dM = M, dD = D, dF = F, dE = E, dQ = (double)nt * Q, dT = T;
+  const double ln_bytes_f32 = dM * dD * (4 + 2), ln_bytes = dM * dE * (2 + 2);
   // 1. patchify (+ zero CLS rows) and patch-embedding GEMM (+bias +pos)
   if (internvl)
-    EPD_TRY((int)cudaMemsetAsync(ws.xp, 0, (size_t)M * Kpad * 2, s));
-  EPD_TRY(patchify_u8(tiles, nt, d.image_size, d.channels, d.patch_size, Kpad, internvl ? 1 : 0, T,
-                      d.mean, d.std, ws.xp, s));
+    EPD_LAUNCH(PROF_OTHER, 0, (double)M * Kpad * 2, (int)cudaMemsetAsync(ws.xp, 0, (size_t)M * Kpad * 2, s));
+  EPD_LAUNCH(PROF_PATCHIFY, 0, (double)nt * d.image_size * d.image_size * d.channels + (double)nt * npatch * Kpad * 2,
+             patchify_u8(tiles, nt, d.image_size, d.channels, d.patch_size, Kpad, internvl ? 1 : 0, T,
+                         d.mean, d.std, ws.xp, s));
   {
     EpiParams ep;
     ep.bias = dw.pe_b;
@@ -514,13 +568,13 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     ep.r_mod = T;
     ep.out_f = ws.h;
     ep.ldo = D;
-    EPD_TRY(gemm_bf16(ws.xp, Kpad, dw.pe, Kpad, M, D, Kpad, ep, s));
+    EPD_LAUNCH(PROF_GEMM, 2.0 * nt * npatch * Kreal * dD, 0, gemm_bf16(ws.xp, Kpad, dw.pe, Kpad, M, D, Kpad, ep, s));
   }
   // 2. transformer blocks
   const int act = internvl ? ACT_GELU_ERF : ACT_GELU_TANH;
   for (size_t l = 0; l < dl.size(); ++l) {
     const auto& w = dl[l];
-    EPD_TRY(layernorm_f32in(ws.h, D, ws.xn, D, w.ln1w, w.ln1b, M, D, eps, nullptr, 1, s));
+    EPD_LAUNCH(PROF_LN, 0, ln_bytes_f32, layernorm_f32in(ws.h, D, ws.xn, D, w.ln1w, w.ln1b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
       ep.mode = EPI_HEADS;
@@ -528,7 +582,7 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ep.H = H; ep.Dp = Dp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = H * Dp;
       ep.sec_out[0] = ws.q; ep.sec_out[1] = ws.k; ep.sec_out[2] = ws.vt;
       ep.sec_trans[2] = 1;
-      EPD_TRY(gemm_bf16(ws.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * 3 * dD, 0, gemm_bf16(ws.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
     }
     {
       AttnParams ap;
@@ -536,40 +590,41 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ap.B = nt; ap.H = H; ap.Tq = T; ap.Tk = T; ap.Tkpad = Tpad; ap.Dp = Dp; ap.Dv = dh;
       ap.ldo = D;
       ap.scale = 1.f / std::sqrt((float)dh);
-      EPD_TRY(attention_bf16(ap, s));
+      EPD_LAUNCH(PROF_ATTN, 4.0 * nt * dT * dT * dD, 0, attention_bf16(ap, s));
     }
     {
       EpiParams ep;
       ep.bias = w.ob;
       ep.resid_f = ws.h; ep.ldr = D; ep.lscale = w.ls1;
       ep.out_f = ws.h; ep.ldo = D;
-      EPD_TRY(gemm_bf16(ws.ao, D, w.ow, D, M, D, D, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * dD, 0, gemm_bf16(ws.ao, D, w.ow, D, M, D, D, ep, s));
     }
-    EPD_TRY(layernorm_f32in(ws.h, D, ws.xn, D, w.ln2w, w.ln2b, M, D, eps, nullptr, 1, s));
+    EPD_LAUNCH(PROF_LN, 0, ln_bytes_f32, layernorm_f32in(ws.h, D, ws.xn, D, w.ln2w, w.ln2b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
       ep.bias = w.f1b;
       ep.act = act;
       ep.out = ws.f; ep.ldo = F;
-      EPD_TRY(gemm_bf16(ws.xn, D, w.f1w, D, M, F, D, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * dF, 0, gemm_bf16(ws.xn, D, w.f1w, D, M, F, D, ep, s));
     }
     {
       EpiParams ep;
       ep.bias = w.f2b;
       ep.resid_f = ws.h; ep.ldr = D; ep.lscale = w.ls2;
       ep.out_f = ws.h; ep.ldo = D;
-      EPD_TRY(gemm_bf16(ws.f, F, w.f2w, F, M, D, F, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * dF, 0, gemm_bf16(ws.f, F, w.f2w, F, M, D, F, ep, s));
     }
   }
   // 3. resampler / projector
   if (!internvl) {
-    EPD_TRY(layernorm_f32in(ws.h, D, ws.xn, D, dw.post_w, dw.post_b, M, D, eps, nullptr, 1, s));
+    EPD_LAUNCH(PROF_LN, 0, ln_bytes_f32,
+               layernorm_f32in(ws.h, D, ws.xn, D, dw.post_w, dw.post_b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
       ep.out = ws.r1; ep.ldo = E;
-      EPD_TRY(gemm_bf16(ws.xn, D, dw.r_kv, D, M, E, D, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * dE, 0, gemm_bf16(ws.xn, D, dw.r_kv, D, M, E, D, ep, s));
     }
-    EPD_TRY(layernorm_bf16(ws.r1, E, ws.r2, E, dw.r_lnkv_w, dw.r_lnkv_b, M, E, 1e-6f, s));
+    EPD_LAUNCH(PROF_LN, 0, ln_bytes, layernorm_bf16(ws.r1, E, ws.r2, E, dw.r_lnkv_w, dw.r_lnkv_b, M, E, 1e-6f, s));
     {
       // k = (x + pos) Wk^T + bk  ==  x Wk^T + bk + (pos Wk^T)   [pos_k table, rows % T]
       EpiParams ep;
@@ -579,7 +634,7 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ep.H = RH; ep.Dp = RDp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = RH * RDp;
       ep.sec_out[0] = ws.rk; ep.sec_out[1] = ws.rvt;
       ep.sec_trans[1] = 1;
-      EPD_TRY(gemm_bf16(ws.r2, E, dw.r_kvin, E, M, 2 * RH * RDp, E, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 4.0 * dM * dE * dE, 0, gemm_bf16(ws.r2, E, dw.r_kvin, E, M, 2 * RH * RDp, E, ep, s));
     }
     {
       AttnParams ap;
@@ -587,36 +642,37 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ap.B = nt; ap.H = RH; ap.Tq = Q; ap.Tk = T; ap.Tkpad = Tpad; ap.Dp = RDp; ap.Dv = rdh;
       ap.ldo = E; ap.q_shared = 1;
       ap.scale = 1.f / std::sqrt((float)rdh);
-      EPD_TRY(attention_bf16(ap, s));
+      EPD_LAUNCH(PROF_ATTN, 4.0 * dQ * dT * dE, 0, attention_bf16(ap, s));
     }
     {
       EpiParams ep;
       ep.bias = dw.r_ob;
       ep.out = ws.rr; ep.ldo = E;
-      EPD_TRY(gemm_bf16(ws.rao, E, dw.r_ow, E, nt * Q, E, E, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dQ * dE * dE, 0, gemm_bf16(ws.rao, E, dw.r_ow, E, nt * Q, E, E, ep, s));
     }
-    EPD_TRY(layernorm_bf16(ws.rr, E, ws.rao, E, dw.r_lnp_w, dw.r_lnp_b, nt * Q, E, 1e-6f, s));
+    EPD_LAUNCH(PROF_LN, 0, dQ * dE * 4,
+               layernorm_bf16(ws.rr, E, ws.rao, E, dw.r_lnp_w, dw.r_lnp_b, nt * Q, E, 1e-6f, s));
     {
       EpiParams ep;
       ep.out = out; ep.ldo = E;
-      EPD_TRY(gemm_bf16(ws.rao, E, dw.r_projT, E, nt * Q, E, E, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dQ * dE * dE, 0, gemm_bf16(ws.rao, E, dw.r_projT, E, nt * Q, E, E, ep, s));
     }
   } else {
     const int C4 = 4 * D;
-    EPD_TRY(layernorm_f32in(ws.h, D, ws.r2, C4, dw.m_ln_w, dw.m_ln_b, nt * Q, C4, 1e-5f,
-                            dw.ps_idx, 4, s));
+    EPD_LAUNCH(PROF_LN, 0, dQ * C4 * (4 + 2),
+               layernorm_f32in(ws.h, D, ws.r2, C4, dw.m_ln_w, dw.m_ln_b, nt * Q, C4, 1e-5f, dw.ps_idx, 4, s));
     {
       EpiParams ep;
       ep.bias = dw.m_f1b;
       ep.act = ACT_GELU_ERF;
       ep.out = ws.rr; ep.ldo = E;
-      EPD_TRY(gemm_bf16(ws.r2, C4, dw.m_f1w, C4, nt * Q, E, C4, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dQ * C4 * dE, 0, gemm_bf16(ws.r2, C4, dw.m_f1w, C4, nt * Q, E, C4, ep, s));
     }
     {
       EpiParams ep;
       ep.bias = dw.m_f2b;
       ep.out = out; ep.ldo = E;
-      EPD_TRY(gemm_bf16(ws.rr, E, dw.m_f2w, E, nt * Q, E, E, ep, s));
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dQ * dE * dE, 0, gemm_bf16(ws.rr, E, dw.m_f2w, E, nt * Q, E, E, ep, s));
     }
   }
   return 0;

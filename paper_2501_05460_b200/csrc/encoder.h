@@ -45,6 +45,15 @@ struct Workspace {
   bf16 *r1 = nullptr, *r2 = nullptr, *rk = nullptr, *rvt = nullptr, *rao = nullptr, *rr = nullptr;
 };
 
+enum ProfClass : int { PROF_PATCHIFY = 0, PROF_GEMM = 1, PROF_ATTN = 2, PROF_LN = 3, PROF_OTHER = 4, PROF_NCLASS = 5 };
+
+struct ProfRec {
+  int cls;
+  int ev;
+  double flops;
+  double bytes;
+};
+
 class Encoder {
  public:
   Encoder(const epd_encoder_desc_t& desc, int device);
@@ -55,6 +64,8 @@ class Encoder {
   int launches(int n) const;
   double flops_per_tile() const;
   int64_t numel(int i) const;
+  int prof_read(double* ms, double* flops, double* bytes, int64_t* count, int nclass);
+  bool prof_on = false;
 
   epd_encoder_desc_t d;
   int dev;
@@ -65,6 +76,11 @@ class Encoder {
   int add(const std::string& name, std::vector<int64_t> shape);
   const float* host(int i) const;
   int forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
+  int prof_begin(cudaStream_t s);
+  void prof_end(cudaStream_t s, int ev, int cls, double flops, double bytes);
+  std::vector<cudaEvent_t> prof_events;
+  size_t prof_used = 0;
+  std::vector<ProfRec> prof_recs;
 
   // geometry
   int grid = 0, npatch = 0, T = 0, Tpad = 0, D = 0, H = 0, dh = 0, Dp = 0, F = 0;

@@ -1,0 +1,210 @@
+"""Encode stage runtime: one request's tiles -> packed MM tokens on the prefill GPU.
+
+Mirrors the encode branch of the reference engine, with real work in place of
+modeled time (citations relative to /root/reference/pkg/src/disaggsim/):
+
+1. ``_start_encode`` (engine.py:570-613): the request's tiles are partitioned
+   with ``irp_shard`` over the IRP width = the encode ranks; rank k owns the
+   contiguous range ``shard_ranges(n, w)[k]``; zero shards idle.
+2. MM cache (blocks.py MM manager, engine.py:155-157 + the content cache the
+   reference lacks): on the prefill rank the tiles are hashed and looked up;
+   only first occurrences of uncached tiles are sharded and encoded.
+3. ``_send_ready_shards`` / ``_on_transfer_end("ep")`` (engine.py:424-435,
+   521-526): each rank's shard of post-projector tokens
+   (``tiles * tokens_per_patch * mm_bytes_per_token`` bytes) goes to the
+   prefill rank with NCCL point-to-point over NVLink, landing at its tile
+   offset, so the packed buffer is in request order whatever the arrival
+   order; prefill may start only once all shards landed.
+
+Multi-GPU layout: one process per GPU (torchrun); ranks 0..w-1 are the encode
+workers and rank ``prefill_rank`` (default 0) is also the prefill sink (at
+w = 8 on an 8-GPU node the sink shares a GPU with encode worker 0 -- the
+documented deviation from the reference's GPU budget rule, simconfig.py:86-88).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .routing import ep_bytes, shard_ranges
+
+
+@dataclass
+class ShardRecord:
+    """trace.ShardRecord (trace.py:18-24) with measured device times (seconds)."""
+
+    worker: int
+    patches: int
+    start: float | None = None
+    end: float | None = None
+    transfer_end: float | None = None
+
+
+@dataclass
+class RequestResult:
+    rid: int
+    n_tiles: int
+    encoded_tiles: int
+    shards: list = field(default_factory=list)
+    kinds: list | None = None           # cache classification per tile (hit/miss/dup)
+    ep_bytes: int = 0                    # bytes moved to the prefill rank (engine.py:524)
+    tokens: torch.Tensor | None = None   # packed [n, tokens_per_tile, hidden] on the prefill rank
+
+
+class EncodeStage:
+    """Per-rank encode-stage executor.
+
+    ``encoder`` must expose ``cfg`` (an EncoderConfig) and
+    ``encode(tiles_dev, out)``; in production it is
+    :class:`~.encoder.VisionEncoder` (sm_100a kernels). ``cache`` is an
+    optional :class:`~.mmcache.MMTokenCache` living on the prefill rank.
+    """
+
+    def __init__(self, encoder, device: torch.device, rank: int = 0, world: int = 1, prefill_rank: int = 0,
+                 cache=None, group=None):
+        self.enc = encoder
+        self.cfg = encoder.cfg
+        self.device = torch.device(device)
+        self.rank = rank
+        self.world = world
+        self.prefill_rank = prefill_rank
+        self.cache = cache
+        self.group = group
+        if cache is not None and rank != prefill_rank:
+            raise ValueError("the MM-token cache lives on the prefill rank")
+        self._staging = None
+
+    # ------------------------------------------------------------------ helpers
+    def _tokens_shape(self, n: int):
+        return (n, self.cfg.out_tokens, self.cfg.out_dim)
+
+    def _buffer(self, n: int) -> torch.Tensor:
+        return torch.empty(self._tokens_shape(n), dtype=torch.bfloat16, device=self.device)
+
+    def _upload(self, tiles_host: torch.Tensor, idx) -> torch.Tensor:
+        if idx is None:
+            return tiles_host.to(self.device, non_blocking=True)
+        if isinstance(idx, slice):
+            return tiles_host[idx].to(self.device, non_blocking=True)
+        sel = tiles_host.index_select(0, torch.as_tensor(idx, dtype=torch.int64))
+        return sel.to(self.device, non_blocking=True)
+
+    def _gather(self, local: torch.Tensor | None, dest: torch.Tensor | None, ranges) -> None:
+        """Shards -> prefill rank at their unit offsets (grouped point-to-point)."""
+        if self.world == 1:
+            return
+        ops = []
+        if self.rank == self.prefill_rank:
+            for k, (first, count) in enumerate(ranges):
+                if k != self.rank and count > 0:
+                    ops.append(dist.P2POp(dist.irecv, dest[first:first + count], k, self.group))
+        else:
+            first, count = ranges[self.rank]
+            if count > 0:
+                ops.append(dist.P2POp(dist.isend, local, self.prefill_rank, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    # ------------------------------------------------------------------ request
+    def process(self, tiles_host: torch.Tensor, rid: int = 0, tiles_dev: torch.Tensor | None = None
+                ) -> RequestResult:
+        """Encode one request. ``tiles_host``: uint8 [n, S, S, C] (pinned for async copies);
+        if ``tiles_dev`` (all tiles, already on this rank's device) is given, no H2D copy
+        is made. Returns the packed tokens on the prefill rank."""
+        n = tiles_host.shape[0] if tiles_host is not None else tiles_dev.shape[0]
+        is_sink = self.rank == self.prefill_rank
+        res = RequestResult(rid=rid, n_tiles=n, encoded_tiles=0)
+        tpp, bpt = self.cfg.out_tokens, self.cfg.out_dim * 2
+
+        if self.cache is None:
+            ranges = shard_ranges(n, self.world)
+            first, count = ranges[self.rank]
+            packed = self._buffer(n) if is_sink else None
+            local = None
+            if count > 0:
+                src = (tiles_dev[first:first + count] if tiles_dev is not None
+                       else self._upload(tiles_host, slice(first, first + count)))
+                local = packed[first:first + count] if is_sink else self._buffer(count)
+                self.enc.encode(src.contiguous(), local)
+            self._gather(local, packed, ranges)
+            res.encoded_tiles = count
+            res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
+            res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != self.prefill_rank)
+            res.tokens = packed
+            return res
+
+        # ---- cached path (cache on the prefill rank)
+        from .mmcache import hash_tiles
+        plan = None
+        if is_sink:
+            all_dev = tiles_dev if tiles_dev is not None else self._upload(tiles_host, None)
+            keys = hash_tiles(all_dev.contiguous())
+            plan = self.cache.plan(keys)
+            miss = torch.as_tensor(plan.miss_tiles, dtype=torch.int64)
+        if self.world > 1:
+            cnt = torch.tensor([0 if plan is None else len(plan.miss_tiles)], dtype=torch.int64, device=self.device)
+            dist.broadcast(cnt, self.prefill_rank, group=self.group)
+            m = int(cnt.item())
+            midx = miss.to(self.device) if is_sink else torch.empty(m, dtype=torch.int64, device=self.device)
+            if m:
+                dist.broadcast(midx, self.prefill_rank, group=self.group)
+            miss = midx.cpu()
+        m = miss.numel()
+        ranges = shard_ranges(m, self.world)
+        first, count = ranges[self.rank]
+        staging = self._buffer(m) if is_sink and m else None
+        local = None
+        if count > 0:
+            my = miss[first:first + count]
+            if is_sink:
+                src = all_dev.index_select(0, my.to(self.device))
+                local = staging[first:first + count]
+            else:
+                src = (tiles_dev.index_select(0, my.to(self.device)) if tiles_dev is not None
+                       else self._upload(tiles_host, my))
+                local = self._buffer(count)
+            self.enc.encode(src.contiguous(), local)
+        self._gather(local, staging, ranges)
+        res.encoded_tiles = count
+        res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
+        res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != self.prefill_rank)
+        if is_sink:
+            from ._lib import call
+            import ctypes as C
+            rec = tpp * bpt
+            s = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+            if m:
+                ent = torch.as_tensor(plan.miss_entries, dtype=torch.int32).to(self.device)
+                call("epd_scatter_records", C.c_void_p(staging.data_ptr()), C.c_void_p(ent.data_ptr()), m, rec,
+                     C.c_void_p(self.cache.store.data_ptr()), s)
+            packed = self._buffer(n)
+            idx = torch.as_tensor(plan.entries, dtype=torch.int32).to(self.device)
+            call("epd_gather_records", C.c_void_p(self.cache.store.data_ptr()), C.c_void_p(idx.data_ptr()), n, rec,
+                 C.c_void_p(packed.data_ptr()), s)
+            res.kinds = plan.kinds
+            res.tokens = packed
+        return res
+
+
+def tiles_for_request(n: int, cfg, seed: int, repeat_period: int | None = None) -> torch.Tensor:
+    """Synthetic uint8 HWC tiles [n, S, S, C] (uniform 0..255, seeded). With
+    ``repeat_period`` p, tile i repeats tile i - p (the C4 repeated-image workload)."""
+    g = torch.Generator().manual_seed(seed)
+    S, Cc = cfg.image_size, cfg.channels
+    if repeat_period:
+        base = torch.randint(0, 256, (repeat_period, S, S, Cc), dtype=torch.uint8, generator=g)
+        reps = -(-n // repeat_period)
+        return base.repeat(reps, 1, 1, 1)[:n].contiguous()
+    return torch.randint(0, 256, (n, S, S, Cc), dtype=torch.uint8, generator=g)
+
+
+def unit_order(n: int, world: int) -> np.ndarray:
+    """Owner rank of each unit under shard_ranges (for tests/inspection)."""
+    owner = np.empty(n, dtype=np.int64)
+    for k, (f, c) in enumerate(shard_ranges(n, world)):
+        owner[f:f + c] = k
+    return owner
