@@ -1,0 +1,86 @@
+"""MM-token cache and KV handoff on the B200, bit-exact against the CPU oracles:
+content keys (K11), hash-table hit/miss/dup classification, entry ids and evictions
+(K12), the cached encode path (C4 shape, scaled), and the paged KV pack/unpack (C2)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.hashing import content_hash
+from oracle.mmcache import MMCacheOracle
+
+pytestmark = pytest.mark.gpu
+
+
+def test_hash_kernel_matches_oracle(cuda):
+    from paper_2501_05460_b200.mmcache import hash_tiles
+    rng = np.random.default_rng(3)
+    for shape in [(5, 448, 448, 3), (3, 56, 56, 3), (4, 8), (2, 64), (7, 4096)]:
+        arr = rng.integers(0, 256, shape, dtype=np.uint8)
+        if shape == (4, 8):
+            arr[:] = 0
+        keys = hash_tiles(torch.from_numpy(arr).to(cuda)).cpu().numpy().view(np.uint64)
+        for i in range(shape[0]):
+            assert tuple(int(k) for k in keys[i]) == content_hash(arr[i]), (shape, i)
+
+
+def test_cache_sequence_matches_oracle(cuda):
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    rng = np.random.default_rng(11)
+    pool = rng.integers(0, 256, (30, 8 * 8 * 3), dtype=np.uint8)  # 30 distinct records
+    cache = MMTokenCache(capacity=12, tokens_per_tile=4, hidden=8, device=cuda)
+    oracle = MMCacheOracle(12)
+    from paper_2501_05460_b200.mmcache import hash_tiles
+    for step in range(40):
+        n = int(rng.integers(1, 12))
+        ids = rng.integers(0, 30 if step > 5 else 10, n)
+        tiles = torch.from_numpy(pool[ids]).to(cuda)
+        plan = cache.plan(hash_tiles(tiles))
+        expect = oracle.process([content_hash(pool[i]) for i in ids])
+        got = list(zip(plan.kinds, [int(e) for e in plan.entries]))
+        assert got == expect, step
+        assert plan.victims == oracle.last_victims
+    cache.check()
+
+
+def test_cached_stage_bit_exact(cuda):
+    """C4 shape scaled down: 40 tiles with tile i+20 == tile i. First request: 20 misses
+    + 20 in-batch dups; second: 40 hits. Packed tokens == encoding every tile directly."""
+    from paper_2501_05460_b200.configs import SEED, TINY_VIT
+    from paper_2501_05460_b200.encoder import VisionEncoder
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    from paper_2501_05460_b200.stage import EncodeStage, tiles_for_request
+    cfg = TINY_VIT
+    enc = VisionEncoder(cfg, cuda, max_tiles=16)
+    tiles = tiles_for_request(40, cfg, SEED, repeat_period=20)
+    direct = enc.encode(tiles.to(cuda))
+    cache = MMTokenCache(64, cfg.out_tokens, cfg.out_dim, cuda)
+    st = EncodeStage(enc, cuda, cache=cache)
+    r1 = st.process(tiles.pin_memory())
+    assert r1.kinds.count("miss") == 20 and r1.kinds.count("dup") == 20 and r1.encoded_tiles == 20
+    r2 = st.process(tiles.pin_memory())
+    assert r2.kinds == ["hit"] * 40 and r2.encoded_tiles == 0
+    torch.cuda.synchronize()
+    assert torch.equal(r1.tokens, direct)
+    assert torch.equal(r2.tokens, direct)
+
+
+def test_kv_pack_unpack_and_local_handoff(cuda):
+    from paper_2501_05460_b200.handoff import PagedKVCache, kv_handoff
+    p = PagedKVCache(num_layers=4, kv_heads=2, head_dim=16, block_size=16, num_blocks=40, device=cuda)
+    d = PagedKVCache(num_layers=4, kv_heads=2, head_dim=16, block_size=16, num_blocks=50, device=cuda)
+    p.pool.copy_(torch.randn_like(p.pool, dtype=torch.float32).to(torch.bfloat16))
+    d.manager.allocate(99, 100)  # decode side already busy: ids shift
+    total, out_tok = 70, 5
+    src_ids = p.manager.allocate(1, total)
+    assert src_ids == [0, 1, 2, 3, 4]
+    packed = p.pack(src_ids)
+    assert torch.equal(packed, p.pool[:, src_ids].permute(1, 0, 2))
+    expect = p.pool[:, src_ids].clone()
+    info = kv_handoff(1, total, out_tok, p, d, 0, 0, rank=0)
+    torch.cuda.synchronize()
+    dst = info["dst_blocks"]
+    assert len(dst) == d.manager.blocks_needed(total + out_tok)
+    assert torch.equal(d.pool[:, dst[:5]], expect)
+    assert info["pd_bytes"] == total * p.kv_bytes_per_token
+    assert info["moved_bytes"] == 5 * 16 * p.kv_bytes_per_token
+    assert 1 not in p.manager.allocated  # prefill side freed after the send (engine.py:437)

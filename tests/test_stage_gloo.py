@@ -1,0 +1,98 @@
+"""Multi-process CPU tier (gloo, world_size 2 and 3) for the IRP encode stage: tile
+routing, the EP gather to the prefill rank in request order, and the byte
+accounting -- with a deterministic stand-in encoder (the real one needs the B200;
+its numerics are covered by tests/test_encoder_gpu.py)."""
+import os
+import socket
+from dataclasses import dataclass
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2501_05460_b200.routing import shard_ranges
+
+
+@dataclass(frozen=True)
+class _Cfg:
+    image_size: int = 8
+    channels: int = 3
+    out_tokens: int = 4
+    out_dim: int = 8
+
+
+class _StandInEncoder:
+    """tokens[i, t, d] = mean(tile_i) + t + d/10 + rank*0 (rank-independent, tile-determined)."""
+
+    cfg = _Cfg()
+
+    def __init__(self):
+        self.calls = []
+
+    def encode(self, tiles, out):
+        self.calls.append(tiles.shape[0])
+        m = tiles.float().mean(dim=(1, 2, 3))
+        t = torch.arange(4).view(1, 4, 1).float()
+        d = torch.arange(8).view(1, 1, 8).float() / 10
+        out.copy_((m.view(-1, 1, 1) + t + d).to(out.dtype))
+        return out
+
+
+def _expected(tiles):
+    enc = _StandInEncoder()
+    out = torch.empty(tiles.shape[0], 4, 8, dtype=torch.bfloat16)
+    return enc.encode(tiles, out)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_05460_b200.stage import EncodeStage
+        g = torch.Generator().manual_seed(n)
+        tiles = torch.randint(0, 256, (n, 8, 8, 3), dtype=torch.uint8, generator=g)
+        enc = _StandInEncoder()
+        st = EncodeStage(enc, torch.device("cpu"), rank=rank, world=world, prefill_rank=0)
+        res = st.process(tiles, rid=7)
+        first, count = shard_ranges(n, world)[rank]
+        out = {"rank": rank, "encoded": res.encoded_tiles, "calls": enc.calls,
+               "shards": [(s.worker, s.patches) for s in res.shards], "ep_bytes": res.ep_bytes}
+        if rank == 0:
+            out["tokens"] = res.tokens.float()
+            out["expected"] = _expected(tiles).float()
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 10), (3, 10), (2, 1), (3, 13)])
+def test_irp_gather_request_order(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    outs.sort(key=lambda o: o["rank"])
+    ranges = shard_ranges(n, world)
+    for o in outs:
+        assert o["encoded"] == ranges[o["rank"]][1]
+        assert sum(o["calls"]) == ranges[o["rank"]][1]
+        assert o["shards"] == [(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
+    # EP bytes: every non-prefill shard, tokens_per_tile * hidden * 2 bytes per tile (engine.py:524)
+    assert outs[0]["ep_bytes"] == sum(c for k, (_, c) in enumerate(ranges) if k != 0) * 4 * 8 * 2
+    assert torch.equal(outs[0]["tokens"], outs[0]["expected"])
