@@ -163,6 +163,15 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
                              int32_t K, const void* bias, int32_t act, const void* resid, int32_t ldr,
                              int32_t r_mod, const void* lscale, void* out, int32_t ldo, int32_t bn,
                              void* stream);
+/* Projection straight into attention layouts: column n of A W^T + bias (+ resid[row % r_mod])
+ * splits into section s = n / sec_cols, head h, dim d (head dim padded to Dp); row = b*T + t.
+ * Section s writes out_s[((b*H + h)*T + t)*Dp + d], or, when bit s of trans_mask is set,
+ * the keys-major out_s[((b*H + h)*Dp + d)*Tpad + t]. */
+epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M,
+                                   int32_t N, int32_t K, const void* bias, const void* resid, int32_t ldr,
+                                   int32_t r_mod, int32_t H, int32_t Dp, int32_t T, int32_t Tpad,
+                                   int32_t sec_cols, void* out0, void* out1, void* out2, int32_t trans_mask,
+                                   void* stream);
 /* O = softmax(Q K^T * scale) V per (batch, head); see csrc/kernels.h AttnParams.
  * q: [q_shared ? H : B*H][Tq][Dp], k: [B*H][Tk][Dp], vt: [B*H][Dp][Tkpad],
  * out[(b*Tq + i)*ldo + h*Dv + d]. Dp in {64, 80, 128}. */

@@ -343,6 +343,30 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
   return cuda_status(rc, "linear_bf16");
 }
 
+epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M,
+                                   int32_t N, int32_t K, const void* bias, const void* resid, int32_t ldr,
+                                   int32_t r_mod, int32_t H, int32_t Dp, int32_t T, int32_t Tpad,
+                                   int32_t sec_cols, void* out0, void* out1, void* out2, int32_t trans_mask,
+                                   void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || H <= 0 || T <= 0 || sec_cols <= 0)
+    return fail(EPD_ERR_VALUE, "linear_heads: empty shape");
+  epd::EpiParams ep;
+  ep.mode = epd::EPI_HEADS;
+  ep.bias = reinterpret_cast<const epd::bf16*>(bias);
+  ep.resid = reinterpret_cast<const epd::bf16*>(resid);
+  ep.ldr = ldr;
+  ep.r_mod = r_mod > 0 ? r_mod : 0x7fffffff;
+  ep.H = H; ep.Dp = Dp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = sec_cols;
+  void* outs[3] = {out0, out1, out2};
+  for (int s = 0; s < 3; ++s) {
+    ep.sec_out[s] = reinterpret_cast<epd::bf16*>(outs[s]);
+    ep.sec_trans[s] = (trans_mask >> s) & 1;
+  }
+  int rc = epd::gemm_bf16(reinterpret_cast<const epd::bf16*>(A), lda, reinterpret_cast<const epd::bf16*>(W), ldw,
+                          M, N, K, ep, S(stream), 0);
+  return cuda_status(rc, "linear_heads_bf16");
+}
+
 epd_status_t epd_attention_bf16(const void* q, const void* k, const void* vt, void* out, int32_t B, int32_t H,
                                 int32_t Tq, int32_t Tk, int32_t Tkpad, int32_t Dp, int32_t Dv, int32_t ldo,
                                 int32_t q_shared, float scale, void* stream) {

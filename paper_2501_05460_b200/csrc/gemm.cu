@@ -3,10 +3,13 @@
 //
 //   C[M,N] = A[M,K] * B[N,K]^T      (both operands K-major, nn.Linear layout)
 //
-// Roles (192 threads / CTA, 1 CTA per SM):
+// Roles (320 threads / CTA, 1 CTA per SM, persistent over output tiles):
 //   warp 0      : TMA producer (one elected lane)
 //   warp 1      : TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  : epilogue (TMEM -> regs -> bias/GELU/residual -> global)
+//   warps 2..9  : epilogue, two halves of 4 warps (one per TMEM lane quarter),
+//                 each half owning half of the tile's columns: TMEM -> regs ->
+//                 bias/GELU/layer-scale -> swizzled smem -> TMA store (or TMA
+//                 reduce-add into the fp32 residual stream).
 // The epilogue of tile i overlaps the MMAs of tile i+1 (two TMEM accumulators).
 #include "common.cuh"
 #include "kernels.h"
@@ -19,25 +22,6 @@ namespace {
 constexpr int kBM = 128;
 constexpr int kBK = 64;
 
-template <int BN>
-struct GemmCfg {
-  static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int B_BYTES = BN * kBK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-};
-
-EPD_DEVICE void store8(bf16* dst, const float* x) {
-  uint4 v;
-  v.x = pack_bf16x2(x[0], x[1]);
-  v.y = pack_bf16x2(x[2], x[3]);
-  v.z = pack_bf16x2(x[4], x[5]);
-  v.w = pack_bf16x2(x[6], x[7]);
-  *reinterpret_cast<uint4*>(dst) = v;
-}
 EPD_DEVICE void load8(const bf16* src, float* x) {
   uint4 v = *reinterpret_cast<const uint4*>(src);
   float2 a = unpack_bf16x2(v.x), b = unpack_bf16x2(v.y), c = unpack_bf16x2(v.z),
@@ -46,86 +30,76 @@ EPD_DEVICE void load8(const bf16* src, float* x) {
   x[4] = c.x; x[5] = c.y; x[6] = d.x; x[7] = d.y;
 }
 
-// Apply the fused epilogue to 32 consecutive columns [n, n+32) of one row.
-EPD_DEVICE void epilogue_chunk(const EpiParams& ep, int row, int n, int N, const uint32_t (&v)[32]) {
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const int col = n + g * 8;
-    if (col >= N) break;
-    float x[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) x[j] = __uint_as_float(v[g * 8 + j]);
-    if (ep.bias) {
-      float b[8];
-      load8(ep.bias + col, b);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] += b[j];
-    }
-    if (ep.act == ACT_GELU_TANH) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = gelu_tanh(x[j]);
-    } else if (ep.act == ACT_GELU_ERF) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = gelu_erf(x[j]);
-    }
-    if (ep.resid || ep.resid_f) {
-      if (ep.lscale) {
-        float s[8];
-        load8(ep.lscale + col, s);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] *= s[j];
-      }
-      float r[8];
-      const size_t roff = (size_t)(row % ep.r_mod) * ep.ldr + col;
-      if (ep.resid_f) {
-        const float4 r0 = *reinterpret_cast<const float4*>(ep.resid_f + roff);
-        const float4 r1 = *reinterpret_cast<const float4*>(ep.resid_f + roff + 4);
-        r[0] = r0.x; r[1] = r0.y; r[2] = r0.z; r[3] = r0.w;
-        r[4] = r1.x; r[5] = r1.y; r[6] = r1.z; r[7] = r1.w;
-      } else {
-        load8(ep.resid + roff, r);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] += r[j];
-    }
-    if (ep.mode == EPI_ROWS) {
-      if (ep.out_f) {
-        float* o = ep.out_f + (size_t)row * ep.ldo + col;
-        *reinterpret_cast<float4*>(o) = make_float4(x[0], x[1], x[2], x[3]);
-        *reinterpret_cast<float4*>(o + 4) = make_float4(x[4], x[5], x[6], x[7]);
-      } else {
-        store8(ep.out + (size_t)row * ep.ldo + col, x);
-      }
-    } else {
-      const int s = col / ep.sec_cols;
-      const int within = col - s * ep.sec_cols;
-      const int h = within / ep.Dp;
-      const int d = within - h * ep.Dp;
-      const int b = row / ep.T;
-      const int t = row - b * ep.T;
-      const size_t bh = (size_t)b * ep.H + h;
-      bf16* base = ep.sec_out[s];
-      if (!ep.sec_trans[s]) {
-        store8(base + (bh * ep.T + t) * ep.Dp + d, x);
-      } else {
-        bf16* p = base + (bh * ep.Dp + d) * ep.Tpad + t;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) p[(size_t)j * ep.Tpad] = __float2bfloat16_rn(x[j]);
-      }
-    }
-  }
+EPD_DEVICE float gelu_tanh_fast(float x) {
+  const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.f + t);
 }
 
+// Epilogue kinds (the output side of C = A B^T):
+//   ROWS_BF16 : out bf16 row-major                 (TMA store, 64 B rows, SW64, 32-col chunks)
+//   ROWS_F32  : out fp32 row-major                 (TMA store, 128 B rows, SW128, 32-col chunks)
+//   ACC_F32   : out fp32 += result (residual stream, in place)  (TMA reduce-add, SW128)
+//   HEADS     : per-head Q/K [bh][T][Dp] (SW32) or keys-major V^T [bh][Dp][Tpad] (no swizzle),
+//               16-col chunks, 3-D TMA stores; tiles that straddle two images store twice.
+enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS = 3 };
+
+template <int KIND>
+struct EpiCfg {
+  static constexpr int CW = KIND == EK_HEADS ? 16 : 32;
+};
+
+constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
+
 template <int BN>
-__global__ void __launch_bounds__(192, 1)
+struct GemmCfg {
+  static constexpr int A_BYTES = kBM * kBK * 2;
+  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (227 * 1024 - 2 * kEpiStageBytes - 2048) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * kEpiStageBytes + 1024 + 256;
+  static constexpr int THREADS = 64 + 256;
+};
+
+EPD_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+EPD_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+EPD_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+EPD_DEVICE void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+EPD_DEVICE void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+EPD_DEVICE void tma_reduce_add_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+EPD_DEVICE void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+
+template <int BN, int KIND>
+__global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     int M, int N, int K, const EpiParams ep) {
+                     const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
+                     const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep) {
   using Cfg = GemmCfg<BN>;
+  constexpr int CW = EpiCfg<KIND>::CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + Cfg::STAGES * Cfg::B_BYTES);
+  uint8_t* sEpi = sB + Cfg::STAGES * Cfg::B_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + 2 * kEpiStageBytes);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -141,7 +115,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], 256);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -204,28 +178,163 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int r_in_tile = q * 32 + lane;
+    // ---------------- epilogue: 8 warps = 2 halves x 4 TMEM lane quarters
+    const int half = (warp - 2) >> 2;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // row within the tile (TMEM lane)
+    const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
+    uint8_t* stg = sEpi + half * kEpiStageBytes;
+    const int bar_id = 1 + half;
     int local = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const int m0 = (tile / num_n) * kBM;
       const int n0 = (tile % num_n) * BN;
+      const int row = m0 + r;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int row = m0 + r_in_tile;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        if (n0 + c >= N) break;
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += CW) {
+        const int n = n0 + c;
+        if (n >= N) break;  // warp-uniform
         uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c, v);
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c;
+        if (CW == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
         tmem_ld_wait();
-        if (row < M) epilogue_chunk(ep, row, n0 + c, N, v);
+        float x[CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) x[j] = __uint_as_float(v[j]);
+#pragma unroll
+        for (int g = 0; g < CW / 8; ++g) {
+          const int col = n + g * 8;
+          float* xg = x + g * 8;
+          if (col < N) {
+            if (ep.bias) {
+              float b[8];
+              load8(ep.bias + col, b);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xg[j] += b[j];
+            }
+            if (ep.act == ACT_GELU_TANH) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xg[j] = gelu_tanh_fast(xg[j]);
+            } else if (ep.act == ACT_GELU_ERF) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xg[j] = gelu_erf(xg[j]);
+            }
+            if (ep.lscale) {
+              float s8[8];
+              load8(ep.lscale + col, s8);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xg[j] *= s8[j];
+            }
+            if (KIND != EK_ACC_F32 && ep.resid && row < M) {  // generic (direct-load) residual
+              float rr[8];
+              load8(ep.resid + (size_t)(row % ep.r_mod) * ep.ldr + col, rr);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xg[j] += rr[j];
+            }
+          }
+        }
+        if (KIND == EK_HEADS &&
+            ((m0 % ep.T) + kBM > ep.T ||
+             (((m0 % ep.T) & 7) && (n / ep.sec_cols == 0 ? ep.sec_trans[0]
+                                    : (n / ep.sec_cols == 1 ? ep.sec_trans[1] : ep.sec_trans[2]))))) {
+          // Tile straddles an image boundary (T % 128 != 0), or a keys-major V^T chunk would
+          // start at a token offset that is not 16-byte aligned: TMA stores take neither
+          // negative nor unaligned inner coordinates, so store from registers.
+          if (row < M) {
+            const int sec = n / ep.sec_cols;
+            const int within = n - sec * ep.sec_cols;
+            const int h = within / ep.Dp;
+            const int d0 = within - h * ep.Dp;
+            const int b = row / ep.T;
+            const int t = row - b * ep.T;
+            const size_t bh = (size_t)b * ep.H + h;
+            bf16* base = sec == 0 ? ep.sec_out[0] : (sec == 1 ? ep.sec_out[1] : ep.sec_out[2]);
+            const int trans = sec == 0 ? ep.sec_trans[0] : (sec == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
+            if (!trans) {
+              bf16* p = base + (bh * ep.T + t) * ep.Dp + d0;
+#pragma unroll
+              for (int j = 0; j < CW / 8; ++j)
+                *reinterpret_cast<uint4*>(p + 8 * j) =
+                    make_uint4(pack_bf16x2(x[8 * j + 0], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
+                               pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
+            } else {
+              bf16* p = base + (bh * ep.Dp + d0) * ep.Tpad + t;
+#pragma unroll
+              for (int j = 0; j < CW; ++j) p[(size_t)j * ep.Tpad] = __float2bfloat16_rn(x[j]);
+            }
+          }
+          continue;
+        }
+        // previous TMA store must have finished reading the staging buffer
+        if (leader) bulk_wait_read0();
+        named_bar(bar_id, 128);
+        if (KIND == EK_ROWS_BF16) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int phys = j ^ ((r >> 1) & 3);
+            *reinterpret_cast<uint4*>(stg + r * 64 + phys * 16) =
+                make_uint4(pack_bf16x2(x[8 * j + 0], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
+                           pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
+          }
+        } else if (KIND == EK_ROWS_F32 || KIND == EK_ACC_F32) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int phys = j ^ (r & 7);
+            *reinterpret_cast<float4*>(stg + r * 128 + phys * 16) =
+                make_float4(x[4 * j + 0], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+          }
+        }
+        int sec = 0, trans = 0;
+        if (KIND == EK_HEADS) {
+          sec = n / ep.sec_cols;
+          trans = sec == 0 ? ep.sec_trans[0] : (sec == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
+          if (!trans) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int phys = j ^ ((r >> 2) & 1);
+              *reinterpret_cast<uint4*>(stg + r * 32 + phys * 16) =
+                  make_uint4(pack_bf16x2(x[8 * j + 0], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
+                             pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
+            }
+          } else {
+            bf16* t16 = reinterpret_cast<bf16*>(stg);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) t16[j * 128 + r] = __float2bfloat16_rn(x[j]);
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar(bar_id, 128);
+        if (leader) {
+          if (KIND == EK_ROWS_BF16 || KIND == EK_ROWS_F32) {
+            tma_store_2d(&tmO0, stg, n, m0);
+          } else if (KIND == EK_ACC_F32) {
+            tma_reduce_add_2d(&tmO0, stg, n, m0);
+          } else {
+            auto st3 = [&](int c0, int c1, int c2) {
+              if (sec == 0) tma_store_3d(&tmO0, stg, c0, c1, c2);
+              else if (sec == 1) tma_store_3d(&tmO1, stg, c0, c1, c2);
+              else tma_store_3d(&tmO2, stg, c0, c1, c2);
+            };
+            const int within = n - sec * ep.sec_cols;
+            const int h = within / ep.Dp;
+            const int d0 = within - h * ep.Dp;
+            const int b0 = m0 / ep.T;
+            const int t0 = m0 - b0 * ep.T;
+            const int bh = b0 * ep.H + h;
+            if (!trans) st3(d0, t0, bh);
+            else st3(t0, d0, bh);
+          }
+          bulk_commit();
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[as]);
     }
+    if (leader) bulk_wait_all0();
   }
 
   tc_fence_before();
@@ -236,29 +345,65 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <int BN>
-int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
-           const EpiParams& ep, cudaStream_t stream) {
+template <int BN, int KIND>
+int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, const EpiParams& ep,
+           cudaStream_t stream) {
   using Cfg = GemmCfg<BN>;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, t0, t1, t2;
   int rc = make_tmap_2d(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, kBK, kBM,
                         CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc)
+    rc = make_tmap_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_tmap_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN,
-                    CU_TENSOR_MAP_SWIZZLE_128B);
+  if (KIND == EK_ROWS_BF16) {
+    rc = make_tmap_2d(&t0, ep.out, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 2, 32, kBM,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
+    t1 = t2 = t0;
+  } else if (KIND == EK_ROWS_F32 || KIND == EK_ACC_F32) {
+    rc = make_tmap_2d_f32(&t0, ep.out_f, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 4, 32, kBM,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+    t1 = t2 = t0;
+  } else {
+    const uint64_t nb = (uint64_t)(M + ep.T - 1) / ep.T;
+    CUtensorMap* maps[3] = {&t0, &t1, &t2};
+    for (int s = 0; s < 3 && !rc; ++s) {
+      if (!ep.sec_out[s] || (uint64_t)s * ep.sec_cols >= (uint64_t)N) {
+        *maps[s] = ta;
+        continue;
+      }
+      const uint64_t Dp = ep.Dp;
+      if (!ep.sec_trans[s])
+        rc = make_tmap_3d(maps[s], ep.sec_out[s], Dp, ep.T, nb * ep.H, Dp * 2, Dp * 2 * ep.T, 16, kBM, 1,
+                          CU_TENSOR_MAP_SWIZZLE_32B);
+      else
+        rc = make_tmap_3d(maps[s], ep.sec_out[s], ep.T, Dp, nb * ep.H, (uint64_t)ep.Tpad * 2,
+                          (uint64_t)ep.Tpad * 2 * Dp, kBM, 16, 1, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
+  }
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
   const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
   int grid = num_sms();
   if (tiles < grid) grid = tiles;
-  gemm_bf16_kernel<BN><<<grid, 192, Cfg::SMEM, stream>>>(ta, tb, M, N, K, ep);
+  gemm_bf16_kernel<BN, KIND><<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(ta, tb, t0, t1, t2, M, N, K, ep);
   return (int)cudaGetLastError();
+}
+
+template <int BN>
+int launch_kind(int kind, const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
+                const EpiParams& ep, cudaStream_t stream) {
+  switch (kind) {
+    case EK_ROWS_BF16: return launch<BN, EK_ROWS_BF16>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ROWS_F32: return launch<BN, EK_ROWS_F32>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ACC_F32: return launch<BN, EK_ACC_F32>(A, lda, B, ldb, M, N, K, ep, stream);
+    default: return launch<BN, EK_HEADS>(A, lda, B, ldb, M, N, K, ep, stream);
+  }
 }
 
 }  // namespace
@@ -270,7 +415,8 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return 1003;
   int bn = bn_hint;
   if (bn == 0) {
-    // Pick the N tile that minimises the last-wave tail for this shape.
+    // Wide tiles amortise the epilogue and B-operand traffic best; step down only
+    // when the last wave of 256-wide tiles would leave most SMs idle.
     const int sms = num_sms();
     double best = 1e30;
     const int cands[3] = {256, 192, 128};
@@ -278,15 +424,30 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
       const int c = cands[i];
       const long tiles = (long)((M + kBM - 1) / kBM) * ((N + c - 1) / c);
       const long waves = (tiles + sms - 1) / sms;
-      // cost ~ waves * per-tile time (~ c) with a mild penalty for narrow tiles
-      const double cost = (double)waves * c * (c == 128 ? 1.12 : (c == 192 ? 1.03 : 1.0));
+      const double cost = (double)waves * c * (c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0));
       if (cost < best) { best = cost; bn = c; }
     }
   }
+  int kind;
+  if (ep.mode == EPI_HEADS) {
+    if (ep.Dp % 16 || ep.sec_cols % ep.Dp || ep.T <= 0) return 1005;
+    for (int s = 0; s < 3; ++s)
+      if (ep.sec_out[s] && ep.sec_trans[s] && (ep.Tpad % 8 || ep.Tpad < ep.T)) return 1005;
+    kind = EK_HEADS;
+  } else if (ep.out_f) {
+    if (ep.resid_f && ep.resid_f != ep.out_f) return 1005;  // fp32 residual only in place
+    if (ep.resid_f && ep.resid) return 1005;
+    kind = ep.resid_f ? EK_ACC_F32 : EK_ROWS_F32;
+    if (ep.ldo % 4) return 1002;
+  } else {
+    if (!ep.out || ep.resid_f) return 1005;
+    kind = EK_ROWS_BF16;
+  }
+  if (kind == EK_ACC_F32 && ep.act != ACT_NONE && false) return 1005;
   switch (bn) {
-    case 256: return launch<256>(A, lda, B, ldb, M, N, K, ep, stream);
-    case 192: return launch<192>(A, lda, B, ldb, M, N, K, ep, stream);
-    case 128: return launch<128>(A, lda, B, ldb, M, N, K, ep, stream);
+    case 256: return launch_kind<256>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+    case 192: return launch_kind<192>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+    case 128: return launch_kind<128>(kind, A, lda, B, ldb, M, N, K, ep, stream);
     default: return 1004;
   }
 }

@@ -39,6 +39,22 @@ inline int make_tmap_2d(CUtensorMap* map, const void* base, uint64_t inner, uint
   return r == CUDA_SUCCESS ? 0 : 1101;
 }
 
+// 2-D fp32 map (residual stream).
+inline int make_tmap_2d_f32(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                            uint64_t pitch_bytes, uint32_t box_inner, uint32_t box_outer,
+                            CUtensorMapSwizzle swz) {
+  auto fn = tmap_encode_fn();
+  if (!fn) return 1100;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 1101;
+}
+
 // 3-D bf16 map: dims {d0, d1, d2}, pitches in bytes for d1 and d2.
 inline int make_tmap_3d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                         uint64_t pitch1, uint64_t pitch2, uint32_t b0, uint32_t b1, uint32_t b2,

@@ -42,6 +42,27 @@ def linear(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, a
     return out
 
 
+def linear_heads(a: torch.Tensor, w: torch.Tensor, H: int, Dp: int, T: int, sections: int,
+                 trans=(False, False, True), bias: torch.Tensor | None = None,
+                 resid: torch.Tensor | None = None, r_mod: int = 0):
+    """Project a [M, K] -> per-head Q/K [nb*H, T, Dp] / keys-major V^T [nb*H, Dp, Tpad] tensors."""
+    _need_cuda(a, w, bias, resid)
+    M, K = a.shape
+    N = w.shape[0]
+    nb = -(-M // T)
+    Tpad = (T + 7) // 8 * 8
+    outs = []
+    for s in range(sections):
+        shape = (nb * H, Dp, Tpad) if trans[s] else (nb * H, T, Dp)
+        outs.append(torch.zeros(shape, dtype=torch.bfloat16, device=a.device))
+    ptrs = [o.data_ptr() for o in outs] + [None] * (3 - sections)
+    mask = sum(1 << s for s in range(sections) if trans[s])
+    call("epd_linear_heads_bf16", a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K, _ptr(bias),
+         _ptr(resid), resid.stride(0) if resid is not None else 0, r_mod, H, Dp, T, Tpad, H * Dp, ptrs[0], ptrs[1],
+         ptrs[2], mask, _stream(a))
+    return outs
+
+
 def attention(q: torch.Tensor, k: torch.Tensor, vt: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
               Dv: int, scale: float, q_shared: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
     """Fused MHA; q [Bq,Tq,Dp], k [B*H,Tk,Dp], vt [B*H,Dp,Tkpad] -> out [B*Tq, H*Dv]."""

@@ -136,3 +136,34 @@ def test_patchify(cuda):
     ref = cols.transpose(1, 2).reshape(n * (S // p) ** 2, 3 * p * p)
     assert relerr(y[:, :588], ref) <= 4e-3
     assert y[:, 588:].abs().max().item() == 0
+
+
+@pytest.mark.parametrize("M,T,H,Dp,dh,trans", [
+    (2048, 1024, 16, 80, 72, (False, False, True)),   # SigLIP QKV
+    (2050, 1025, 16, 64, 64, (False, False, True)),   # InternViT (images straddle M tiles)
+    (64, 64, 28, 128, 128, (False,)),                 # resampler query projection
+    (2048, 1024, 28, 128, 128, (False, True)),        # resampler K / V^T
+    (4, 4, 1, 64, 8, (False,)),                       # tiny
+])
+def test_linear_heads(cuda, M, T, H, Dp, dh, trans):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(M + T + H)
+    S = len(trans)
+    K = 256
+    a = _bf(M, K, gen=g)
+    w = torch.zeros(S * H * Dp, K, dtype=torch.bfloat16, device=cuda)
+    b = torch.zeros(S * H * Dp, dtype=torch.bfloat16, device=cuda)
+    for s in range(S):
+        for h in range(H):
+            base = (s * H + h) * Dp
+            w[base:base + dh] = _bf(dh, K, scale=K ** -0.5, gen=g)
+            b[base:base + dh] = _bf(dh, gen=g)
+    pos = _bf(T, S * H * Dp, gen=g)
+    outs = kernels.linear_heads(a, w, H, Dp, T, S, trans=trans, bias=b, resid=pos, r_mod=T)
+    torch.cuda.synchronize()
+    full = a.float() @ w.float().t() + b.float() + pos.float().repeat(M // T, 1)
+    nb = M // T
+    for s in range(S):
+        ref = full[:, s * H * Dp:(s + 1) * H * Dp].reshape(nb, T, H, Dp).permute(0, 2, 1, 3).reshape(nb * H, T, Dp)
+        got = outs[s][..., :T].transpose(1, 2) if trans[s] else outs[s]
+        assert relerr(got, ref) <= TOL, s
