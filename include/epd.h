@@ -173,10 +173,10 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
                                    int32_t sec_cols, void* out0, void* out1, void* out2, int32_t trans_mask,
                                    void* stream);
 /* O = softmax(Q K^T * scale) V per (batch, head); see csrc/kernels.h AttnParams.
- * q: [q_shared ? H : B*H][Tq][Dp], k: [B*H][Tk][Dp], vt: [B*H][Dp][Tkpad],
+ * q: [q_shared ? H : B*H][Tq][Dp], k and v: [B*H][Tk][Dp],
  * out[(b*Tq + i)*ldo + h*Dv + d]. Dp in {64, 80, 128}. */
-epd_status_t epd_attention_bf16(const void* q, const void* k, const void* vt, void* out, int32_t B,
-                                int32_t H, int32_t Tq, int32_t Tk, int32_t Tkpad, int32_t Dp, int32_t Dv,
+epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, void* out, int32_t B,
+                                int32_t H, int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv,
                                 int32_t ldo, int32_t q_shared, float scale, void* stream);
 epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
                                 const void* beta, int32_t rows, int32_t D, float eps, void* stream);

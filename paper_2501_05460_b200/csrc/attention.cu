@@ -1,15 +1,20 @@
-// Fused multi-head attention (bidirectional, no causal mask) for sm_100a.
+// Fused multi-head attention (bidirectional) for sm_100a, FA4-style.
 //
-// One CTA = 128 query rows of one (batch, head). Per 128-key block j:
-//   S_j  = Q K_j^T           tcgen05.mma, M=128 N=128 K=Dp, fp32 in TMEM
-//   P_j  = exp2(S_j*c - m_j) softmax warps: TMEM -> regs -> bf16 P in smem (SW128)
-//   O_j  = P_j V_j           tcgen05.mma, M=128 N=Dp K=128, fp32 in TMEM
-//   acc  = acc*alpha_j + O_j softmax warps, fp32 registers (online softmax)
-// S_{j+1} is issued before O_j so the tensor core overlaps the softmax.
+// One CTA = NQ (1 or 2) tiles of 128 query rows of one (batch, head); the
+// tiles share every K/V block. Per 128-key block j and query tile g:
+//   S_g  = Q_g K_j^T          tcgen05.mma M=128 N=128 K=Dp  -> TMEM (fp32)
+//   P_g  = exp2(S_g*c - m_g)  softmax warpgroup g (TMEM -> regs -> bf16 P, SW128 smem)
+//   O_g += P_g V_j            tcgen05.mma M=128 N=Dp K=128  -> TMEM (fp32), V MN-major
+// The running max m_g is only raised (and O_g rescaled in TMEM) when a row's
+// max grows by more than 2^8, so most blocks need no correction pass.
+// While warpgroup g computes softmax, the tensor core runs the other group's
+// S / PV MMAs.
 //
-// Roles (192 threads): warp 0 TMA, warp 1 TMEM alloc + MMA issue, warps 2..5 softmax.
-// Head dims that are not a multiple of 64 (SigLIP 72 -> padded 80) are split
-// into a 64-wide 128B-swizzled atom plus a 16-wide 32B-swizzled atom.
+// Warps: 0 TMA, 1 TMEM alloc + MMA issue, 2..5 softmax group 0, 6..9 group 1.
+// Layouts: Q, K, V all [bh][T][Dp] bf16 (Dp = head dim zero-padded to a
+// multiple of 16). Q/K are K-major operands (64-wide SW128 atoms + a 16-wide
+// SW32 tail when Dp % 64 != 0); V is the MN-major B operand from 16-wide
+// SW32 atoms (LBO = 4 KB between atoms, SBO = 256 B between 8-key groups).
 #include "common.cuh"
 #include "kernels.h"
 #include "tmap.h"
@@ -18,63 +23,71 @@ namespace epd {
 
 namespace {
 
-template <int DP>
-struct AttnCfg {
-  static constexpr int QROWS = 128;
-  static constexpr int KB = 128;  // keys per block
-  static constexpr bool TAIL32 = (DP % 64) != 0;          // 16-wide 32B-swizzled tail atom
-  static constexpr int MAIN_ATOMS = DP / 64;              // full 64-wide SW128 atoms
-  static constexpr int QK_ATOM_BYTES = 128 * 128;         // 128 rows x 128 B
-  static constexpr int QK_TAIL_BYTES = TAIL32 ? 128 * 32 : 0;
-  static constexpr int QK_BYTES = MAIN_ATOMS * QK_ATOM_BYTES + QK_TAIL_BYTES;  // = 128*DP*2
-  static constexpr int QK_BYTES_AL = (QK_BYTES + 1023) / 1024 * 1024;
-  static constexpr int V_ATOM_BYTES = DP * 128;           // DP rows x 64 keys x 2 B
-  static constexpr int V_BYTES = 2 * V_ATOM_BYTES;
-  static constexpr int P_ATOM_BYTES = 128 * 128;
-  static constexpr int P_BYTES = 2 * P_ATOM_BYTES;
+EPD_DEVICE float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+EPD_DEVICE void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+EPD_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int DP, int NQ>
+struct Cfg {
+  static constexpr int KB = 128;                       // keys per block
+  static constexpr int MAIN = DP / 64;                 // 64-wide SW128 atoms of Q/K
+  static constexpr bool TAIL = (DP % 64) != 0;         // 16-wide SW32 tail (DP % 64 == 16)
+  static constexpr int QK_ATOM = 128 * 128;            // 128 rows x 128 B
+  static constexpr int QK_BYTES = 128 * DP * 2;
+  static constexpr int QK_AL = (QK_BYTES + 1023) / 1024 * 1024;
+  static constexpr int V_ATOM = 128 * 32;              // 128 keys x 16 dims x 2 B
+  static constexpr int V_BYTES = (DP / 16) * V_ATOM;
+  static constexpr int P_ATOM = 128 * 128;
+  static constexpr int P_BYTES = 2 * P_ATOM;           // 128 rows x 128 keys bf16
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + QK_BYTES_AL;
-  static constexpr int OFF_V = OFF_K + 2 * QK_BYTES_AL;
+  static constexpr int OFF_K = OFF_Q + NQ * QK_AL;
+  static constexpr int OFF_V = OFF_K + 2 * QK_AL;
   static constexpr int OFF_P = OFF_V + 2 * V_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int OFF_BAR = OFF_P + NQ * P_BYTES;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int KSTEPS_QK = DP / 16;
+  static constexpr int THREADS = 64 + NQ * 128;
 };
 
-template <int DP>
-__global__ void __launch_bounds__(192, 1)
+template <int DP, int NQ>
+__global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     attention_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQt,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmKt,
                      const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
-  using C = AttnCfg<DP>;
+  using C = Cfg<DP, NQ>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem + C::OFF_Q;
-  uint8_t* sK = smem + C::OFF_K;
-  uint8_t* sV = smem + C::OFF_V;
-  uint8_t* sP = smem + C::OFF_P;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;   // [2]
   uint64_t* k_empty = bars + 3;  // [2]
   uint64_t* v_full = bars + 5;   // [2]
   uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2]
-  uint64_t* s_free = bars + 11;  // [2]
-  uint64_t* p_full = bars + 13;  // [2]
-  uint64_t* p_free = bars + 15;  // [2]
-  uint64_t* o_full = bars + 17;  // [2]
-  uint64_t* o_free = bars + 19;  // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* s_full = bars + 9;   // [NQ]
+  uint64_t* p_ready = bars + 11; // [NQ]
+  uint64_t* o_done = bars + 13;  // [NQ]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 15);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int qtile = blockIdx.x;
   const int h = blockIdx.y;
   const int b = blockIdx.z;
   const int bh = b * p.H + h;
   const int qbatch = p.q_shared ? h : bh;
-  const int q0 = qtile * C::QROWS;
+  const int q0 = blockIdx.x * (NQ * 128);
+  const int rem = p.Tq - q0;
+  const int nq = rem > 128 ? NQ : 1;  // query tiles with at least one valid row
   const int nkb = (p.Tk + C::KB - 1) / C::KB;
 
   if (warp == 0 && lane == 0) {
@@ -84,12 +97,11 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&p_free[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_free[i], 128);
+    }
+    for (int g = 0; g < NQ; ++g) {
+      mbar_init(&s_full[g], 1);
+      mbar_init(&p_ready[g], 128);
+      mbar_init(&o_done[g], 1);
     }
     fence_barrier_init();
   }
@@ -98,178 +110,189 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  // TMEM columns: S buffers at [0,128) and [128,256); O buffers at 256 and 384.
+  // TMEM columns: S_g at [g*128, g*128+128), O_g at [256 + g*128, 256 + g*128 + DP)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, C::QK_BYTES);
-      for (int a = 0; a < C::MAIN_ATOMS; ++a)
-        tma_load_3d(sQ + a * C::QK_ATOM_BYTES, &tmQ, q_full, a * 64, q0, qbatch);
-      if (C::TAIL32) tma_load_3d(sQ + C::MAIN_ATOMS * C::QK_ATOM_BYTES, &tmQt, q_full, C::MAIN_ATOMS * 64, q0, qbatch);
+      mbar_arrive_expect_tx(q_full, nq * C::QK_BYTES);
+      for (int g = 0; g < nq; ++g) {
+        uint8_t* qd = smem + C::OFF_Q + g * C::QK_AL;
+        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(qd + a * C::QK_ATOM, &tmQ, q_full, a * 64, q0 + g * 128, qbatch);
+        if (C::TAIL) tma_load_3d(qd + C::MAIN * C::QK_ATOM, &tmQt, q_full, C::MAIN * 64, q0 + g * 128, qbatch);
+      }
       for (int j = 0; j < nkb; ++j) {
         const int s = j & 1;
         const uint32_t ph = (j >> 1) & 1;
         mbar_wait(&k_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&k_full[s], C::QK_BYTES);
-        uint8_t* kd = sK + s * C::QK_BYTES_AL;
-        for (int a = 0; a < C::MAIN_ATOMS; ++a)
-          tma_load_3d(kd + a * C::QK_ATOM_BYTES, &tmK, &k_full[s], a * 64, j * C::KB, bh);
-        if (C::TAIL32) tma_load_3d(kd + C::MAIN_ATOMS * C::QK_ATOM_BYTES, &tmKt, &k_full[s], C::MAIN_ATOMS * 64, j * C::KB, bh);
+        uint8_t* kd = smem + C::OFF_K + s * C::QK_AL;
+        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(kd + a * C::QK_ATOM, &tmK, &k_full[s], a * 64, j * C::KB, bh);
+        if (C::TAIL) tma_load_3d(kd + C::MAIN * C::QK_ATOM, &tmKt, &k_full[s], C::MAIN * 64, j * C::KB, bh);
         mbar_wait(&v_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
-        uint8_t* vd = sV + s * C::V_BYTES;
-        tma_load_3d(vd, &tmV, &v_full[s], j * C::KB, 0, bh);
-        tma_load_3d(vd + C::V_ATOM_BYTES, &tmV, &v_full[s], j * C::KB + 64, 0, bh);
+        uint8_t* vd = smem + C::OFF_V + s * C::V_BYTES;
+        for (int a = 0; a < DP / 16; ++a) tma_load_3d(vd + a * C::V_ATOM, &tmV, &v_full[s], a * 16, j * C::KB, bh);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KB);
-      constexpr uint32_t idesc_o = make_idesc_bf16(128, DP);
-      const uint32_t q_addr = smem_u32(sQ);
+      constexpr uint32_t idesc_o = make_idesc_bf16(128, DP) | (1u << 16);  // B (V) is MN-major
       mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
+      auto issue_s = [&](int g, int j) {
         const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_full[s], ph);
-        mbar_wait(&s_free[s], ph ^ 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + s * C::QK_BYTES_AL);
+        const uint32_t q_addr = smem_u32(smem + C::OFF_Q + g * C::QK_AL);
+        const uint32_t k_addr = smem_u32(smem + C::OFF_K + s * C::QK_AL);
 #pragma unroll
-        for (int kk = 0; kk < C::KSTEPS_QK; ++kk) {
+        for (int kk = 0; kk < DP / 16; ++kk) {
           const int atom = kk >> 2;
           uint64_t ad, bd;
-          if (atom < C::MAIN_ATOMS) {
-            ad = make_sdesc(q_addr + atom * C::QK_ATOM_BYTES + (kk & 3) * 32, 1024, 2);
-            bd = make_sdesc(k_addr + atom * C::QK_ATOM_BYTES + (kk & 3) * 32, 1024, 2);
+          if (atom < C::MAIN) {
+            ad = make_sdesc(q_addr + atom * C::QK_ATOM + (kk & 3) * 32, 1024, 2);
+            bd = make_sdesc(k_addr + atom * C::QK_ATOM + (kk & 3) * 32, 1024, 2);
           } else {
-            ad = make_sdesc(q_addr + C::MAIN_ATOMS * C::QK_ATOM_BYTES, 256, 6);
-            bd = make_sdesc(k_addr + C::MAIN_ATOMS * C::QK_ATOM_BYTES, 256, 6);
+            ad = make_sdesc(q_addr + C::MAIN * C::QK_ATOM, 256, 6);
+            bd = make_sdesc(k_addr + C::MAIN * C::QK_ATOM, 256, 6);
           }
-          umma_bf16(tmem + s * 128, ad, bd, idesc_s, kk != 0);
+          umma_bf16(tmem + g * 128, ad, bd, idesc_s, kk != 0);
         }
-        tc_commit(&s_full[s]);
-        tc_commit(&k_empty[s]);
+        tc_commit(&s_full[g]);
       };
-      issue_s(0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      for (int g = 0; g < nq; ++g) issue_s(g, 0);
+      tc_commit(&k_empty[0]);
       for (int j = 0; j < nkb; ++j) {
-        if (j + 1 < nkb) issue_s(j + 1);
         const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&p_full[s], ph);
-        mbar_wait(&v_full[s], ph);
-        mbar_wait(&o_free[s], ph ^ 1);
-        tc_fence_after();
-        const uint32_t p_addr = smem_u32(sP + s * C::P_BYTES);
-        const uint32_t v_addr = smem_u32(sV + s * C::V_BYTES);
+        for (int g = 0; g < nq; ++g) {
+          mbar_wait(&p_ready[g], j & 1);
+          if (j + 1 < nkb) {
+            if (g == 0) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_s(g, j + 1);
+            if (g == nq - 1) tc_commit(&k_empty[(j + 1) & 1]);
+          }
+          if (g == 0) mbar_wait(&v_full[s], (j >> 1) & 1);
+          tc_fence_after();
+          const uint32_t p_addr = smem_u32(smem + C::OFF_P + g * C::P_BYTES);
+          const uint32_t v_addr = smem_u32(smem + C::OFF_V + s * C::V_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const int atom = kk >> 2;
-          const uint64_t ad = make_sdesc(p_addr + atom * C::P_ATOM_BYTES + (kk & 3) * 32, 1024, 2);
-          const uint64_t bd = make_sdesc(v_addr + atom * C::V_ATOM_BYTES + (kk & 3) * 32, 1024, 2);
-          umma_bf16(tmem + 256 + s * 128, ad, bd, idesc_o, kk != 0);
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t ad = make_sdesc(p_addr + (kk >> 2) * C::P_ATOM + (kk & 3) * 32, 1024, 2);
+            // MN-major SW32: start at key row kk*16 (512 B), LBO = 4 KB (next 16 dims), SBO = 256 B
+            const uint64_t bd = make_sdesc_lbo(v_addr + kk * 512, C::V_ATOM, 256, 6);
+            umma_bf16(tmem + 256 + g * 128, ad, bd, idesc_o, (j | kk) != 0);
+          }
+          tc_commit(&o_done[g]);
         }
-        tc_commit(&o_full[s]);
         tc_commit(&v_empty[s]);
-        tc_commit(&p_free[s]);
       }
     }
   } else {
-    // ---------------- softmax / correction warps: one query row per thread
+    // ---------------- softmax warpgroups: one query row per thread
+    const int g = (warp - 2) >> 2;
     const int qq = warp & 3;
     const int r = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
+    const uint32_t s_tm = tmem + lane_off + g * 128;
+    const uint32_t o_tm = tmem + lane_off + 256 + g * 128;
     const float c = p.scale * 1.4426950408889634f;
-    float m = -INFINITY, l = 0.f, alpha_pend = 0.f;
-    float acc[DP];
+    if (g < nq) {
+      float m_used = -INFINITY, l = 0.f;
+      uint8_t* prow = smem + C::OFF_P + g * C::P_BYTES + r * 128;
+      for (int j = 0; j < nkb; ++j) {
+        const int kvalid = p.Tk - j * C::KB;
+        mbar_wait(&s_full[g], j & 1);
+        tc_fence_after();
+        uint32_t sv[128];
 #pragma unroll
-    for (int i = 0; i < DP; ++i) acc[i] = 0.f;
-
-    auto consume_o = [&](int j, float alpha) {
-      const int s = j & 1;
-      mbar_wait(&o_full[s], (j >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < DP; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(tmem + lane_off + 256 + s * 128 + c0, v);
+        for (int c0 = 0; c0 < 128; c0 += 32) tmem_ld32(s_tm + c0, *reinterpret_cast<uint32_t(*)[32]>(sv + c0));
         tmem_ld_wait();
+        float mx = -INFINITY;
+        if (kvalid >= 128) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[c0 + i] = acc[c0 + i] * alpha + __uint_as_float(v[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(&o_free[s]);
-    };
-
-    for (int j = 0; j < nkb; ++j) {
-      const int s = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      const int kvalid = p.Tk - j * C::KB;  // keys >= kvalid are padding
-      mbar_wait(&s_full[s], ph);
-      tc_fence_after();
-      const uint32_t sbase = tmem + lane_off + s * 128;
-      float mx = -INFINITY;
+          for (int i = 0; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(sv[i]));
+        } else {
 #pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(sbase + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c0 + i < kvalid) mx = fmaxf(mx, __uint_as_float(v[i]));
-      }
-      const float m_new = fmaxf(m, mx * c);
-      const float alpha = exp2f(m - m_new);  // 0 on the first block
-      mbar_wait(&p_free[s], ph ^ 1);
-      float rs = 0.f;
-      uint8_t* prow = sP + s * C::P_BYTES + r * 128;
-#pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(sbase + c0, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float e0 = (c0 + i < kvalid) ? exp2f(__uint_as_float(v[i]) * c - m_new) : 0.f;
-          const float e1 = (c0 + i + 1 < kvalid) ? exp2f(__uint_as_float(v[i + 1]) * c - m_new) : 0.f;
-          rs += e0 + e1;
-          pk[i >> 1] = pack_bf16x2(e0, e1);
+          for (int i = 0; i < 128; ++i)
+            if (i < kvalid) mx = fmaxf(mx, __uint_as_float(sv[i]));
         }
-        const int atom = c0 >> 6;
-        uint8_t* arow = prow + atom * C::P_ATOM_BYTES;
+        const float m_new = fmaxf(m_used, mx * c);
+        if (j == 0) {
+          m_used = m_new;
+        } else {
+          mbar_wait(&o_done[g], (j - 1) & 1);  // PV of block j-1 done: P buffer free, O stable
+          tc_fence_after();
+          const bool need = m_new > m_used + 8.f;
+          if (__any_sync(0xffffffffu, need)) {
+            const float alpha = need ? ex2(m_used - m_new) : 1.f;
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int chunk = ((c0 & 63) >> 3) + q4;  // 16-byte chunk within the 128 B row
-          const int phys = chunk ^ (r & 7);
-          *reinterpret_cast<uint4*>(arow + phys * 16) =
-              make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+            for (int c0 = 0; c0 < DP; c0 += 16) {
+              uint32_t o[16];
+              tmem_ld16(o_tm + c0, o);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st16(o_tm + c0, o);
+            }
+            tmem_st_wait();
+            if (need) {
+              l *= alpha;
+              m_used = m_new;
+            }
+          }
         }
+        const float nm = -m_used;
+        float rs = 0.f;
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), c, nm));
+            float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), c, nm));
+            if (kvalid < 128) {
+              if (c0 + i >= kvalid) e0 = 0.f;
+              if (c0 + i + 1 >= kvalid) e1 = 0.f;
+            }
+            rs += e0 + e1;
+            pk[i >> 1] = pack_bf16x2(e0, e1);
+          }
+          uint8_t* arow = prow + (c0 >> 6) * C::P_ATOM;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const int chunk = ((c0 & 63) >> 3) + q4;
+            *reinterpret_cast<uint4*>(arow + ((chunk ^ (r & 7)) * 16)) =
+                make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+          }
+        }
+        l += rs;
+        tc_fence_before();
+        fence_proxy_async_smem();
+        mbar_arrive(&p_ready[g]);
       }
-      tc_fence_before();
-      mbar_arrive(&s_free[s]);
-      fence_proxy_async_smem();
-      mbar_arrive(&p_full[s]);
-      l = l * alpha + rs;
-      m = m_new;
-      if (j >= 1) consume_o(j - 1, alpha_pend);
-      alpha_pend = alpha;
-    }
-    consume_o(nkb - 1, alpha_pend);
-
-    const int qrow = q0 + r;
-    if (qrow < p.Tq) {
+      mbar_wait(&o_done[g], (nkb - 1) & 1);
+      tc_fence_after();
+      const int qrow = q0 + g * 128 + r;
       const float inv = 1.f / l;
       bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv;
 #pragma unroll
-      for (int d = 0; d < DP; d += 8) {
-        if (d < p.Dv) {
-          uint4 v;
-          v.x = pack_bf16x2(acc[d + 0] * inv, acc[d + 1] * inv);
-          v.y = pack_bf16x2(acc[d + 2] * inv, acc[d + 3] * inv);
-          v.z = pack_bf16x2(acc[d + 4] * inv, acc[d + 5] * inv);
-          v.w = pack_bf16x2(acc[d + 6] * inv, acc[d + 7] * inv);
-          *reinterpret_cast<uint4*>(dst + d) = v;
+      for (int c0 = 0; c0 < DP; c0 += 16) {
+        uint32_t o[16];
+        tmem_ld16(o_tm + c0, o);
+        tmem_ld_wait();
+        if (qrow < p.Tq) {
+#pragma unroll
+          for (int d = 0; d < 16; d += 8) {
+            if (c0 + d < p.Dv) {
+              uint4 v;
+              v.x = pack_bf16x2(__uint_as_float(o[d + 0]) * inv, __uint_as_float(o[d + 1]) * inv);
+              v.y = pack_bf16x2(__uint_as_float(o[d + 2]) * inv, __uint_as_float(o[d + 3]) * inv);
+              v.z = pack_bf16x2(__uint_as_float(o[d + 4]) * inv, __uint_as_float(o[d + 5]) * inv);
+              v.w = pack_bf16x2(__uint_as_float(o[d + 6]) * inv, __uint_as_float(o[d + 7]) * inv);
+              *reinterpret_cast<uint4*>(dst + c0 + d) = v;
+            }
+          }
         }
       }
     }
@@ -283,37 +306,28 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <int DP>
+template <int DP, int NQ>
 int launch_attn(const AttnParams& p, cudaStream_t stream) {
-  using C = AttnCfg<DP>;
-  const int Bq = p.q_shared ? p.H : p.B * p.H;
+  using C = Cfg<DP, NQ>;
+  const uint64_t Bq = p.q_shared ? p.H : (uint64_t)p.B * p.H;
+  const uint64_t Bk = (uint64_t)p.B * p.H;
+  const uint64_t pitch = (uint64_t)DP * 2;
   CUtensorMap mq, mqt, mk, mkt, mv;
-  const uint64_t qk_pitch1 = (uint64_t)DP * 2;
-  int rc = make_tmap_3d(&mq, p.q, DP, p.Tq, Bq, qk_pitch1, qk_pitch1 * p.Tq, 64, 128, 1,
-                        CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = make_tmap_3d(&mk, p.k, DP, p.Tk, (uint64_t)p.B * p.H, qk_pitch1, qk_pitch1 * p.Tk,
-                             64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc && C::TAIL32) {
-    rc = make_tmap_3d(&mqt, p.q, DP, p.Tq, Bq, qk_pitch1, qk_pitch1 * p.Tq, 16, 128, 1,
-                      CU_TENSOR_MAP_SWIZZLE_32B);
-    if (!rc) rc = make_tmap_3d(&mkt, p.k, DP, p.Tk, (uint64_t)p.B * p.H, qk_pitch1,
-                               qk_pitch1 * p.Tk, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
-  } else {
-    mqt = mq;
-    mkt = mk;
-  }
-  if (!rc) rc = make_tmap_3d(&mv, p.vt, p.Tk, DP, (uint64_t)p.B * p.H, (uint64_t)p.Tkpad * 2,
-                             (uint64_t)p.Tkpad * 2 * DP, 64, DP, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  int rc = make_tmap_3d(&mq, p.q, DP, p.Tq, Bq, pitch, pitch * p.Tq, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_3d(&mk, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_3d(&mqt, p.q, DP, p.Tq, Bq, pitch, pitch * p.Tq, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_3d(&mkt, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_3d(&mv, p.v, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attention_kernel<DP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attention_kernel<DP, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  dim3 grid((p.Tq + 127) / 128, p.H, p.B);
-  attention_kernel<DP><<<grid, 192, C::SMEM, stream>>>(mq, mqt, mk, mkt, mv, p);
+  dim3 grid((p.Tq + NQ * 128 - 1) / (NQ * 128), p.H, p.B);
+  attention_kernel<DP, NQ><<<grid, C::THREADS, C::SMEM, stream>>>(mq, mqt, mk, mkt, mv, p);
   return (int)cudaGetLastError();
 }
 
@@ -321,11 +335,12 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
 
 int attention_bf16(const AttnParams& p, cudaStream_t stream) {
   if (p.B <= 0 || p.H <= 0 || p.Tq <= 0 || p.Tk <= 0 || p.Dv <= 0 || p.Dv > p.Dp) return 1001;
-  if (p.Tkpad < p.Tk || (p.Tkpad % 8) != 0 || (p.ldo % 8) != 0 || (p.Dv % 8) != 0) return 1002;
+  if ((p.ldo % 8) != 0 || (p.Dv % 8) != 0) return 1002;
+  const bool two = p.Tq > 128;
   switch (p.Dp) {
-    case 64: return launch_attn<64>(p, stream);
-    case 80: return launch_attn<80>(p, stream);
-    case 128: return launch_attn<128>(p, stream);
+    case 64: return two ? launch_attn<64, 2>(p, stream) : launch_attn<64, 1>(p, stream);
+    case 80: return two ? launch_attn<80, 2>(p, stream) : launch_attn<80, 1>(p, stream);
+    case 128: return launch_attn<128, 1>(p, stream);
     default: return 1004;
   }
 }

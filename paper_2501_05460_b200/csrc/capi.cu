@@ -367,15 +367,15 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
   return cuda_status(rc, "linear_heads_bf16");
 }
 
-epd_status_t epd_attention_bf16(const void* q, const void* k, const void* vt, void* out, int32_t B, int32_t H,
-                                int32_t Tq, int32_t Tk, int32_t Tkpad, int32_t Dp, int32_t Dv, int32_t ldo,
+epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, void* out, int32_t B, int32_t H,
+                                int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv, int32_t ldo,
                                 int32_t q_shared, float scale, void* stream) {
   epd::AttnParams p;
   p.q = reinterpret_cast<const epd::bf16*>(q);
   p.k = reinterpret_cast<const epd::bf16*>(k);
-  p.vt = reinterpret_cast<const epd::bf16*>(vt);
+  p.v = reinterpret_cast<const epd::bf16*>(v);
   p.out = reinterpret_cast<epd::bf16*>(out);
-  p.B = B; p.H = H; p.Tq = Tq; p.Tk = Tk; p.Tkpad = Tkpad; p.Dp = Dp; p.Dv = Dv; p.ldo = ldo;
+  p.B = B; p.H = H; p.Tq = Tq; p.Tk = Tk; p.Dp = Dp; p.Dv = Dv; p.ldo = ldo;
   p.q_shared = q_shared;
   p.scale = scale;
   return cuda_status(epd::attention_bf16(p, S(stream)), "attention_bf16");

@@ -135,6 +135,19 @@ EPD_DEVICE uint64_t make_sdesc(uint32_t smem_addr, uint32_t sbo_bytes, uint32_t 
   return d;
 }
 
+// Same with an explicit leading-dimension byte offset (MN-major operands: LBO =
+// byte distance between swizzle atoms along M/N, SBO = between 8-row K groups).
+EPD_DEVICE uint64_t make_sdesc_lbo(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                   uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7u) << 61;
+  return d;
+}
+
 // TMEM -> registers: 32 lanes x 32 consecutive 32-bit columns (one row per thread).
 EPD_DEVICE void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(

@@ -361,7 +361,7 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   const size_t o_ao = plan(M * D * 2);
   const size_t o_q = plan(nt * H * T * Dp * 2);
   const size_t o_k = plan(nt * H * T * Dp * 2);
-  const size_t o_vt = plan(nt * H * Dp * Tpad * 2);
+  const size_t o_vt = plan(nt * H * T * Dp * 2);
   size_t big = M * F * 2;
   size_t o_r1 = 0, o_r2 = 0, o_rk = 0, o_rvt = 0, o_rao = 0, o_rr = 0;
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
@@ -371,7 +371,7 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
     o_r2 = plan(M * (size_t)E * 2);  // ln_kv output
     o_rk = plan(nt * RH * T * RDp * 2);
-    o_rvt = plan(nt * RH * RDp * Tpad * 2);
+    o_rvt = plan(nt * RH * T * RDp * 2);
     o_rao = plan(nt * Q * (size_t)E * 2);
     o_rr = plan(nt * Q * (size_t)E * 2);
     o_r1 = o_f;  // kv_proj output reuses the MLP buffer
@@ -581,13 +581,13 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ep.bias = w.qkvb;
       ep.H = H; ep.Dp = Dp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = H * Dp;
       ep.sec_out[0] = ws.q; ep.sec_out[1] = ws.k; ep.sec_out[2] = ws.vt;
-      ep.sec_trans[2] = 1;
+
       EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * 3 * dD, 0, gemm_bf16(ws.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
     }
     {
       AttnParams ap;
-      ap.q = ws.q; ap.k = ws.k; ap.vt = ws.vt; ap.out = ws.ao;
-      ap.B = nt; ap.H = H; ap.Tq = T; ap.Tk = T; ap.Tkpad = Tpad; ap.Dp = Dp; ap.Dv = dh;
+      ap.q = ws.q; ap.k = ws.k; ap.v = ws.vt; ap.out = ws.ao;
+      ap.B = nt; ap.H = H; ap.Tq = T; ap.Tk = T; ap.Dp = Dp; ap.Dv = dh;
       ap.ldo = D;
       ap.scale = 1.f / std::sqrt((float)dh);
       EPD_LAUNCH(PROF_ATTN, 4.0 * nt * dT * dT * dD, 0, attention_bf16(ap, s));
@@ -633,13 +633,13 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ep.resid = dw.r_posk; ep.ldr = 2 * RH * RDp; ep.r_mod = T;
       ep.H = RH; ep.Dp = RDp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = RH * RDp;
       ep.sec_out[0] = ws.rk; ep.sec_out[1] = ws.rvt;
-      ep.sec_trans[1] = 1;
+
       EPD_LAUNCH(PROF_GEMM, 4.0 * dM * dE * dE, 0, gemm_bf16(ws.r2, E, dw.r_kvin, E, M, 2 * RH * RDp, E, ep, s));
     }
     {
       AttnParams ap;
-      ap.q = dw.r_qheads; ap.k = ws.rk; ap.vt = ws.rvt; ap.out = ws.rao;
-      ap.B = nt; ap.H = RH; ap.Tq = Q; ap.Tk = T; ap.Tkpad = Tpad; ap.Dp = RDp; ap.Dv = rdh;
+      ap.q = dw.r_qheads; ap.k = ws.rk; ap.v = ws.rvt; ap.out = ws.rao;
+      ap.B = nt; ap.H = RH; ap.Tq = Q; ap.Tk = T; ap.Dp = RDp; ap.Dv = rdh;
       ap.ldo = E; ap.q_shared = 1;
       ap.scale = 1.f / std::sqrt((float)rdh);
       EPD_LAUNCH(PROF_ATTN, 4.0 * dQ * dT * dE, 0, attention_bf16(ap, s));

@@ -43,17 +43,17 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
               const EpiParams& ep, cudaStream_t stream, int bn_hint = 0);
 
 // Fused multi-head attention O = softmax(Q K^T * scale) V on tcgen05.
-//   Q  : [Bq][Tq][Dp]   (q batch index = b * H + h, or h when q_shared)
-//   K  : [B*H][Tk][Dp]
-//   Vt : [B*H][Dp][Tkpad]  (keys contiguous)
-//   O  : out[(b * Tq + q) * ldo + h * Dv + d] for d < Dv
+//   Q : [Bq][Tq][Dp]   (q batch index = b * H + h, or h when q_shared)
+//   K : [B*H][Tk][Dp]
+//   V : [B*H][Tk][Dp]
+//   O : out[(b * Tq + q) * ldo + h * Dv + d] for d < Dv
 // Dp in {64, 80, 128}; zero-padded head dims contribute nothing.
 struct AttnParams {
   const bf16* q = nullptr;
   const bf16* k = nullptr;
-  const bf16* vt = nullptr;
+  const bf16* v = nullptr;
   bf16* out = nullptr;
-  int B = 0, H = 0, Tq = 0, Tk = 0, Tkpad = 0, Dp = 0, Dv = 0, ldo = 0;
+  int B = 0, H = 0, Tq = 0, Tk = 0, Dp = 0, Dv = 0, ldo = 0;
   int q_shared = 0;
   float scale = 1.f;
 };

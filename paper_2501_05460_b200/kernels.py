@@ -63,15 +63,14 @@ def linear_heads(a: torch.Tensor, w: torch.Tensor, H: int, Dp: int, T: int, sect
     return outs
 
 
-def attention(q: torch.Tensor, k: torch.Tensor, vt: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
               Dv: int, scale: float, q_shared: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Fused MHA; q [Bq,Tq,Dp], k [B*H,Tk,Dp], vt [B*H,Dp,Tkpad] -> out [B*Tq, H*Dv]."""
-    _need_cuda(q, k, vt, out)
+    """Fused MHA; q [Bq,Tq,Dp], k and v [B*H,Tk,Dp] -> out [B*Tq, H*Dv]."""
+    _need_cuda(q, k, v, out)
     Dp = q.shape[-1]
-    Tkpad = vt.shape[-1]
     if out is None:
         out = torch.empty(B * Tq, H * Dv, dtype=torch.bfloat16, device=q.device)
-    call("epd_attention_bf16", q.data_ptr(), k.data_ptr(), vt.data_ptr(), out.data_ptr(), B, H, Tq, Tk, Tkpad,
+    call("epd_attention_bf16", q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, H, Tq, Tk,
          Dp, Dv, out.stride(0), int(q_shared), float(scale), _stream(q))
     return out
 

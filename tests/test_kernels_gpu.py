@@ -72,37 +72,37 @@ def test_linear_inplace_residual(cuda):
     assert relerr(h, ref) <= TOL
 
 
-def _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g):
-    Tkpad = (Tk + 7) // 8 * 8
+def _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g, qscale=1.0):
     Bq = H if q_shared else B * H
     q = torch.zeros(Bq, Tq, Dp, dtype=torch.bfloat16, device="cuda")
     k = torch.zeros(B * H, Tk, Dp, dtype=torch.bfloat16, device="cuda")
-    vt = torch.zeros(B * H, Dp, Tkpad, dtype=torch.bfloat16, device="cuda")
-    q[..., :Dv] = _bf(Bq, Tq, Dv, gen=g)
+    v = torch.zeros(B * H, Tk, Dp, dtype=torch.bfloat16, device="cuda")
+    q[..., :Dv] = _bf(Bq, Tq, Dv, scale=qscale, gen=g)
     k[..., :Dv] = _bf(B * H, Tk, Dv, gen=g)
-    vt[:, :Dv, :Tk] = _bf(B * H, Dv, Tk, gen=g)
-    return q, k, vt
+    v[..., :Dv] = _bf(B * H, Tk, Dv, gen=g)
+    return q, k, v
 
 
-@pytest.mark.parametrize("B,H,Tq,Tk,Dv,Dp,q_shared", [
-    (2, 16, 1024, 1024, 72, 80, False),   # SigLIP self-attention
-    (1, 16, 1025, 1025, 64, 64, False),   # InternViT (CLS -> ragged last key block)
-    (2, 28, 64, 1024, 128, 128, True),    # MiniCPM resampler cross-attention (shared queries)
-    (1, 1, 4, 16, 8, 64, True),           # tiny
-    (1, 2, 300, 200, 64, 64, False),
+@pytest.mark.parametrize("B,H,Tq,Tk,Dv,Dp,q_shared,qscale", [
+    (2, 16, 1024, 1024, 72, 80, False, 1.0),   # SigLIP self-attention
+    (1, 16, 1025, 1025, 64, 64, False, 1.0),   # InternViT (CLS -> ragged last key block)
+    (2, 28, 64, 1024, 128, 128, True, 1.0),    # MiniCPM resampler cross-attention (shared queries)
+    (1, 1, 4, 16, 8, 64, True, 1.0),           # tiny
+    (1, 2, 300, 200, 64, 64, False, 1.0),
+    (1, 4, 256, 1024, 72, 80, False, 6.0),     # peaked scores: exercises the lazy O rescale
 ])
-def test_attention(cuda, B, H, Tq, Tk, Dv, Dp, q_shared):
+def test_attention(cuda, B, H, Tq, Tk, Dv, Dp, q_shared, qscale):
     from paper_2501_05460_b200 import kernels
     g = torch.Generator(device=cuda).manual_seed(B * 100 + H + Tq + Tk)
-    q, k, vt = _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g)
+    q, k, v = _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g, qscale)
     scale = 1.0 / math.sqrt(Dv)
-    y = kernels.attention(q, k, vt, B, H, Tq, Tk, Dv, scale, q_shared=q_shared)
+    y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, q_shared=q_shared)
     torch.cuda.synchronize()
     qf = q[..., :Dv].float()
     if q_shared:
         qf = qf.unsqueeze(0).expand(B, H, Tq, Dv).reshape(B * H, Tq, Dv)
     kf = k[..., :Dv].float()
-    vf = vt[:, :Dv, :Tk].float().transpose(1, 2)
+    vf = v[..., :Dv].float()
     p = torch.softmax(qf @ kf.transpose(1, 2) * scale, dim=-1)
     o = (p @ vf).reshape(B, H, Tq, Dv).permute(0, 2, 1, 3).reshape(B * Tq, H * Dv)
     assert relerr(y, o) <= TOL

@@ -39,12 +39,11 @@ def main():
         ms = timeit(lambda: torch.matmul(a, w.t(), out=out))
         print(f"  torch/cuBLAS {name}: {ms*1e3:8.1f} us  {2*M*N*K/ms/1e9:7.1f} TFLOP/s")
     for (B, H, T, Dv, Dp, Tq, qs) in [(10, 16, 1024, 72, 80, 1024, False), (10, 28, 1024, 128, 128, 64, True)]:
-        Tkpad = T
         q = torch.randn(H if qs else B * H, Tq, Dp, device=dev).to(torch.bfloat16)
         k = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-        vt = torch.randn(B * H, Dp, Tkpad, device=dev).to(torch.bfloat16)
+        v = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
         out = torch.empty(B * Tq, H * Dv, device=dev, dtype=torch.bfloat16)
-        ms = timeit(lambda: kernels.attention(q, k, vt, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out))
+        ms = timeit(lambda: kernels.attention(q, k, v, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out))
         fl = 4 * B * H * Tq * T * Dv
         print(f"attn B={B} H={H} Tq={Tq} Tk={T} Dv={Dv}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s (algorithmic)")
     x = torch.randn(M, 1152, device=dev).to(torch.bfloat16)
