@@ -83,16 +83,33 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        # In-process NVML (no fork/exec inside the timed region); nvidia-smi as fallback.
+        nvml = None
+        try:
+            import pynvml as nvml
+            nvml.nvmlInit()
+            h = nvml.nvmlDeviceGetHandleByIndex(self.index)
+            smax = nvml.nvmlDeviceGetMaxClockInfo(h, nvml.NVML_CLOCK_SM)
+            bits = [nvml.nvmlClocksEventReasonHwSlowdown, nvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    nvml.nvmlClocksEventReasonSwThermalSlowdown, nvml.nvmlClocksEventReasonSwPowerCap]
+        except Exception:
+            nvml = None
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                if nvml is not None:
+                    sm = nvml.nvmlDeviceGetClockInfo(h, nvml.NVML_CLOCK_SM)
+                    reasons = nvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    flags = ["Active" if reasons & b else "Not Active" for b in bits]
+                    self.samples.append([str(sm), str(smax), "0"] + flags)
+                else:
+                    out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05 if nvml is not None else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)

@@ -98,7 +98,11 @@ epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t 
 double epd_encoder_flops_per_tile(const epd_encoder_t* enc);
 /* Kernel launches issued by one epd_encode_tiles call over n tiles. */
 int32_t epd_encoder_launches(const epd_encoder_t* enc, int32_t n);
-/* Per-launch CUDA-event profiling of subsequent encode calls (on = 1/0). */
+/* Replay each forward pass as one CUDA graph per chunk size (default on; the
+ * graph reads/writes encoder-owned staging buffers). Off = direct launches. */
+epd_status_t epd_encoder_set_graphs(epd_encoder_t* enc, int32_t on);
+/* Per-launch CUDA-event profiling of subsequent encode calls (on = 1/0; uses
+ * direct launches while on). */
 epd_status_t epd_encoder_profile(epd_encoder_t* enc, int32_t on);
 /* Drain the profile (synchronises on the last recorded event). Per kernel class
  * c in {0 patchify, 1 gemm, 2 attention, 3 layernorm, 4 other}: summed device

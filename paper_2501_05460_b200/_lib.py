@@ -56,6 +56,7 @@ _SIGS = {
     "epd_encode_tiles": (_i32, [_vp, _vp, _i32, _vp, _vp]),
     "epd_encoder_flops_per_tile": (C.c_double, [_vp]),
     "epd_encoder_launches": (_i32, [_vp, _i32]),
+    "epd_encoder_set_graphs": (_i32, [_vp, _i32]),
     "epd_encoder_profile": (_i32, [_vp, _i32]),
     "epd_encoder_profile_read": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32]),
     "epd_hash_records": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp]),

@@ -10,7 +10,8 @@
 // While warpgroup g computes softmax, the tensor core runs the other group's
 // S / PV MMAs.
 //
-// Warps: 0 TMA, 1 TMEM alloc + MMA issue, 2..5 softmax group 0, 6..9 group 1.
+// Warps: 0 TMA, 1 TMEM alloc + MMA issue, 2..9 softmax group 0, 10..17 group 1
+// (two warps per TMEM lane quarter, each owning half of the key columns).
 // Layouts: Q, K, V all [bh][T][Dp] bf16 (Dp = head dim zero-padded to a
 // multiple of 16). Q/K are K-major operands (64-wide SW128 atoms + a 16-wide
 // SW32 tail when Dp % 64 != 0); V is the MN-major B operand from 16-wide
@@ -37,11 +38,24 @@ EPD_DEVICE void tmem_st16(uint32_t taddr, const uint32_t* r) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+EPD_DEVICE void tmem_ld8(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+EPD_DEVICE void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+EPD_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 EPD_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int DP, int NQ>
 struct Cfg {
   static constexpr int KB = 128;                       // keys per block
+  static constexpr int KVS = DP <= 64 ? 3 : 2;         // V pipeline stages (smem permitting)
+  static constexpr int KS = DP <= 80 ? 3 : 2;          // K pipeline stages (S is on the critical path)
   static constexpr int MAIN = DP / 64;                 // 64-wide SW128 atoms of Q/K
   static constexpr bool TAIL = (DP % 64) != 0;         // 16-wide SW32 tail (DP % 64 == 16)
   static constexpr int QK_ATOM = 128 * 128;            // 128 rows x 128 B
@@ -53,11 +67,12 @@ struct Cfg {
   static constexpr int P_BYTES = 2 * P_ATOM;           // 128 rows x 128 keys bf16
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NQ * QK_AL;
-  static constexpr int OFF_V = OFF_K + 2 * QK_AL;
-  static constexpr int OFF_P = OFF_V + 2 * V_BYTES;
-  static constexpr int OFF_BAR = OFF_P + NQ * P_BYTES;
+  static constexpr int OFF_V = OFF_K + KS * QK_AL;
+  static constexpr int OFF_P = OFF_V + KVS * V_BYTES;
+  static constexpr int OFF_RED = OFF_P + NQ * P_BYTES;      // [NQ][2][2][128] fp32 row exchange
+  static constexpr int OFF_BAR = OFF_RED + NQ * 2 * 2 * 128 * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int THREADS = 64 + NQ * 128;
+  static constexpr int THREADS = 64 + NQ * 256;
 };
 
 template <int DP, int NQ>
@@ -70,14 +85,15 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [NQ]
-  uint64_t* p_ready = bars + 11; // [NQ]
-  uint64_t* o_done = bars + 13;  // [NQ]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* k_full = bars + 1;    // [KVS]
+  uint64_t* k_empty = bars + 4;   // [KVS]
+  uint64_t* v_full = bars + 7;    // [KVS]
+  uint64_t* v_empty = bars + 10;  // [KVS]
+  uint64_t* s_full = bars + 13;   // [NQ]
+  uint64_t* p_ready = bars + 15;  // [NQ]
+  uint64_t* o_done = bars + 17;   // [NQ]
+  uint64_t* s_free = bars + 19;   // [NQ]  S_g read into registers: buffer reusable
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -92,15 +108,18 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < C::KVS; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
     for (int g = 0; g < NQ; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&p_ready[g], 128);
+      mbar_init(&s_free[g], 256);
+      mbar_init(&p_ready[g], 256);
       mbar_init(&o_done[g], 1);
     }
     fence_barrier_init();
@@ -113,6 +132,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   // TMEM columns: S_g at [g*128, g*128+128), O_g at [256 + g*128, 256 + g*128 + DP)
 
   if (warp == 0) {
+    // lane 0 streams Q then K, lane 1 streams V: independent lookahead per operand
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, nq * C::QK_BYTES);
       for (int g = 0; g < nq; ++g) {
@@ -121,14 +141,17 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         if (C::TAIL) tma_load_3d(qd + C::MAIN * C::QK_ATOM, &tmQt, q_full, C::MAIN * 64, q0 + g * 128, qbatch);
       }
       for (int j = 0; j < nkb; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_empty[s], ph ^ 1);
+        const int s = j % C::KS;
+        mbar_wait(&k_empty[s], ((j / C::KS) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[s], C::QK_BYTES);
         uint8_t* kd = smem + C::OFF_K + s * C::QK_AL;
         for (int a = 0; a < C::MAIN; ++a) tma_load_3d(kd + a * C::QK_ATOM, &tmK, &k_full[s], a * 64, j * C::KB, bh);
         if (C::TAIL) tma_load_3d(kd + C::MAIN * C::QK_ATOM, &tmKt, &k_full[s], C::MAIN * 64, j * C::KB, bh);
-        mbar_wait(&v_empty[s], ph ^ 1);
+      }
+    } else if (lane == 1) {
+      for (int j = 0; j < nkb; ++j) {
+        const int s = j % C::KVS;
+        mbar_wait(&v_empty[s], ((j / C::KVS) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
         uint8_t* vd = smem + C::OFF_V + s * C::V_BYTES;
         for (int a = 0; a < DP / 16; ++a) tma_load_3d(vd + a * C::V_ATOM, &tmV, &v_full[s], a * 16, j * C::KB, bh);
@@ -140,7 +163,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DP) | (1u << 16);  // B (V) is MN-major
       mbar_wait(q_full, 0);
       auto issue_s = [&](int g, int j) {
-        const int s = j & 1;
+        const int s = j % C::KS;
         const uint32_t q_addr = smem_u32(smem + C::OFF_Q + g * C::QK_AL);
         const uint32_t k_addr = smem_u32(smem + C::OFF_K + s * C::QK_AL);
 #pragma unroll
@@ -163,16 +186,21 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       for (int g = 0; g < nq; ++g) issue_s(g, 0);
       tc_commit(&k_empty[0]);
       for (int j = 0; j < nkb; ++j) {
-        const int s = j & 1;
-        for (int g = 0; g < nq; ++g) {
-          mbar_wait(&p_ready[g], j & 1);
-          if (j + 1 < nkb) {
-            if (g == 0) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        const int s = j % C::KVS;
+        // Next block's scores as soon as each group has pulled S_g(j) into registers:
+        // the tensor core computes S(j+1) while the softmax warps exponentiate S(j).
+        if (j + 1 < nkb) {
+          for (int g = 0; g < nq; ++g) {
+            mbar_wait(&s_free[g], j & 1);
+            if (g == 0) mbar_wait(&k_full[(j + 1) % C::KS], ((j + 1) / C::KS) & 1);
             tc_fence_after();
             issue_s(g, j + 1);
-            if (g == nq - 1) tc_commit(&k_empty[(j + 1) & 1]);
           }
-          if (g == 0) mbar_wait(&v_full[s], (j >> 1) & 1);
+          tc_commit(&k_empty[(j + 1) % C::KS]);
+        }
+        for (int g = 0; g < nq; ++g) {
+          mbar_wait(&p_ready[g], j & 1);
+          if (g == 0) mbar_wait(&v_full[s], (j / C::KVS) & 1);
           tc_fence_after();
           const uint32_t p_addr = smem_u32(smem + C::OFF_P + g * C::P_BYTES);
           const uint32_t v_addr = smem_u32(smem + C::OFF_V + s * C::V_BYTES);
@@ -189,34 +217,50 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       }
     }
   } else {
-    // ---------------- softmax warpgroups: one query row per thread
-    const int g = (warp - 2) >> 2;
+    // ---------------- softmax: per query tile g, 8 warps = 2 per TMEM lane quarter;
+    // thread (row r, half hf) owns key columns [hf*64, hf*64+64) of S and head dims
+    // [hf*DP/2, (hf+1)*DP/2) of O. Row maxima are combined through smem each block.
+    const int wi = warp - 2;
+    const int g = wi >> 3;
+    const int hf = (wi >> 2) & 1;
     const int qq = warp & 3;
     const int r = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    const uint32_t s_tm = tmem + lane_off + g * 128;
-    const uint32_t o_tm = tmem + lane_off + 256 + g * 128;
+    const uint32_t s_tm = tmem + lane_off + g * 128 + hf * 64;
+    constexpr int OH = DP / 2;  // O columns per half (multiple of 8)
+    const uint32_t o_tm = tmem + lane_off + 256 + g * 128 + hf * OH;
+    // [2 block parity][2 hf][128]: row-max exchange; the final row sums reuse a slot
+    float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + g * (2 * 2 * 128);
     const float c = p.scale * 1.4426950408889634f;
+    const int bar_id = 1 + g;
     if (g < nq) {
       float m_used = -INFINITY, l = 0.f;
-      uint8_t* prow = smem + C::OFF_P + g * C::P_BYTES + r * 128;
+      uint8_t* prow = smem + C::OFF_P + g * C::P_BYTES + hf * C::P_ATOM + r * 128;
       for (int j = 0; j < nkb; ++j) {
-        const int kvalid = p.Tk - j * C::KB;
+        const int kvalid = p.Tk - j * C::KB - hf * 64;  // valid keys among this thread's 64
         mbar_wait(&s_full[g], j & 1);
         tc_fence_after();
-        uint32_t sv[128];
-#pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) tmem_ld32(s_tm + c0, *reinterpret_cast<uint32_t(*)[32]>(sv + c0));
+        uint32_t sv[64];
+        tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
+        tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
         tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[g]);
         float mx = -INFINITY;
-        if (kvalid >= 128) {
+        if (kvalid >= 64) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) mx = fmaxf(mx, __uint_as_float(sv[i]));
+          for (int i = 0; i < 64; ++i) mx = fmaxf(mx, __uint_as_float(sv[i]));
         } else {
 #pragma unroll
-          for (int i = 0; i < 128; ++i)
-            if (i < kvalid) mx = fmaxf(mx, __uint_as_float(sv[i]));
+          for (int i = 0; i < 64; ++i) {
+            if (i >= kvalid) sv[i] = __float_as_uint(-INFINITY);
+            mx = fmaxf(mx, __uint_as_float(sv[i]));
+          }
         }
+        float* rb = red + (j & 1) * 256;
+        rb[hf * 128 + r] = mx;
+        named_bar_sync(bar_id, 256);
+        mx = fmaxf(mx, rb[(hf ^ 1) * 128 + r]);
         const float m_new = fmaxf(m_used, mx * c);
         if (j == 0) {
           m_used = m_new;
@@ -227,13 +271,13 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
           if (__any_sync(0xffffffffu, need)) {
             const float alpha = need ? ex2(m_used - m_new) : 1.f;
 #pragma unroll
-            for (int c0 = 0; c0 < DP; c0 += 16) {
-              uint32_t o[16];
-              tmem_ld16(o_tm + c0, o);
+            for (int c0 = 0; c0 < OH; c0 += 8) {
+              uint32_t o[8];
+              tmem_ld8(o_tm + c0, o);
               tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st16(o_tm + c0, o);
+              for (int i = 0; i < 8; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              tmem_st8(o_tm + c0, o);
             }
             tmem_st_wait();
             if (need) {
@@ -243,56 +287,54 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
           }
         }
         const float nm = -m_used;
-        float rs = 0.f;
+        float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t pk[16];
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          uint32_t pk[8];
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), c, nm));
-            float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), c, nm));
-            if (kvalid < 128) {
-              if (c0 + i >= kvalid) e0 = 0.f;
-              if (c0 + i + 1 >= kvalid) e1 = 0.f;
-            }
-            rs += e0 + e1;
+          for (int i = 0; i < 16; i += 2) {
+            const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), c, nm));
+            const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), c, nm));
+            rs0 += e0;
+            rs1 += e1;
             pk[i >> 1] = pack_bf16x2(e0, e1);
           }
-          uint8_t* arow = prow + (c0 >> 6) * C::P_ATOM;
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const int chunk = ((c0 & 63) >> 3) + q4;
-            *reinterpret_cast<uint4*>(arow + ((chunk ^ (r & 7)) * 16)) =
-                make_uint4(pk[q4 * 4 + 0], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
+          for (int q2 = 0; q2 < 2; ++q2) {
+            const int chunk = (c0 >> 3) + q2;
+            *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) * 16)) =
+                make_uint4(pk[q2 * 4 + 0], pk[q2 * 4 + 1], pk[q2 * 4 + 2], pk[q2 * 4 + 3]);
           }
         }
-        l += rs;
+        l += rs0 + rs1;
         tc_fence_before();
         fence_proxy_async_smem();
         mbar_arrive(&p_ready[g]);
       }
+      // combine the two halves' row sums
+      // the parity slot of block nkb was last read during block nkb-2's exchange, which
+      // every thread of the group has passed (block nkb-1's barrier): safe to reuse
+      float* lb = red + (nkb & 1) * 256;
+      lb[hf * 128 + r] = l;
+      named_bar_sync(bar_id, 256);
+      l += lb[(hf ^ 1) * 128 + r];
       mbar_wait(&o_done[g], (nkb - 1) & 1);
       tc_fence_after();
       const int qrow = q0 + g * 128 + r;
       const float inv = 1.f / l;
-      bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv;
+      bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv + hf * OH;
 #pragma unroll
-      for (int c0 = 0; c0 < DP; c0 += 16) {
-        uint32_t o[16];
-        tmem_ld16(o_tm + c0, o);
+      for (int c0 = 0; c0 < OH; c0 += 8) {
+        uint32_t o[8];
+        tmem_ld8(o_tm + c0, o);
         tmem_ld_wait();
-        if (qrow < p.Tq) {
-#pragma unroll
-          for (int d = 0; d < 16; d += 8) {
-            if (c0 + d < p.Dv) {
-              uint4 v;
-              v.x = pack_bf16x2(__uint_as_float(o[d + 0]) * inv, __uint_as_float(o[d + 1]) * inv);
-              v.y = pack_bf16x2(__uint_as_float(o[d + 2]) * inv, __uint_as_float(o[d + 3]) * inv);
-              v.z = pack_bf16x2(__uint_as_float(o[d + 4]) * inv, __uint_as_float(o[d + 5]) * inv);
-              v.w = pack_bf16x2(__uint_as_float(o[d + 6]) * inv, __uint_as_float(o[d + 7]) * inv);
-              *reinterpret_cast<uint4*>(dst + c0 + d) = v;
-            }
-          }
+        if (qrow < p.Tq && hf * OH + c0 < p.Dv) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv);
+          v.y = pack_bf16x2(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv);
+          v.z = pack_bf16x2(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv);
+          v.w = pack_bf16x2(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c0) = v;
         }
       }
     }

@@ -186,6 +186,12 @@ epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t 
 double epd_encoder_flops_per_tile(const epd_encoder_t* enc) { return enc ? enc->impl.flops_per_tile() : 0.0; }
 int32_t epd_encoder_launches(const epd_encoder_t* enc, int32_t n) { return enc ? enc->impl.launches(n) : 0; }
 
+epd_status_t epd_encoder_set_graphs(epd_encoder_t* enc, int32_t on) {
+  if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
+  enc->impl.use_graphs = on != 0;
+  return EPD_OK;
+}
+
 epd_status_t epd_encoder_profile(epd_encoder_t* enc, int32_t on) {
   if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
   enc->impl.prof_on = on != 0;

@@ -39,6 +39,8 @@ Encoder::~Encoder() {
   if (blob) cudaFree(blob);
   if (work) cudaFree(work);
   for (auto e : prof_events) cudaEventDestroy(e);
+  for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  if (cap_stream) cudaStreamDestroy(cap_stream);
 }
 
 int Encoder::add(const std::string& name, std::vector<int64_t> shape) {
@@ -379,12 +381,16 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
     o_r2 = plan(nt * Q * (size_t)4 * D * 2);  // shuffled + LN rows
     o_rr = plan(nt * Q * (size_t)E * 2);      // fc1 output
   }
+  const size_t o_in = plan(nt * (size_t)d.image_size * d.image_size * d.channels);
+  const size_t o_out = plan(nt * (size_t)Q * E * 2);
   e = cudaMalloc(&work, wsz);
   if (e != cudaSuccess) {
     err = std::string("cudaMalloc(workspace): ") + cudaGetErrorString(e);
     return EPD_ERR_CUDA;
   }
   uint8_t* wb = reinterpret_cast<uint8_t*>(work);
+  in_buf = wb + o_in;
+  out_buf = reinterpret_cast<bf16*>(wb + o_out);
   ws.xp = reinterpret_cast<bf16*>(wb + o_xp);
   ws.h = reinterpret_cast<float*>(wb + o_h);
   ws.xn = reinterpret_cast<bf16*>(wb + o_xn);
@@ -482,7 +488,13 @@ int Encoder::encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std:
   const size_t tile_bytes = (size_t)d.image_size * d.image_size * d.channels;
   for (int c0 = 0; c0 < n; c0 += d.max_tiles) {
     const int nt = std::min(d.max_tiles, n - c0);
-    int rc = forward_chunk(tiles + (size_t)c0 * tile_bytes, nt, out + (size_t)c0 * Q * E, s);
+    const uint8_t* src = tiles + (size_t)c0 * tile_bytes;
+    bf16* dst = out + (size_t)c0 * Q * E;
+    int rc;
+    if (prof_on || !use_graphs)
+      rc = forward_chunk(src, nt, dst, s);
+    else
+      rc = forward_graph(src, nt, dst, s);
     if (rc) {
       err = "kernel launch failed (code " + std::to_string(rc) + "): " +
             (rc < 1000 ? cudaGetErrorString((cudaError_t)rc) : "argument/shape");
@@ -497,6 +509,36 @@ int Encoder::encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std:
     int _rc = (x);            \
     if (_rc) return _rc;      \
   } while (0)
+
+// One CUDA graph per chunk size: the ~200 launches of a forward pass replay with a
+// single cudaGraphLaunch. The graph reads/writes the encoder-owned staging buffers
+// (in_buf / out_buf), so caller buffers only cost two device copies.
+int Encoder::forward_graph(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s) {
+  const size_t in_bytes = (size_t)nt * d.image_size * d.image_size * d.channels;
+  const size_t out_bytes = (size_t)nt * Q * E * 2;
+  auto it = graphs.find(nt);
+  if (it == graphs.end()) {
+    if (!cap_stream) EPD_TRY((int)cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+    EPD_TRY((int)cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = forward_chunk(in_buf, nt, out_buf, cap_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return (int)e;
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return (int)e;
+    it = graphs.emplace(nt, ex).first;
+  }
+  if (tiles != in_buf) EPD_TRY((int)cudaMemcpyAsync(in_buf, tiles, in_bytes, cudaMemcpyDeviceToDevice, s));
+  EPD_TRY((int)cudaGraphLaunch(it->second, s));
+  if (out != out_buf) EPD_TRY((int)cudaMemcpyAsync(out, out_buf, out_bytes, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
 
 // Launch with optional per-launch CUDA-event profiling (class, algorithmic FLOPs, bytes).
 #define EPD_LAUNCH(cls, flops, bytes, x)        \

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -66,6 +67,7 @@ class Encoder {
   int64_t numel(int i) const;
   int prof_read(double* ms, double* flops, double* bytes, int64_t* count, int nclass);
   bool prof_on = false;
+  bool use_graphs = true;
 
   epd_encoder_desc_t d;
   int dev;
@@ -76,6 +78,11 @@ class Encoder {
   int add(const std::string& name, std::vector<int64_t> shape);
   const float* host(int i) const;
   int forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
+  int forward_graph(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
+  std::map<int, cudaGraphExec_t> graphs;
+  cudaStream_t cap_stream = nullptr;
+  uint8_t* in_buf = nullptr;
+  bf16* out_buf = nullptr;
   int prof_begin(cudaStream_t s);
   void prof_end(cudaStream_t s, int ev, int cls, double flops, double bytes);
   std::vector<cudaEvent_t> prof_events;

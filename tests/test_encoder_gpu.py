@@ -66,6 +66,21 @@ def test_encoder_chunking_and_tile_independence(cuda):
     assert torch.equal(together, alone)
 
 
+def test_graph_replay_equals_direct_launches(cuda):
+    """The CUDA-graph replay path (default) is bit-identical to direct launches."""
+    from paper_2501_05460_b200 import _lib
+    cfg = SIGLIP_MINICPM.with_layers(2)
+    w, enc = _setup(cfg, cuda, max_tiles=2)
+    tiles = _tiles(cfg, 3, seed=9).to(cuda)
+    g1 = enc.encode(tiles)
+    g2 = enc.encode(tiles)
+    _lib.call("epd_encoder_set_graphs", enc._h, 0)
+    d = enc.encode(tiles)
+    _lib.call("epd_encoder_set_graphs", enc._h, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, d) and torch.equal(g2, d)
+
+
 def test_encoder_rejects_bad_input(cuda):
     cfg = TINY_VIT
     _, enc = _setup(cfg, cuda)
