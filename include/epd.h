@@ -167,6 +167,11 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
                              int32_t K, const void* bias, int32_t act, const void* resid, int32_t ldr,
                              int32_t r_mod, const void* lscale, void* out, int32_t ldo, int32_t bn,
                              void* stream);
+/* Residual-stream update: h[M,N] (fp32, in place) += lscale * (A W^T + bias); lscale may be NULL.
+ * The epilogue is a TMA reduce-add, so h is never read by the SMs. */
+epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
+                                int32_t K, const void* bias, const void* lscale, float* h, int32_t ldh, int32_t bn,
+                                void* stream);
 /* Projection straight into attention layouts: column n of A W^T + bias (+ resid[row % r_mod])
  * splits into section s = n / sec_cols, head h, dim d (head dim padded to Dp); row = b*T + t.
  * Section s writes out_s[((b*H + h)*T + t)*Dp + d], or, when bit s of trans_mask is set,

@@ -349,6 +349,23 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
   return cuda_status(rc, "linear_bf16");
 }
 
+epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
+                                int32_t K, const void* bias, const void* lscale, float* h, int32_t ldh, int32_t bn,
+                                void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || !h) return fail(EPD_ERR_VALUE, "linear_acc: empty shape or null output");
+  if (ldh % 4 || (reinterpret_cast<uintptr_t>(h) & 15)) return fail(EPD_ERR_VALUE, "linear_acc: h must be 16-byte aligned");
+  epd::EpiParams ep;
+  ep.bias = reinterpret_cast<const epd::bf16*>(bias);
+  ep.lscale = reinterpret_cast<const epd::bf16*>(lscale);
+  ep.resid_f = h;
+  ep.out_f = h;
+  ep.ldr = ldh;
+  ep.ldo = ldh;
+  int rc = epd::gemm_bf16(reinterpret_cast<const epd::bf16*>(A), lda, reinterpret_cast<const epd::bf16*>(W), ldw,
+                          M, N, K, ep, S(stream), bn);
+  return cuda_status(rc, "linear_acc_f32");
+}
+
 epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M,
                                    int32_t N, int32_t K, const void* bias, const void* resid, int32_t ldr,
                                    int32_t r_mod, int32_t H, int32_t Dp, int32_t T, int32_t Tpad,

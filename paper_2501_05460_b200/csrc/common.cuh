@@ -51,6 +51,19 @@ EPD_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
+// Non-blocking probe: true once the phase with the given parity has completed.
+EPD_DEVICE bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
 // Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA reads).
 EPD_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -150,13 +150,16 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(kBM, BN);
+      constexpr uint32_t idesc_full = make_idesc_bf16(kBM, BN);
+      constexpr uint32_t idesc_half = make_idesc_bf16(kBM, BN / 2);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
+        // ragged last N tile: issue half-width MMAs when the valid columns fit
+        const uint32_t idesc = (N - (tile % num_n) * BN <= BN / 2) ? idesc_half : idesc_full;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t dtmem = tmem_base + as * BN;

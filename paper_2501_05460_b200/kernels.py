@@ -42,6 +42,19 @@ def linear(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, a
     return out
 
 
+def linear_acc(a: torch.Tensor, w: torch.Tensor, h: torch.Tensor, bias: torch.Tensor | None = None,
+               lscale: torch.Tensor | None = None, bn: int = 0) -> torch.Tensor:
+    """h (fp32, in place) += lscale * (a @ w.T + bias)."""
+    _need_cuda(a, w, h, bias, lscale)
+    if h.dtype != torch.float32:
+        raise ValueError("h must be fp32")
+    M, K = a.shape
+    N = w.shape[0]
+    call("epd_linear_acc_f32", a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K, _ptr(bias),
+         _ptr(lscale), h.data_ptr(), h.stride(0), bn, _stream(a))
+    return h
+
+
 def linear_heads(a: torch.Tensor, w: torch.Tensor, H: int, Dp: int, T: int, sections: int,
                  trans=(False, False, True), bias: torch.Tensor | None = None,
                  resid: torch.Tensor | None = None, r_mod: int = 0):

@@ -72,6 +72,22 @@ def test_linear_inplace_residual(cuda):
     assert relerr(h, ref) <= TOL
 
 
+@pytest.mark.parametrize("M,N,K,bn,ls", [(2048, 1152, 1152, 0, True), (1000, 1152, 4304, 256, False),
+                                          (4, 64, 64, 0, True)])
+def test_linear_acc_f32(cuda, M, N, K, bn, ls):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    a = _bf(M, K, gen=g)
+    w = _bf(N, K, scale=K ** -0.5, gen=g)
+    b = _bf(N, gen=g)
+    s = _bf(N, scale=0.1, gen=g) if ls else None
+    h = torch.randn(M, N, generator=g, device=cuda)
+    ref = h.clone() + (a.float() @ w.float().t() + b.float()) * (s.float() if ls else 1.0)
+    kernels.linear_acc(a, w, h, bias=b, lscale=s, bn=bn)
+    torch.cuda.synchronize()
+    assert relerr(h, ref) <= 2e-3
+
+
 def _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g, qscale=1.0):
     Bq = H if q_shared else B * H
     q = torch.zeros(Bq, Tq, Dp, dtype=torch.bfloat16, device="cuda")

@@ -38,6 +38,11 @@ def main():
             print(f"gemm {name:8s} M={M} N={N} K={K} bn={bn:3d}: {ms*1e3:8.1f} us  {tf:7.1f} TFLOP/s")
         ms = timeit(lambda: torch.matmul(a, w.t(), out=out))
         print(f"  torch/cuBLAS {name}: {ms*1e3:8.1f} us  {2*M*N*K/ms/1e9:7.1f} TFLOP/s")
+        if name in ("o", "fc2"):
+            h = torch.zeros(M, N, device=dev)
+            for bn in (0, 128, 192, 256):
+                ms = timeit(lambda: kernels.linear_acc(a, w, h, bias=b, bn=bn))
+                print(f"gemm {name}+acc_f32 bn={bn:3d}: {ms*1e3:8.1f} us  {2*M*N*K/ms/1e9:7.1f} TFLOP/s")
     for (B, H, T, Dv, Dp, Tq, qs) in [(10, 16, 1024, 72, 80, 1024, False), (10, 28, 1024, 128, 128, 64, True)]:
         q = torch.randn(H if qs else B * H, Tq, Dp, device=dev).to(torch.bfloat16)
         k = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
