@@ -56,8 +56,9 @@ def workload(name: str):
         return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True,
                     desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
     if name == "c5":
-        return dict(cfg=INTERNVIT_300M, tiles=12, repeat=None, cache=False,
-                    desc="C5: InternVL2-8B-shaped InternViT-300M + pixel shuffle + mlp1, 12 tiles per request")
+        return dict(cfg=INTERNVIT_300M, tiles=12, repeat=None, cache=False, kv_handoff=True,
+                    desc="C5: InternVL2-8B-shaped InternViT-300M + pixel shuffle + mlp1, 12 tiles per request, "
+                         "+ prefill->decode KV-block handoff (3094 tokens)")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -292,6 +293,8 @@ def run_ours(args, wl, world, rank, local):
     _lib.call("epd_encoder_profile_read", enc._h, ms, fl, by, cnt, nc)
     _lib.call("epd_encoder_profile", enc._h, 0)
 
+    kv = kv_handoff_bench(wl, cfg, n, world, rank, dev, args) if wl.get("kv_handoff") else None
+
     encoded_tiles = n  # tiles that complete the request per step (cache hits count as served)
     value = encoded_tiles * args.steps / (total_ms / 1e3)
     e2e_value = encoded_tiles * args.steps / (e2e_ms / 1e3)
@@ -353,10 +356,56 @@ def run_ours(args, wl, world, rank, local):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
+    if wl.get("kv_handoff"):
+        line["kv_handoff"] = kv
     if cache is not None and last is not None and last.kinds is not None:
         line["cache"] = {"hits": last.kinds.count("hit"), "misses": last.kinds.count("miss"),
                          "dups": last.kinds.count("dup")}
     print(json.dumps(line), flush=True)
+
+
+def kv_handoff_bench(wl, cfg, n, world, rank, dev, args):
+    """Prefill -> decode KV-block handoff of one request (engine.py:542-555, 436-439):
+    pack the prefill rank's paged blocks, NCCL P2P to the decode rank (the last rank;
+    the same GPU at N = 1), unpack into the decode-side block ids."""
+    import torch.distributed as dist
+
+    from paper_2501_05460_b200.handoff import PagedKVCache, kv_handoff
+    geo = cfg.geometry
+    total = n * geo.tokens_per_patch + PROMPT_TOKENS
+    out_tokens = 64
+    p_rank, d_rank = 0, world - 1
+    nblk = -(-(total + out_tokens) // 16) + 4
+    src = PagedKVCache(geo.num_layers, geo.kv_heads, geo.head_dim, 16, nblk, dev) if rank == p_rank else None
+    dst = PagedKVCache(geo.num_layers, geo.kv_heads, geo.head_dim, 16, nblk, dev) if rank == d_rank else None
+    if rank not in (p_rank, d_rank):
+        return None
+
+    def one(rid):
+        if src is not None:
+            src.manager.allocate(rid, total)
+        info = kv_handoff(rid, total, out_tokens, src, dst, p_rank, d_rank, rank)
+        if dst is not None:
+            dst.manager.free(rid)
+        return info
+
+    for i in range(args.warmup):
+        one(10_000 + i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        info = one(20_000 + i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    if rank != 0:
+        return None
+    moved = info["moved_bytes"]
+    return {"tokens": total, "pd_bytes": total * geo.kv_bytes_per_token(), "moved_bytes_per_request": moved,
+            "ms_per_request": ms, "GBps": moved / (ms / 1e3) / 1e9,
+            "path": "pack -> self-copy -> unpack (same GPU)" if world == 1 else "pack -> NCCL P2P -> unpack",
+            "note": "whole 16-token blocks move; pd_bytes is the reference's token-exact count (engine.py:553-554)"}
 
 
 def stage_tiles_per_rank(n: int, world: int, rank: int) -> int:

@@ -349,6 +349,12 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
   return cuda_status(rc, "linear_bf16");
 }
 
+epd_status_t epd_set_gemm_cta_group(int32_t policy) {
+  if (policy < 0 || policy > 2) return fail(EPD_ERR_VALUE, "cta group policy must be 0, 1 or 2");
+  epd::set_gemm_cta_group(policy);
+  return EPD_OK;
+}
+
 epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
                                 int32_t K, const void* bias, const void* lscale, float* h, int32_t ldh, int32_t bn,
                                 void* stream) {

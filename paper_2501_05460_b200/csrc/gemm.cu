@@ -52,10 +52,10 @@ struct EpiCfg {
 
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
 
-template <int BN>
+template <int BN, int CG>
 struct GemmCfg {
   static constexpr int A_BYTES = kBM * kBK * 2;
-  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int B_BYTES = (BN / CG) * kBK * 2;  // with CTA pairs each CTA holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (227 * 1024 - 2 * kEpiStageBytes - 2048) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -63,6 +63,57 @@ struct GemmCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * kEpiStageBytes + 1024 + 256;
   static constexpr int THREADS = 64 + 256;
 };
+
+EPD_DEVICE uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+EPD_DEVICE void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Map a local shared::cta address to the same offset in CTA `rank` of the cluster.
+EPD_DEVICE uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+EPD_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load issued by either CTA of a pair; the transaction bytes land on the leader's barrier.
+EPD_DEVICE void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+EPD_DEVICE void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the same barrier offset in both CTAs of the pair once the pair's MMAs complete.
+EPD_DEVICE void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+EPD_DEVICE void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+EPD_DEVICE void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
 
 EPD_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 EPD_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -87,12 +138,15 @@ EPD_DEVICE void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int 
                : "memory");
 }
 
-template <int BN, int KIND>
-__global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
+// CG = 1: one CTA per 128 x BN tile. CG = 2: a CTA pair (cluster of 2) computes a
+// 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA loads its 128 rows of A
+// and half of B, the leader issues M=256 MMAs, both CTAs drain their own TMEM.
+template <int BN, int KIND, int CG>
+__global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
                      const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   constexpr int CW = EpiCfg<KIND>::CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -107,6 +161,9 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+  const int pid = blockIdx.x / CG;     // CTA pair (or CTA) index
+  const int npid = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
@@ -115,19 +172,22 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 256);
+      mbar_init(&tempty[s], 8 * CG);  // one arrive per epilogue warp of every CTA in the pair
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
-  if (warp == 1) tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2) tmem_alloc_pair(tmem_holder, Cfg::TMEM_COLS);
+    else tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int num_m = (M + kBM - 1) / kBM;
+  const int num_m = (M + kBM * CG - 1) / (kBM * CG);
   const int num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
   const int nk = (K + kBK - 1) / kBK;
@@ -136,30 +196,37 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / num_n) * kBM;
-        const int n0 = (tile % num_n) * BN;
+      for (int tile = pid; tile < num_tiles; tile += npid) {
+        const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
+        const int n0 = (tile % num_n) * BN + crank * (BN / CG);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
-          tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+          if (CG == 1) {
+            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+          } else {
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
+            tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+          }
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_full = make_idesc_bf16(kBM, BN);
+    if (lane == 0 && crank == 0) {
+      constexpr uint32_t idesc_full = make_idesc_bf16(kBM * CG, BN);
       constexpr uint32_t idesc_half = make_idesc_bf16(kBM, BN / 2);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
-        // ragged last N tile: issue half-width MMAs when the valid columns fit
-        const uint32_t idesc = (N - (tile % num_n) * BN <= BN / 2) ? idesc_half : idesc_full;
+        // ragged last N tile (1-CTA only): issue half-width MMAs when the valid columns fit
+        const uint32_t idesc =
+            (CG == 1 && N - (tile % num_n) * BN <= BN / 2) ? idesc_half : idesc_full;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t dtmem = tmem_base + as * BN;
@@ -172,12 +239,13 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
           for (int k = 0; k < kBK / 16; ++k) {
             const uint64_t adesc = make_sdesc(a_addr + k * 32, 1024, 2);
             const uint64_t bdesc = make_sdesc(b_addr + k * 32, 1024, 2);
-            umma_bf16(dtmem, adesc, bdesc, idesc, (kb | k) != 0);
+            if (CG == 2) umma_bf16_pair(dtmem, adesc, bdesc, idesc, (kb | k) != 0);
+            else umma_bf16(dtmem, adesc, bdesc, idesc, (kb | k) != 0);
           }
-          tc_commit(&empty[stage]);
+          if (CG == 2) tc_commit_pair(&empty[stage]); else tc_commit(&empty[stage]);
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[as]);
+        if (CG == 2) tc_commit_pair(&tfull[as]); else tc_commit(&tfull[as]);
       }
     }
   } else {
@@ -188,11 +256,12 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
     const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
     uint8_t* stg = sEpi + half * kEpiStageBytes;
     const int bar_id = 1 + half;
+    const uint32_t tempty_leader = mapa_rank(smem_u32(&tempty[0]), 0);
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m0 = (tile / num_n) * kBM;
+      const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
       const int n0 = (tile % num_n) * BN;
       const int row = m0 + r;
       mbar_wait(&tfull[as], aphase);
@@ -335,28 +404,33 @@ __global__ void __launch_bounds__(GemmCfg<BN>::THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[as]);
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(tempty_leader + as * 8);
+        else mbar_arrive(&tempty[as]);
+      }
     }
     if (leader) bulk_wait_all0();
   }
 
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if (CG == 2) tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
-template <int BN, int KIND>
+template <int BN, int KIND, int CG>
 int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, const EpiParams& ep,
            cudaStream_t stream) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG>;
   CUtensorMap ta, tb, t0, t1, t2;
   int rc = make_tmap_2d(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, kBK, kBM,
                         CU_TENSOR_MAP_SWIZZLE_128B);
   if (!rc)
-    rc = make_tmap_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = make_tmap_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (KIND == EK_ROWS_BF16) {
     rc = make_tmap_2d(&t0, ep.out, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 2, 32, kBM,
@@ -386,51 +460,76 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN, KIND, CG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
-  int grid = num_sms();
-  if (tiles < grid) grid = tiles;
-  gemm_bf16_kernel<BN, KIND><<<grid, Cfg::THREADS, Cfg::SMEM, stream>>>(ta, tb, t0, t1, t2, M, N, K, ep);
+  const int tiles = ((M + kBM * CG - 1) / (kBM * CG)) * ((N + BN - 1) / BN);
+  int units = num_sms() / CG;
+  if (tiles < units) units = tiles;
+  if (CG == 1) {
+    gemm_bf16_kernel<BN, KIND, 1><<<units, Cfg::THREADS, Cfg::SMEM, stream>>>(ta, tb, t0, t1, t2, M, N, K, ep);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(units * CG);
+    cfg.blockDim = dim3(Cfg::THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, KIND, CG>, ta, tb, t0, t1, t2, M, N, K, ep);
+    if (e != cudaSuccess) return (int)e;
+  }
   return (int)cudaGetLastError();
 }
 
-template <int BN>
+template <int BN, int CG>
 int launch_kind(int kind, const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
                 const EpiParams& ep, cudaStream_t stream) {
   switch (kind) {
-    case EK_ROWS_BF16: return launch<BN, EK_ROWS_BF16>(A, lda, B, ldb, M, N, K, ep, stream);
-    case EK_ROWS_F32: return launch<BN, EK_ROWS_F32>(A, lda, B, ldb, M, N, K, ep, stream);
-    case EK_ACC_F32: return launch<BN, EK_ACC_F32>(A, lda, B, ldb, M, N, K, ep, stream);
-    default: return launch<BN, EK_HEADS>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ROWS_BF16: return launch<BN, EK_ROWS_BF16, CG>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ROWS_F32: return launch<BN, EK_ROWS_F32, CG>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ACC_F32: return launch<BN, EK_ACC_F32, CG>(A, lda, B, ldb, M, N, K, ep, stream);
+    default: return launch<BN, EK_HEADS, CG>(A, lda, B, ldb, M, N, K, ep, stream);
   }
 }
 
+int g_cta_group_policy = 0;  // 0 auto, 1 force single-CTA, 2 force CTA pairs
+
 }  // namespace
+
+void set_gemm_cta_group(int policy) { g_cta_group_policy = policy; }
 
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
               const EpiParams& ep, cudaStream_t stream, int bn_hint) {
   if (M <= 0 || N <= 0 || K <= 0) return 1001;
   if (N % 8 != 0 || (lda * 2) % 16 != 0 || (ldb * 2) % 16 != 0) return 1002;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return 1003;
+  // CTA pairs (256-row tiles, half of B per SM) for large M; single CTAs for small M.
+  int cg = g_cta_group_policy ? g_cta_group_policy : (M >= 2048 ? 2 : 1);
   int bn = bn_hint;
   if (bn == 0) {
     // Wide tiles amortise the epilogue and B-operand traffic best; step down only
     // when the last wave of 256-wide tiles would leave most SMs idle.
-    const int sms = num_sms();
+    const int units = num_sms() / cg;
     double best = 1e30;
     const int cands[3] = {256, 192, 128};
     for (int i = 0; i < 3; ++i) {
       const int c = cands[i];
-      const long tiles = (long)((M + kBM - 1) / kBM) * ((N + c - 1) / c);
-      const long waves = (tiles + sms - 1) / sms;
+      if (cg == 2 && c == 128) continue;
+      const long tiles = (long)((M + kBM * cg - 1) / (kBM * cg)) * ((N + c - 1) / c);
+      const long waves = (tiles + units - 1) / units;
       const double cost = (double)waves * c * (c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0));
       if (cost < best) { best = cost; bn = c; }
     }
   }
+  if (cg == 2 && bn == 128) cg = 1;
   int kind;
   if (ep.mode == EPI_HEADS) {
     if (ep.Dp % 16 || ep.sec_cols % ep.Dp || ep.T <= 0) return 1005;
@@ -446,11 +545,17 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
     if (!ep.out || ep.resid_f) return 1005;
     kind = EK_ROWS_BF16;
   }
-  if (kind == EK_ACC_F32 && ep.act != ACT_NONE && false) return 1005;
+  if (cg == 2) {
+    switch (bn) {
+      case 256: return launch_kind<256, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+      case 192: return launch_kind<192, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+      default: return 1004;
+    }
+  }
   switch (bn) {
-    case 256: return launch_kind<256>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-    case 192: return launch_kind<192>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-    case 128: return launch_kind<128>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+    case 256: return launch_kind<256, 1>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+    case 192: return launch_kind<192, 1>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+    case 128: return launch_kind<128, 1>(kind, A, lda, B, ldb, M, N, K, ep, stream);
     default: return 1004;
   }
 }

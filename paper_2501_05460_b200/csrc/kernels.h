@@ -39,6 +39,8 @@ struct EpiParams {
 };
 
 // Returns a cudaError_t-compatible code (0 = success); 1000+ for argument errors.
+// GEMM CTA-group policy for subsequent launches: 0 auto, 1 single CTAs, 2 CTA pairs.
+void set_gemm_cta_group(int policy);
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
               const EpiParams& ep, cudaStream_t stream, int bn_hint = 0);
 

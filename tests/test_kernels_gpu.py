@@ -183,3 +183,44 @@ def test_linear_heads(cuda, M, T, H, Dp, dh, trans):
         ref = full[:, s * H * Dp:(s + 1) * H * Dp].reshape(nb, T, H, Dp).permute(0, 2, 1, 3).reshape(nb * H, T, Dp)
         got = outs[s][..., :T].transpose(1, 2) if trans[s] else outs[s]
         assert relerr(got, ref) <= TOL, s
+
+
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+def cta_group(request, cuda):
+    from paper_2501_05460_b200._lib import call
+    call("epd_set_gemm_cta_group", request.param)
+    yield request.param
+    call("epd_set_gemm_cta_group", 0)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(1000, 1152, 1152, 256), (2048, 3840, 1152, 0), (4096, 4304, 1152, 192),
+                                      (2304, 1152, 4304, 0), (300, 512, 64, 256)])
+def test_linear_cta_groups(cuda, cta_group, M, N, K, bn):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(M + N + K + cta_group)
+    a = _bf(M, K, gen=g)
+    w = _bf(N, K, scale=K ** -0.5, gen=g)
+    b = _bf(N, gen=g)
+    y = kernels.linear(a, w, bias=b, act="gelu_tanh", bn=bn)
+    h = torch.randn(M, N, generator=g, device=cuda)
+    ref_h = h.clone() + a.float() @ w.float().t()
+    kernels.linear_acc(a, w, h, bn=bn)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.gelu(a.float() @ w.float().t() + b.float(), approximate="tanh")
+    assert relerr(y, ref) <= TOL
+    assert relerr(h, ref_h) <= 2e-3
+
+
+def test_linear_heads_cta_pairs(cuda, cta_group):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(77)
+    M, T, H, Dp, K = 3075, 1025, 16, 64, 256  # InternViT-like: images straddle 256-row pair tiles
+    a = _bf(M, K, gen=g)
+    w = _bf(3 * H * Dp, K, scale=K ** -0.5, gen=g)
+    outs = kernels.linear_heads(a, w, H, Dp, T, 3, trans=(False, False, False))
+    torch.cuda.synchronize()
+    full = a.float() @ w.float().t()
+    nb = M // T
+    for s in range(3):
+        ref = full[:, s * H * Dp:(s + 1) * H * Dp].reshape(nb, T, H, Dp).permute(0, 2, 1, 3).reshape(nb * H, T, Dp)
+        assert relerr(outs[s], ref) <= TOL

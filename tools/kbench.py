@@ -23,7 +23,11 @@ def timeit(fn, iters=20, warm=3):
 
 
 def main():
+    from paper_2501_05460_b200._lib import call
     dev = torch.device("cuda")
+    cg = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+    call("epd_set_gemm_cta_group", cg)
+    print(f"gemm cta-group policy {cg}")
     M = 10240
     for (N, K, act, name) in [(3840, 1152, "none", "qkv"), (1152, 1152, "none", "o"),
                               (4304, 1152, "gelu_tanh", "fc1"), (1152, 4304, "none", "fc2"),
