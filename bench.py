@@ -337,6 +337,8 @@ def run_ours(args, wl, world, rank, local):
                    "weights": "random-init N(0,0.02), seed 20260808"},
         "p50_ttft_ms": p50_ttft,
         "p50_ttft_ms_resident": p50_resident,
+        "ttft_ms_dist": {"p90": _percentile(e2e_per, 0.9), "max": max(e2e_per), "mean": sum(e2e_per) / len(e2e_per),
+                         "resident_max": max(per_ms)},
         "p50_ttft_ms_with_modeled_prefill": (p50_ttft + prefill_ms) if prefill_ms is not None else None,
         "ttft_note": "encode-side TTFT measured on B200 (H2D of the request's tiles -> MM tokens packed on the "
                      "prefill GPU -> D2H); modeled prefill = reference costs.prefill_latency with "

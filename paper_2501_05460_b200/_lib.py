@@ -7,10 +7,11 @@ reference raises for the same condition (see ``include/epd.h``).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libepd.so"
+LIB_PATH = Path(os.environ.get("EPD_LIB_PATH") or Path(__file__).resolve().parent / "libepd.so")
 
 EPD_OK = 0
 EPD_ERR_VALUE = 1

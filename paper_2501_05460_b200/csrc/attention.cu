@@ -2,20 +2,23 @@
 //
 // One CTA = NQ (1 or 2) tiles of 128 query rows of one (batch, head); the
 // tiles share every K/V block. Per 128-key block j and query tile g:
-//   S_g  = Q_g K_j^T          tcgen05.mma M=128 N=128 K=Dp  -> TMEM (fp32)
-//   P_g  = exp2(S_g*c - m_g)  softmax warpgroup g (TMEM -> regs -> bf16 P, SW128 smem)
-//   O_g += P_g V_j            tcgen05.mma M=128 N=Dp K=128  -> TMEM (fp32), V MN-major
+//   S_g  = Q_g K_j^T          tcgen05.mma (A, B from smem)  M=128 N=128 K=Dp -> TMEM fp32
+//   P_g  = exp2(S_g*c - m_g)  softmax warps: TMEM -> regs -> bf16 P written back to TMEM,
+//                             aliasing the first 64 columns of S_g (no smem round trip)
+//   O_g += P_g V_j            tcgen05.mma (A = P from TMEM, B = V from smem, MN-major)
 // The running max m_g is only raised (and O_g rescaled in TMEM) when a row's
-// max grows by more than 2^8, so most blocks need no correction pass.
-// While warpgroup g computes softmax, the tensor core runs the other group's
-// S / PV MMAs.
+// max grows by more than 2^8, so most blocks need no correction pass. Because
+// S_g(j+1) is issued after PV_g(j), the arrival of S_g(j) also means O_g is
+// stable and P_g(j-1) has been consumed. While one tile runs its softmax the
+// tensor core works on the other tile's PV and S.
 //
-// Warps: 0 TMA, 1 TMEM alloc + MMA issue, 2..9 softmax group 0, 10..17 group 1
-// (two warps per TMEM lane quarter, each owning half of the key columns).
+// Warps: 0 TMA (lane 0: Q, K; lane 1: V), 1 TMEM alloc + MMA issue,
+// 2..9 softmax tile 0, 10..17 tile 1 (two warps per TMEM lane quarter, each
+// owning half of the key columns and half of the head dims).
 // Layouts: Q, K, V all [bh][T][Dp] bf16 (Dp = head dim zero-padded to a
-// multiple of 16). Q/K are K-major operands (64-wide SW128 atoms + a 16-wide
-// SW32 tail when Dp % 64 != 0); V is the MN-major B operand from 16-wide
-// SW32 atoms (LBO = 4 KB between atoms, SBO = 256 B between 8-key groups).
+// multiple of 16). Q/K are K-major smem operands (64-wide SW128 atoms + a
+// 16-wide SW32 tail when Dp % 64 != 0); V is the MN-major B operand from
+// 16-wide SW32 atoms (LBO = 4 KB between atoms, SBO = 256 B between 8-key groups).
 #include "common.cuh"
 #include "kernels.h"
 #include "tmap.h"
@@ -30,14 +33,6 @@ EPD_DEVICE float ex2(float x) {
   return y;
 }
 
-EPD_DEVICE void tmem_st16(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
 EPD_DEVICE void tmem_ld8(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -48,14 +43,35 @@ EPD_DEVICE void tmem_st8(uint32_t taddr, const uint32_t* r) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
+EPD_DEVICE void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
 EPD_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 EPD_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]^T (A operand from tensor memory).
+EPD_DEVICE void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 
 template <int DP, int NQ>
 struct Cfg {
   static constexpr int KB = 128;                       // keys per block
-  static constexpr int KVS = DP <= 64 ? 3 : 2;         // V pipeline stages (smem permitting)
-  static constexpr int KS = DP <= 80 ? 3 : 2;          // K pipeline stages (S is on the critical path)
+  static constexpr int KS = 3;                         // K pipeline stages
+  static constexpr int KVS = DP <= 80 ? 3 : 2;         // V pipeline stages (smem permitting)
   static constexpr int MAIN = DP / 64;                 // 64-wide SW128 atoms of Q/K
   static constexpr bool TAIL = (DP % 64) != 0;         // 16-wide SW32 tail (DP % 64 == 16)
   static constexpr int QK_ATOM = 128 * 128;            // 128 rows x 128 B
@@ -63,13 +79,10 @@ struct Cfg {
   static constexpr int QK_AL = (QK_BYTES + 1023) / 1024 * 1024;
   static constexpr int V_ATOM = 128 * 32;              // 128 keys x 16 dims x 2 B
   static constexpr int V_BYTES = (DP / 16) * V_ATOM;
-  static constexpr int P_ATOM = 128 * 128;
-  static constexpr int P_BYTES = 2 * P_ATOM;           // 128 rows x 128 keys bf16
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + NQ * QK_AL;
   static constexpr int OFF_V = OFF_K + KS * QK_AL;
-  static constexpr int OFF_P = OFF_V + KVS * V_BYTES;
-  static constexpr int OFF_RED = OFF_P + NQ * P_BYTES;      // [NQ][2][2][128] fp32 row exchange
+  static constexpr int OFF_RED = OFF_V + KVS * V_BYTES;     // [NQ][2][2][128] fp32 row exchange
   static constexpr int OFF_BAR = OFF_RED + NQ * 2 * 2 * 128 * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int THREADS = 64 + NQ * 256;
@@ -85,15 +98,14 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [KVS]
-  uint64_t* k_empty = bars + 4;   // [KVS]
+  uint64_t* k_full = bars + 1;    // [KS]
+  uint64_t* k_empty = bars + 4;   // [KS]
   uint64_t* v_full = bars + 7;    // [KVS]
   uint64_t* v_empty = bars + 10;  // [KVS]
-  uint64_t* s_full = bars + 13;   // [NQ]
-  uint64_t* p_ready = bars + 15;  // [NQ]
-  uint64_t* o_done = bars + 17;   // [NQ]
-  uint64_t* s_free = bars + 19;   // [NQ]  S_g read into registers: buffer reusable
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* s_full = bars + 13;   // [NQ] S_g(j) in TMEM (and, by issue order, PV_g(j-1) complete)
+  uint64_t* p_ready = bars + 15;  // [NQ] P_g(j) written to TMEM
+  uint64_t* o_done = bars + 17;   // [NQ] last PV_g complete
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -118,7 +130,6 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     }
     for (int g = 0; g < NQ; ++g) {
       mbar_init(&s_full[g], 1);
-      mbar_init(&s_free[g], 256);
       mbar_init(&p_ready[g], 256);
       mbar_init(&o_done[g], 1);
     }
@@ -129,10 +140,10 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  // TMEM columns: S_g at [g*128, g*128+128), O_g at [256 + g*128, 256 + g*128 + DP)
+  // TMEM columns: S_g / P_g at [g*128, g*128+128) (P = bf16 pairs in the first 64),
+  // O_g at [256 + g*128, 256 + g*128 + DP)
 
   if (warp == 0) {
-    // lane 0 streams Q then K, lane 1 streams V: independent lookahead per operand
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, nq * C::QK_BYTES);
       for (int g = 0; g < nq; ++g) {
@@ -162,22 +173,27 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KB);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DP) | (1u << 16);  // B (V) is MN-major
       mbar_wait(q_full, 0);
+      // Descriptors are precomputed: per MMA the issuing thread only adds a constant
+      // (start address >> 4) to a base descriptor -- at N = 80..128 the tensor core
+      // finishes an MMA in 40..64 cycles, so a serial descriptor build would starve it.
+      const uint64_t q_main0 = make_sdesc(smem_u32(smem + C::OFF_Q), 1024, 2);
+      const uint64_t q_tail0 = make_sdesc(smem_u32(smem + C::OFF_Q + C::MAIN * C::QK_ATOM), 256, 6);
+      const uint64_t k_main0 = make_sdesc(smem_u32(smem + C::OFF_K), 1024, 2);
+      const uint64_t k_tail0 = make_sdesc(smem_u32(smem + C::OFF_K + C::MAIN * C::QK_ATOM), 256, 6);
+      const uint64_t v_base0 = make_sdesc_lbo(smem_u32(smem + C::OFF_V), C::V_ATOM, 256, 6);
       auto issue_s = [&](int g, int j) {
-        const int s = j % C::KS;
-        const uint32_t q_addr = smem_u32(smem + C::OFF_Q + g * C::QK_AL);
-        const uint32_t k_addr = smem_u32(smem + C::OFF_K + s * C::QK_AL);
+        const uint64_t qo = (uint64_t)((g * C::QK_AL) >> 4);
+        const uint64_t ko = (uint64_t)(((j % C::KS) * C::QK_AL) >> 4);
+        const uint32_t d = tmem + g * 128;
 #pragma unroll
         for (int kk = 0; kk < DP / 16; ++kk) {
           const int atom = kk >> 2;
-          uint64_t ad, bd;
           if (atom < C::MAIN) {
-            ad = make_sdesc(q_addr + atom * C::QK_ATOM + (kk & 3) * 32, 1024, 2);
-            bd = make_sdesc(k_addr + atom * C::QK_ATOM + (kk & 3) * 32, 1024, 2);
+            const uint64_t off = (uint64_t)((atom * C::QK_ATOM + (kk & 3) * 32) >> 4);
+            umma_bf16(d, q_main0 + qo + off, k_main0 + ko + off, idesc_s, kk != 0);
           } else {
-            ad = make_sdesc(q_addr + C::MAIN * C::QK_ATOM, 256, 6);
-            bd = make_sdesc(k_addr + C::MAIN * C::QK_ATOM, 256, 6);
+            umma_bf16(d, q_tail0 + qo, k_tail0 + ko, idesc_s, kk != 0);
           }
-          umma_bf16(tmem + g * 128, ad, bd, idesc_s, kk != 0);
         }
         tc_commit(&s_full[g]);
       };
@@ -186,34 +202,30 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       for (int g = 0; g < nq; ++g) issue_s(g, 0);
       tc_commit(&k_empty[0]);
       for (int j = 0; j < nkb; ++j) {
-        const int s = j % C::KVS;
-        // Next block's scores as soon as each group has pulled S_g(j) into registers:
-        // the tensor core computes S(j+1) while the softmax warps exponentiate S(j).
-        if (j + 1 < nkb) {
-          for (int g = 0; g < nq; ++g) {
-            mbar_wait(&s_free[g], j & 1);
+        const int sv = j % C::KVS;
+        for (int g = 0; g < nq; ++g) {
+          mbar_wait(&p_ready[g], j & 1);
+          if (g == 0) mbar_wait(&v_full[sv], (j / C::KVS) & 1);
+          tc_fence_after();
+          const uint64_t vb = v_base0 + (uint64_t)((sv * C::V_BYTES) >> 4);
+          const uint32_t od = tmem + 256 + g * 128, pa = tmem + g * 128;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            // A = P from TMEM: keys 16kk..16kk+15 are bf16 pairs in columns 8kk..8kk+7
+            // B = V, MN-major SW32: key row kk*16 (512 B), LBO = 4 KB (next 16 dims), SBO = 256 B
+            umma_bf16_ts(od, pa + kk * 8, vb + (uint64_t)(kk * 32), idesc_o, (j | kk) != 0);
+          }
+          if (j + 1 == nkb) {
+            tc_commit(&o_done[g]);
+          } else {
+            // S_g(j+1) overwrites P_g(j) only after PV_g(j) (in-order tensor pipe)
             if (g == 0) mbar_wait(&k_full[(j + 1) % C::KS], ((j + 1) / C::KS) & 1);
             tc_fence_after();
             issue_s(g, j + 1);
           }
-          tc_commit(&k_empty[(j + 1) % C::KS]);
         }
-        for (int g = 0; g < nq; ++g) {
-          mbar_wait(&p_ready[g], j & 1);
-          if (g == 0) mbar_wait(&v_full[s], (j / C::KVS) & 1);
-          tc_fence_after();
-          const uint32_t p_addr = smem_u32(smem + C::OFF_P + g * C::P_BYTES);
-          const uint32_t v_addr = smem_u32(smem + C::OFF_V + s * C::V_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t ad = make_sdesc(p_addr + (kk >> 2) * C::P_ATOM + (kk & 3) * 32, 1024, 2);
-            // MN-major SW32: start at key row kk*16 (512 B), LBO = 4 KB (next 16 dims), SBO = 256 B
-            const uint64_t bd = make_sdesc_lbo(v_addr + kk * 512, C::V_ATOM, 256, 6);
-            umma_bf16(tmem + 256 + g * 128, ad, bd, idesc_o, (j | kk) != 0);
-          }
-          tc_commit(&o_done[g]);
-        }
-        tc_commit(&v_empty[s]);
+        tc_commit(&v_empty[sv]);
+        if (j + 1 < nkb) tc_commit(&k_empty[(j + 1) % C::KS]);
       }
     }
   } else {
@@ -227,6 +239,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     const int r = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     const uint32_t s_tm = tmem + lane_off + g * 128 + hf * 64;
+    const uint32_t p_tm = tmem + lane_off + g * 128 + hf * 32;
     constexpr int OH = DP / 2;  // O columns per half (multiple of 8)
     const uint32_t o_tm = tmem + lane_off + 256 + g * 128 + hf * OH;
     // [2 block parity][2 hf][128]: row-max exchange; the final row sums reuse a slot
@@ -235,7 +248,6 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     const int bar_id = 1 + g;
     if (g < nq) {
       float m_used = -INFINITY, l = 0.f;
-      uint8_t* prow = smem + C::OFF_P + g * C::P_BYTES + hf * C::P_ATOM + r * 128;
       for (int j = 0; j < nkb; ++j) {
         const int kvalid = p.Tk - j * C::KB - hf * 64;  // valid keys among this thread's 64
         mbar_wait(&s_full[g], j & 1);
@@ -244,8 +256,6 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
         tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
         tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&s_free[g]);
         float mx = -INFINITY;
         if (kvalid >= 64) {
 #pragma unroll
@@ -259,14 +269,14 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         }
         float* rb = red + (j & 1) * 256;
         rb[hf * 128 + r] = mx;
+        // Both halves have read their S columns before either writes P over them.
         named_bar_sync(bar_id, 256);
         mx = fmaxf(mx, rb[(hf ^ 1) * 128 + r]);
         const float m_new = fmaxf(m_used, mx * c);
         if (j == 0) {
           m_used = m_new;
         } else {
-          mbar_wait(&o_done[g], (j - 1) & 1);  // PV of block j-1 done: P buffer free, O stable
-          tc_fence_after();
+          // S_g(j) was issued after PV_g(j-1): O_g is stable here.
           const bool need = m_new > m_used + 8.f;
           if (__any_sync(0xffffffffu, need)) {
             const float alpha = need ? ex2(m_used - m_new) : 1.f;
@@ -279,7 +289,6 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
               for (int i = 0; i < 8; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
               tmem_st8(o_tm + c0, o);
             }
-            tmem_st_wait();
             if (need) {
               l *= alpha;
               m_used = m_new;
@@ -288,27 +297,19 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         }
         const float nm = -m_used;
         float rs0 = 0.f, rs1 = 0.f;
+        uint32_t pk[32];
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 16) {
-          uint32_t pk[8];
-#pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            const float e0 = ex2(fmaf(__uint_as_float(sv[c0 + i]), c, nm));
-            const float e1 = ex2(fmaf(__uint_as_float(sv[c0 + i + 1]), c, nm));
-            rs0 += e0;
-            rs1 += e1;
-            pk[i >> 1] = pack_bf16x2(e0, e1);
-          }
-#pragma unroll
-          for (int q2 = 0; q2 < 2; ++q2) {
-            const int chunk = (c0 >> 3) + q2;
-            *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) * 16)) =
-                make_uint4(pk[q2 * 4 + 0], pk[q2 * 4 + 1], pk[q2 * 4 + 2], pk[q2 * 4 + 3]);
-          }
+        for (int i = 0; i < 64; i += 2) {
+          const float e0 = ex2(fmaf(__uint_as_float(sv[i]), c, nm));
+          const float e1 = ex2(fmaf(__uint_as_float(sv[i + 1]), c, nm));
+          rs0 += e0;
+          rs1 += e1;
+          pk[i >> 1] = pack_bf16x2(e0, e1);
         }
+        tmem_st32(p_tm, pk);
+        tmem_st_wait();
         l += rs0 + rs1;
         tc_fence_before();
-        fence_proxy_async_smem();
         mbar_arrive(&p_ready[g]);
       }
       // combine the two halves' row sums
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       lb[hf * 128 + r] = l;
       named_bar_sync(bar_id, 256);
       l += lb[(hf ^ 1) * 128 + r];
-      mbar_wait(&o_done[g], (nkb - 1) & 1);
+      mbar_wait(&o_done[g], 0);
       tc_fence_after();
       const int qrow = q0 + g * 128 + r;
       const float inv = 1.f / l;

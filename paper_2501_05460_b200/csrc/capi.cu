@@ -3,7 +3,7 @@
 #include <cstring>
 #include <string>
 
-#include "../../include/epd.h"
+#include "epd.h"
 #include "encoder.h"
 #include "kernels.h"
 #include "mmcache.h"

@@ -6,7 +6,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/epd.h"
+#include "epd.h"
 #include "kernels.h"
 
 namespace epd {
