@@ -11,7 +11,7 @@ METRICS = {
     "duration_ns": "gpu__time_duration.sum",
     "dram_read_B": "dram__bytes_read.sum", "dram_write_B": "dram__bytes_write.sum",
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-    "tensor_pct": "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "tensor_pct": "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
     "tc_inst_pct": "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active",
     "sm_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "regs": "launch__registers_per_thread", "smem_B": "launch__shared_mem_per_block_dynamic",
