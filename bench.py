@@ -144,6 +144,9 @@ def init_dist(gpus: int):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # first collective on every rank: the NCCL communicator exists before any rank
+        # issues a grouped P2P gather (ranks with an empty shard skip those calls)
+        dist.barrier()
     return world, rank, local
 
 

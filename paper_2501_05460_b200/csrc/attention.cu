@@ -86,6 +86,9 @@ struct Cfg {
   static constexpr int OFF_BAR = OFF_RED + NQ * 2 * 2 * 128 * 4;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;
   static constexpr int THREADS = 64 + NQ * 256;
+  // TMEM column of Q_0 (bf16 pairs, DP/2 columns) right after O_0; Q_g at QT_COL + 128 g
+  static constexpr int QT_COL = 256 + DP;
+  static_assert(DP + DP / 2 <= 128 || NQ == 1, "O_g and Q_g must share a 128-column slot");
 };
 
 template <int DP, int NQ>
@@ -105,7 +108,8 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   uint64_t* s_full = bars + 13;   // [NQ] S_g(j) in TMEM (and, by issue order, PV_g(j-1) complete)
   uint64_t* p_ready = bars + 15;  // [NQ] P_g(j) written to TMEM
   uint64_t* o_done = bars + 17;   // [NQ] last PV_g complete
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 19);
+  uint64_t* q_tm = bars + 19;     // [NQ] Q_g copied into TMEM
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -132,6 +136,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       mbar_init(&s_full[g], 1);
       mbar_init(&p_ready[g], 256);
       mbar_init(&o_done[g], 1);
+      mbar_init(&q_tm[g], 256);
     }
     fence_barrier_init();
   }
@@ -176,28 +181,29 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       // Descriptors are precomputed: per MMA the issuing thread only adds a constant
       // (start address >> 4) to a base descriptor -- at N = 80..128 the tensor core
       // finishes an MMA in 40..64 cycles, so a serial descriptor build would starve it.
-      const uint64_t q_main0 = make_sdesc(smem_u32(smem + C::OFF_Q), 1024, 2);
-      const uint64_t q_tail0 = make_sdesc(smem_u32(smem + C::OFF_Q + C::MAIN * C::QK_ATOM), 256, 6);
       const uint64_t k_main0 = make_sdesc(smem_u32(smem + C::OFF_K), 1024, 2);
       const uint64_t k_tail0 = make_sdesc(smem_u32(smem + C::OFF_K + C::MAIN * C::QK_ATOM), 256, 6);
       const uint64_t v_base0 = make_sdesc_lbo(smem_u32(smem + C::OFF_V), C::V_ATOM, 256, 6);
+      // S = Q K^T with Q resident in TMEM (A operand): only K is read from smem, so the
+      // S MMAs are no longer smem-bandwidth bound (A+B from smem = 8 KB per 64 cycles).
       auto issue_s = [&](int g, int j) {
-        const uint64_t qo = (uint64_t)((g * C::QK_AL) >> 4);
         const uint64_t ko = (uint64_t)(((j % C::KS) * C::QK_AL) >> 4);
         const uint32_t d = tmem + g * 128;
+        const uint32_t qa = tmem + C::QT_COL + g * 128;
 #pragma unroll
         for (int kk = 0; kk < DP / 16; ++kk) {
           const int atom = kk >> 2;
           if (atom < C::MAIN) {
             const uint64_t off = (uint64_t)((atom * C::QK_ATOM + (kk & 3) * 32) >> 4);
-            umma_bf16(d, q_main0 + qo + off, k_main0 + ko + off, idesc_s, kk != 0);
+            umma_bf16_ts(d, qa + kk * 8, k_main0 + ko + off, idesc_s, kk != 0);
           } else {
-            umma_bf16(d, q_tail0 + qo, k_tail0 + ko, idesc_s, kk != 0);
+            umma_bf16_ts(d, qa + kk * 8, k_tail0 + ko, idesc_s, kk != 0);
           }
         }
         tc_commit(&s_full[g]);
       };
       mbar_wait(&k_full[0], 0);
+      for (int g = 0; g < nq; ++g) mbar_wait(&q_tm[g], 0);
       tc_fence_after();
       for (int g = 0; g < nq; ++g) issue_s(g, 0);
       tc_commit(&k_empty[0]);
@@ -247,6 +253,32 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     const float c = p.scale * 1.4426950408889634f;
     const int bar_id = 1 + g;
     if (g < nq) {
+      {
+        // copy this thread's half of its Q row (K-major swizzled smem) into TMEM as bf16
+        // pairs: column c of Q_g holds head dims 2c, 2c+1 (the TS-MMA A-operand layout)
+        mbar_wait(q_full, 0);
+        const uint8_t* qs = smem + C::OFF_Q + g * C::QK_AL;
+        const uint32_t q_tm_addr = tmem + lane_off + C::QT_COL + g * 128 + hf * (DP / 4);
+#pragma unroll
+        for (int c8 = 0; c8 < DP / 16; ++c8) {  // 8-dim chunks of this half
+          const int d = hf * (DP / 2) + c8 * 8;
+          uint4 u;
+          if (d < C::MAIN * 64) {
+            const int atom = d >> 6, ch = (d & 63) >> 3;
+            u = *reinterpret_cast<const uint4*>(qs + atom * C::QK_ATOM + r * 128 + ((ch ^ (r & 7)) * 16));
+          } else {
+            const int ch = (d - C::MAIN * 64) >> 3;
+            u = *reinterpret_cast<const uint4*>(qs + C::MAIN * C::QK_ATOM + r * 32 + ((ch ^ ((r >> 2) & 1)) * 16));
+          }
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(q_tm_addr + c8 * 4),
+                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                       : "memory");
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&q_tm[g]);
+      }
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkb; ++j) {
         const int kvalid = p.Tk - j * C::KB - hf * 64;  // valid keys among this thread's 64
