@@ -94,6 +94,14 @@ epd_status_t epd_encoder_finalize(epd_encoder_t* enc, void* stream);
 /* tiles: device uint8 [n][S][S][C] (HWC); out: device bf16 [n][out_tokens][out_dim]. */
 epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t n, void* out,
                               void* stream);
+/* fp32 check mode (north star: <= 1e-4 vs the fp32 oracle). Call before
+ * finalize; the library then also keeps fp32 twins of every weight image and
+ * epd_encode_tiles_f32 runs the same pipeline (same layouts and fusions) on
+ * fp32 CUDA cores. A verification path, not a serving path. */
+epd_status_t epd_encoder_enable_fp32_check(epd_encoder_t* enc);
+/* tiles: device uint8 [n][S][S][C]; out: device fp32 [n][out_tokens][out_dim]. */
+epd_status_t epd_encode_tiles_f32(epd_encoder_t* enc, const uint8_t* tiles, int32_t n, float* out,
+                                  void* stream);
 /* Algorithmic FLOPs of one tile (roofline numerator). */
 double epd_encoder_flops_per_tile(const epd_encoder_t* enc);
 /* Kernel launches issued by one epd_encode_tiles call over n tiles. */

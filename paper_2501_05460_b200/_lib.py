@@ -55,6 +55,8 @@ _SIGS = {
     "epd_encoder_set_weight": (_i32, [_vp, _i32, _vp, _i64]),
     "epd_encoder_finalize": (_i32, [_vp, _vp]),
     "epd_encode_tiles": (_i32, [_vp, _vp, _i32, _vp, _vp]),
+    "epd_encoder_enable_fp32_check": (_i32, [_vp]),
+    "epd_encode_tiles_f32": (_i32, [_vp, _vp, _i32, _vp, _vp]),
     "epd_encoder_flops_per_tile": (C.c_double, [_vp]),
     "epd_encoder_launches": (_i32, [_vp, _i32]),
     "epd_encoder_set_graphs": (_i32, [_vp, _i32]),

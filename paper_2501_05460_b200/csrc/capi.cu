@@ -183,6 +183,22 @@ epd_status_t epd_encode_tiles(epd_encoder_t* enc, const uint8_t* tiles, int32_t 
   return EPD_OK;
 }
 
+epd_status_t epd_encoder_enable_fp32_check(epd_encoder_t* enc) {
+  if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
+  if (enc->impl.finalized) return fail(EPD_ERR_RUNTIME, "fp32 check mode must be enabled before finalize");
+  enc->impl.check_f32 = true;
+  return EPD_OK;
+}
+
+epd_status_t epd_encode_tiles_f32(epd_encoder_t* enc, const uint8_t* tiles, int32_t n, float* out, void* stream) {
+  if (!enc) return fail(EPD_ERR_VALUE, "null encoder");
+  if (n > 0 && (!tiles || !out)) return fail(EPD_ERR_VALUE, "null tile or output buffer");
+  std::string err;
+  int rc = enc->impl.encode_f32(tiles, n, out, S(stream), err);
+  if (rc) return fail((epd_status_t)rc, err);
+  return EPD_OK;
+}
+
 double epd_encoder_flops_per_tile(const epd_encoder_t* enc) { return enc ? enc->impl.flops_per_tile() : 0.0; }
 int32_t epd_encoder_launches(const epd_encoder_t* enc, int32_t n) { return enc ? enc->impl.launches(n) : 0; }
 

@@ -8,6 +8,7 @@
 //        2-D sincos key positions, ln_post, proj)
 //   2  InternVL2: InternViT-300M (CLS token, layer scale, GELU-erf, no post-LN)
 //      + pixel shuffle 0.5 + mlp1 (LN, Linear, GELU, Linear)
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -38,6 +39,8 @@ Encoder::Encoder(const epd_encoder_desc_t& desc, int device) : d(desc), dev(devi
 Encoder::~Encoder() {
   if (blob) cudaFree(blob);
   if (work) cudaFree(work);
+  if (blob32) cudaFree(blob32);
+  if (work32) cudaFree(work32);
   for (auto e : prof_events) cudaEventDestroy(e);
   for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
   if (cap_stream) cudaStreamDestroy(cap_stream);
@@ -186,55 +189,59 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
       err = "weight not set: " + slots[i].name;
       return EPD_ERR_VALUE;
     }
-  // ---- build the bf16 device images on the host (B200 layouts)
-  std::vector<std::pair<bf16**, std::vector<uint16_t>>> images;
-  auto plain = [&](bf16** dst, int slot) {
-    std::vector<uint16_t> v(numel(slot));
-    const float* h = host(slot);
-    for (size_t i = 0; i < v.size(); ++i) v[i] = f2bf(h[i]);
-    images.emplace_back(dst, std::move(v));
+  // ---- build the device images on the host (B200 layouts). Each image is
+  // uploaded as bf16 and, in fp32 check mode, also as an fp32 twin.
+  struct Image {
+    bf16** dst;
+    float** dst32;
+    std::vector<float> v;
   };
-  auto transposed = [&](bf16** dst, int slot, int rows, int cols) {  // out[c][r] = in[r][c]
-    std::vector<uint16_t> v((size_t)rows * cols);
+  std::vector<Image> images;
+  auto plain = [&](bf16** dst, float** dst32, int slot) {
+    images.push_back({dst, dst32, std::vector<float>(host(slot), host(slot) + numel(slot))});
+  };
+  auto transposed = [&](bf16** dst, float** dst32, int slot, int rows, int cols) {  // out[c][r] = in[r][c]
+    std::vector<float> v((size_t)rows * cols);
     const float* h = host(slot);
     for (int r = 0; r < rows; ++r)
-      for (int c = 0; c < cols; ++c) v[(size_t)c * rows + r] = f2bf(h[(size_t)r * cols + c]);
-    images.emplace_back(dst, std::move(v));
+      for (int c = 0; c < cols; ++c) v[(size_t)c * rows + r] = h[(size_t)r * cols + c];
+    images.push_back({dst, dst32, std::move(v)});
   };
   // head-padded projection rows: sections s (source slot, row offset), heads nh of dim hd -> pad hp
-  auto headpad_w = [&](bf16** dst, const std::vector<std::pair<int, int>>& secs, int nh, int hd, int hp,
-                       int K) {
-    std::vector<uint16_t> v((size_t)secs.size() * nh * hp * K, 0);
+  auto headpad_w = [&](bf16** dst, float** dst32, const std::vector<std::pair<int, int>>& secs, int nh, int hd,
+                       int hp, int K) {
+    std::vector<float> v((size_t)secs.size() * nh * hp * K, 0.f);
     for (size_t s = 0; s < secs.size(); ++s) {
       const float* h = host(secs[s].first) + (size_t)secs[s].second * K;
       for (int hh = 0; hh < nh; ++hh)
         for (int dd = 0; dd < hd; ++dd) {
           const float* src = h + (size_t)(hh * hd + dd) * K;
-          uint16_t* o = v.data() + ((s * nh + hh) * (size_t)hp + dd) * K;
-          for (int k = 0; k < K; ++k) o[k] = f2bf(src[k]);
+          std::copy(src, src + K, v.data() + ((s * nh + hh) * (size_t)hp + dd) * K);
         }
     }
-    images.emplace_back(dst, std::move(v));
+    images.push_back({dst, dst32, std::move(v)});
   };
-  auto headpad_b = [&](bf16** dst, const std::vector<std::pair<int, int>>& secs, int nh, int hd, int hp) {
-    std::vector<uint16_t> v((size_t)secs.size() * nh * hp, 0);
+  auto headpad_b = [&](bf16** dst, float** dst32, const std::vector<std::pair<int, int>>& secs, int nh, int hd,
+                       int hp) {
+    std::vector<float> v((size_t)secs.size() * nh * hp, 0.f);
     for (size_t s = 0; s < secs.size(); ++s) {
       const float* h = host(secs[s].first) + secs[s].second;
       for (int hh = 0; hh < nh; ++hh)
-        for (int dd = 0; dd < hd; ++dd) v[(s * nh + hh) * hp + dd] = f2bf(h[hh * hd + dd]);
+        for (int dd = 0; dd < hd; ++dd) v[(s * nh + hh) * hp + dd] = h[hh * hd + dd];
     }
-    images.emplace_back(dst, std::move(v));
+    images.push_back({dst, dst32, std::move(v)});
   };
+#define EPD_G(field) &dw.field, &dw32.field
+#define EPD_L(field) &o.field, &o32.field
 
   // patch embedding [D][C*p*p] padded to Kpad columns
   {
-    std::vector<uint16_t> v((size_t)D * Kpad, 0);
+    std::vector<float> v((size_t)D * Kpad, 0.f);
     const float* h = host(w_pe);
-    for (int r = 0; r < D; ++r)
-      for (int k = 0; k < Kreal; ++k) v[(size_t)r * Kpad + k] = f2bf(h[(size_t)r * Kreal + k]);
-    images.emplace_back(&dw.pe, std::move(v));
+    for (int r = 0; r < D; ++r) std::copy(h + (size_t)r * Kreal, h + (size_t)(r + 1) * Kreal, v.data() + (size_t)r * Kpad);
+    images.push_back({EPD_G(pe), std::move(v)});
   }
-  plain(&dw.pe_b, b_pe);
+  plain(EPD_G(pe_b), b_pe);
   {
     // additive table applied in the patch-embed epilogue as resid[row % T]:
     // rows carry the position embedding; InternViT's CLS row (whose patch row
@@ -242,67 +249,77 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
     std::vector<float> pos(host(w_pos), host(w_pos) + (size_t)T * D);
     if (d.family == EPD_FAMILY_INTERNVIT_MLP)
       for (int c = 0; c < D; ++c) pos[c] += host(w_cls)[c] - host(b_pe)[c];
-    std::vector<uint16_t> v(pos.size());
-    for (size_t i = 0; i < pos.size(); ++i) v[i] = f2bf(pos[i]);
-    images.emplace_back(&dw.pos, std::move(v));
+    images.push_back({EPD_G(pos), std::move(pos)});
   }
   dl.resize(lslots.size());
+  dl32.resize(lslots.size());
   for (size_t l = 0; l < lslots.size(); ++l) {
     const auto& s = lslots[l];
     auto& o = dl[l];
-    plain(&o.ln1w, s.ln1w);
-    plain(&o.ln1b, s.ln1b);
+    auto& o32 = dl32[l];
+    plain(EPD_L(ln1w), s.ln1w);
+    plain(EPD_L(ln1b), s.ln1b);
     if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
-      headpad_w(&o.qkv, {{s.qw, 0}, {s.kw, 0}, {s.vw, 0}}, H, dh, Dp, D);
-      headpad_b(&o.qkvb, {{s.qb, 0}, {s.kb, 0}, {s.vb, 0}}, H, dh, Dp);
+      headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.kw, 0}, {s.vw, 0}}, H, dh, Dp, D);
+      headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.kb, 0}, {s.vb, 0}}, H, dh, Dp);
     } else {
-      headpad_w(&o.qkv, {{s.qw, 0}, {s.qw, D}, {s.qw, 2 * D}}, H, dh, Dp, D);
-      headpad_b(&o.qkvb, {{s.qb, 0}, {s.qb, D}, {s.qb, 2 * D}}, H, dh, Dp);
+      headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.qw, D}, {s.qw, 2 * D}}, H, dh, Dp, D);
+      headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.qb, D}, {s.qb, 2 * D}}, H, dh, Dp);
     }
-    plain(&o.ow, s.ow);
-    plain(&o.ob, s.ob);
-    plain(&o.ln2w, s.ln2w);
-    plain(&o.ln2b, s.ln2b);
-    plain(&o.f1w, s.f1w);
-    plain(&o.f1b, s.f1b);
-    plain(&o.f2w, s.f2w);
-    plain(&o.f2b, s.f2b);
+    plain(EPD_L(ow), s.ow);
+    plain(EPD_L(ob), s.ob);
+    plain(EPD_L(ln2w), s.ln2w);
+    plain(EPD_L(ln2b), s.ln2b);
+    plain(EPD_L(f1w), s.f1w);
+    plain(EPD_L(f1b), s.f1b);
+    plain(EPD_L(f2w), s.f2w);
+    plain(EPD_L(f2b), s.f2b);
     if (d.family == EPD_FAMILY_INTERNVIT_MLP) {
-      plain(&o.ls1, s.ls1);
-      plain(&o.ls2, s.ls2);
+      plain(EPD_L(ls1), s.ls1);
+      plain(EPD_L(ls2), s.ls2);
     }
   }
-  bf16 *rs_query = nullptr, *rs_lnq_w = nullptr, *rs_lnq_b = nullptr, *rs_qw = nullptr, *rs_qb = nullptr,
-       *rs_kw = nullptr, *rs_pos = nullptr;
+  // inputs of the weight-only precomputations below (bf16 and fp32 twins)
+  struct RsTmp {
+    bf16 *query = nullptr, *lnq_w = nullptr, *lnq_b = nullptr, *qw = nullptr, *qb = nullptr, *kw = nullptr,
+         *pos = nullptr;
+  } rs;
+  struct RsTmp32 {
+    float *query = nullptr, *lnq_w = nullptr, *lnq_b = nullptr, *qw = nullptr, *qb = nullptr, *kw = nullptr,
+          *pos = nullptr;
+  } rs32;
+#define EPD_R(field) &rs.field, &rs32.field
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
-    plain(&dw.post_w, w_post_w);
-    plain(&dw.post_b, w_post_b);
-    plain(&dw.r_kv, r_kv);
-    plain(&dw.r_lnkv_w, r_lnkv_w);
-    plain(&dw.r_lnkv_b, r_lnkv_b);
-    headpad_w(&dw.r_kvin, {{r_kw, 0}, {r_vw, 0}}, RH, rdh, RDp, E);
-    headpad_b(&dw.r_kvin_b, {{r_kb, 0}, {r_vb, 0}}, RH, rdh, RDp);
-    plain(&dw.r_ow, r_ow);
-    plain(&dw.r_ob, r_ob);
-    plain(&dw.r_lnp_w, r_lnp_w);
-    plain(&dw.r_lnp_b, r_lnp_b);
-    transposed(&dw.r_projT, r_proj, E, E);
-    // inputs for the weight-only precomputations below
-    plain(&rs_query, r_query);
-    plain(&rs_lnq_w, r_lnq_w);
-    plain(&rs_lnq_b, r_lnq_b);
-    headpad_w(&rs_qw, {{r_qw, 0}}, RH, rdh, RDp, E);
-    headpad_b(&rs_qb, {{r_qb, 0}}, RH, rdh, RDp);
-    headpad_w(&rs_kw, {{r_kw, 0}}, RH, rdh, RDp, E);
-    plain(&rs_pos, r_pos);
+    plain(EPD_G(post_w), w_post_w);
+    plain(EPD_G(post_b), w_post_b);
+    plain(EPD_G(r_kv), r_kv);
+    plain(EPD_G(r_lnkv_w), r_lnkv_w);
+    plain(EPD_G(r_lnkv_b), r_lnkv_b);
+    headpad_w(EPD_G(r_kvin), {{r_kw, 0}, {r_vw, 0}}, RH, rdh, RDp, E);
+    headpad_b(EPD_G(r_kvin_b), {{r_kb, 0}, {r_vb, 0}}, RH, rdh, RDp);
+    plain(EPD_G(r_ow), r_ow);
+    plain(EPD_G(r_ob), r_ob);
+    plain(EPD_G(r_lnp_w), r_lnp_w);
+    plain(EPD_G(r_lnp_b), r_lnp_b);
+    transposed(EPD_G(r_projT), r_proj, E, E);
+    plain(EPD_R(query), r_query);
+    plain(EPD_R(lnq_w), r_lnq_w);
+    plain(EPD_R(lnq_b), r_lnq_b);
+    headpad_w(EPD_R(qw), {{r_qw, 0}}, RH, rdh, RDp, E);
+    headpad_b(EPD_R(qb), {{r_qb, 0}}, RH, rdh, RDp);
+    headpad_w(EPD_R(kw), {{r_kw, 0}}, RH, rdh, RDp, E);
+    plain(EPD_R(pos), r_pos);
   } else {
-    plain(&dw.m_ln_w, m_ln_w);
-    plain(&dw.m_ln_b, m_ln_b);
-    plain(&dw.m_f1w, m_f1w);
-    plain(&dw.m_f1b, m_f1b);
-    plain(&dw.m_f2w, m_f2w);
-    plain(&dw.m_f2b, m_f2b);
+    plain(EPD_G(m_ln_w), m_ln_w);
+    plain(EPD_G(m_ln_b), m_ln_b);
+    plain(EPD_G(m_f1w), m_f1w);
+    plain(EPD_G(m_f1b), m_f1b);
+    plain(EPD_G(m_f2w), m_f2w);
+    plain(EPD_G(m_f2b), m_f2b);
   }
+#undef EPD_G
+#undef EPD_L
+#undef EPD_R
 
   // ---- derived device tensors and workspace sizes
   const size_t nt = d.max_tiles;
@@ -314,22 +331,40 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   } else {
     derived += align256(nt * Q * 4 * sizeof(int32_t));        // pixel-shuffle gather index
   }
-  size_t wbytes = derived;
-  for (auto& im : images) wbytes += align256(im.second.size() * 2);
+  size_t wbytes = derived, wbytes32 = 0;
+  for (auto& im : images) wbytes += align256(im.v.size() * 2);
+  if (check_f32) {
+    wbytes32 = derived * 2;
+    for (auto& im : images) wbytes32 += align256(im.v.size() * 4);
+  }
   cudaError_t e = cudaMalloc(&blob, wbytes);
+  if (e == cudaSuccess && check_f32) e = cudaMalloc(&blob32, wbytes32);
   if (e != cudaSuccess) {
     err = std::string("cudaMalloc(weights): ") + cudaGetErrorString(e);
     return EPD_ERR_CUDA;
   }
   Arena a{reinterpret_cast<uint8_t*>(blob), 0, wbytes};
+  Arena a32{reinterpret_cast<uint8_t*>(blob32), 0, wbytes32};
   for (auto& im : images) {
-    void* p = a.take(im.second.size() * 2);
-    e = cudaMemcpy(p, im.second.data(), im.second.size() * 2, cudaMemcpyHostToDevice);
+    std::vector<uint16_t> hb(im.v.size());
+    for (size_t i = 0; i < hb.size(); ++i) hb[i] = f2bf(im.v[i]);
+    void* p = a.take(hb.size() * 2);
+    e = cudaMemcpy(p, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
+    *im.dst = reinterpret_cast<bf16*>(p);
+    if (e == cudaSuccess && check_f32) {
+      void* p32 = a32.take(im.v.size() * 4);
+      e = cudaMemcpy(p32, im.v.data(), im.v.size() * 4, cudaMemcpyHostToDevice);
+      *im.dst32 = reinterpret_cast<float*>(p32);
+    }
     if (e != cudaSuccess) {
       err = std::string("cudaMemcpy(weights): ") + cudaGetErrorString(e);
       return EPD_ERR_CUDA;
     }
-    *im.first = reinterpret_cast<bf16*>(p);
+    std::vector<float>().swap(im.v);
+  }
+  if (check_f32 && d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
+    dw32.r_qheads = reinterpret_cast<float*>(a32.take((size_t)RH * Q * RDp * 4));
+    dw32.r_posk = reinterpret_cast<float*>(a32.take((size_t)T * 2 * RH * RDp * 4));
   }
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
     dw.r_qheads = reinterpret_cast<bf16*>(a.take((size_t)RH * Q * RDp * 2));
@@ -348,6 +383,7 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
             idx[((t * Q) + a2 * g2 + b2) * 4 + s] = (int32_t)(t * T + 1 + pa * grid + pb);
           }
     cudaMemcpy(dw.ps_idx, idx.data(), idx.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    dw32.ps_idx = dw.ps_idx;
   }
 
   // workspace
@@ -413,14 +449,14 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
     // temporaries live in the (not yet used) MLP buffer
     bf16* qn = ws.f;
-    rc = layernorm_bf16(rs_query, E, qn, E, rs_lnq_w, rs_lnq_b, Q, E, 1e-6f, stream);
+    rc = layernorm_bf16(rs.query, E, qn, E, rs.lnq_w, rs.lnq_b, Q, E, 1e-6f, stream);
     if (!rc) {
       EpiParams ep;
       ep.mode = EPI_HEADS;
-      ep.bias = rs_qb;
+      ep.bias = rs.qb;
       ep.H = RH; ep.Dp = RDp; ep.T = Q; ep.Tpad = Q; ep.sec_cols = RH * RDp;
       ep.sec_out[0] = dw.r_qheads;
-      rc = gemm_bf16(qn, E, rs_qw, E, Q, RH * RDp, E, ep, stream);
+      rc = gemm_bf16(qn, E, rs.qw, E, Q, RH * RDp, E, ep, stream);
     }
     if (!rc) {
       // pos_k[t][0:RH*RDp] = pos[t] @ Wk^T (head padded); second half (V section) = 0
@@ -428,7 +464,31 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
       EpiParams ep;
       ep.out = dw.r_posk;
       ep.ldo = 2 * RH * RDp;
-      rc = gemm_bf16(rs_pos, E, rs_kw, E, T, RH * RDp, E, ep, stream);
+      rc = gemm_bf16(rs.pos, E, rs.kw, E, T, RH * RDp, E, ep, stream);
+    }
+    if (!rc && check_f32) {
+      // fp32 twins; temporaries in the (unused) fp32 blob tail would cost memory,
+      // so borrow a cudaMalloc scratch for the normalised queries.
+      float* qn32 = nullptr;
+      rc = (int)cudaMalloc(&qn32, (size_t)Q * E * 4);
+      if (!rc) rc = layernorm_f32_check(rs32.query, E, qn32, E, rs32.lnq_w, rs32.lnq_b, Q, E, 1e-6f, nullptr, 1, stream);
+      if (!rc) {
+        EpiF32 ep;
+        ep.mode = EPI_HEADS;
+        ep.bias = rs32.qb;
+        ep.H = RH; ep.Dp = RDp; ep.T = Q; ep.sec_cols = RH * RDp;
+        ep.sec_out[0] = dw32.r_qheads;
+        rc = gemm_f32(qn32, E, rs32.qw, E, Q, RH * RDp, E, ep, stream);
+      }
+      if (!rc) {
+        cudaMemsetAsync(dw32.r_posk, 0, (size_t)T * 2 * RH * RDp * 4, stream);
+        EpiF32 ep;
+        ep.out = dw32.r_posk;
+        ep.ldo = 2 * RH * RDp;
+        rc = gemm_f32(rs32.pos, E, rs32.kw, E, T, RH * RDp, E, ep, stream);
+      }
+      if (!rc) rc = (int)cudaStreamSynchronize(stream);
+      if (qn32) cudaFree(qn32);
     }
   }
   if (!rc) rc = (int)cudaStreamSynchronize(stream);
@@ -715,6 +775,156 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ep.bias = dw.m_f2b;
       ep.out = out; ep.ldo = E;
       EPD_LAUNCH(PROF_GEMM, 2.0 * dQ * dE * dE, 0, gemm_bf16(ws.rr, E, dw.m_f2w, E, nt * Q, E, E, ep, s));
+    }
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------ fp32 check mode
+
+int Encoder::encode_f32(const uint8_t* tiles, int n, float* out, cudaStream_t s, std::string& err) {
+  if (!finalized || !check_f32) {
+    err = "fp32 check mode: enable it before finalize";
+    return EPD_ERR_RUNTIME;
+  }
+  if (n < 0) {
+    err = "tile count must be non-negative";
+    return EPD_ERR_VALUE;
+  }
+  if (!work32) {
+    f32_chunk = std::min(d.max_tiles, 4);
+    const size_t nt = f32_chunk, M = nt * T;
+    size_t wsz = 0;
+    auto plan = [&](size_t floats) {
+      size_t o = wsz;
+      wsz += align256(floats * 4);
+      return o;
+    };
+    const size_t o_xp = plan(M * Kpad), o_h = plan(M * D), o_xn = plan(M * D), o_ao = plan(M * D);
+    const size_t o_q = plan(nt * H * T * Dp), o_k = plan(nt * H * T * Dp), o_v = plan(nt * H * T * Dp);
+    const size_t o_f = plan(M * std::max(F, E));
+    const bool siglip = d.family == EPD_FAMILY_SIGLIP_RESAMPLER;
+    const size_t o_r2 = plan(siglip ? M * E : nt * Q * 4 * (size_t)D);
+    const size_t o_rk = plan(siglip ? nt * RH * T * RDp : 0), o_rv = plan(siglip ? nt * RH * T * RDp : 0);
+    const size_t o_rao = plan(nt * Q * (size_t)E), o_rr = plan(nt * Q * (size_t)E);
+    cudaError_t e = cudaMalloc(&work32, wsz);
+    if (e != cudaSuccess) {
+      err = std::string("cudaMalloc(fp32 workspace): ") + cudaGetErrorString(e);
+      return EPD_ERR_CUDA;
+    }
+    cudaMemsetAsync(work32, 0, wsz, s);
+    float* b = reinterpret_cast<float*>(work32);
+    auto at = [&](size_t off) { return reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(b) + off); };
+    ws32 = {at(o_xp), at(o_h), at(o_xn), at(o_ao), at(o_q), at(o_k), at(o_v),
+            at(o_f), at(o_r2), at(o_rk), at(o_rv), at(o_rao), at(o_rr)};
+  }
+  const size_t tile_bytes = (size_t)d.image_size * d.image_size * d.channels;
+  for (int c0 = 0; c0 < n; c0 += f32_chunk) {
+    const int nt = std::min(f32_chunk, n - c0);
+    const int rc = forward_f32(tiles + (size_t)c0 * tile_bytes, nt, out + (size_t)c0 * Q * E, s);
+    if (rc) {
+      err = "fp32 check launch failed (code " + std::to_string(rc) + ")";
+      return EPD_ERR_CUDA;
+    }
+  }
+  return EPD_OK;
+}
+
+// Same schedule and fusions as forward_chunk, every tensor fp32.
+int Encoder::forward_f32(const uint8_t* tiles, int nt, float* out, cudaStream_t s) {
+  const int M = nt * T;
+  const float eps = d.ln_eps;
+  const bool internvl = d.family == EPD_FAMILY_INTERNVIT_MLP;
+  const auto& W = dw32;
+  const auto& X = ws32;
+  if (internvl) EPD_TRY((int)cudaMemsetAsync(X.xp, 0, (size_t)M * Kpad * 4, s));
+  EPD_TRY(patchify_f32(tiles, nt, d.image_size, d.channels, d.patch_size, Kpad, internvl ? 1 : 0, T, d.mean,
+                       d.std, X.xp, s));
+  {
+    EpiF32 ep;
+    ep.bias = W.pe_b;
+    ep.resid = W.pos; ep.ldr = D; ep.r_mod = T;
+    ep.out = X.h; ep.ldo = D;
+    EPD_TRY(gemm_f32(X.xp, Kpad, W.pe, Kpad, M, D, Kpad, ep, s));
+  }
+  const int act = internvl ? ACT_GELU_ERF : ACT_GELU_TANH;
+  for (const auto& w : dl32) {
+    EPD_TRY(layernorm_f32_check(X.h, D, X.xn, D, w.ln1w, w.ln1b, M, D, eps, nullptr, 1, s));
+    {
+      EpiF32 ep;
+      ep.mode = EPI_HEADS;
+      ep.bias = w.qkvb;
+      ep.H = H; ep.Dp = Dp; ep.T = T; ep.sec_cols = H * Dp;
+      ep.sec_out[0] = X.q; ep.sec_out[1] = X.k; ep.sec_out[2] = X.v;
+      EPD_TRY(gemm_f32(X.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
+    }
+    EPD_TRY(attention_f32(X.q, X.k, X.v, X.ao, nt, H, T, T, Dp, dh, D, 0, 1.f / std::sqrt((float)dh), s));
+    {
+      EpiF32 ep;
+      ep.bias = w.ob; ep.lscale = w.ls1;
+      ep.accumulate = 1;
+      ep.out = X.h; ep.ldo = D;
+      EPD_TRY(gemm_f32(X.ao, D, w.ow, D, M, D, D, ep, s));
+    }
+    EPD_TRY(layernorm_f32_check(X.h, D, X.xn, D, w.ln2w, w.ln2b, M, D, eps, nullptr, 1, s));
+    {
+      EpiF32 ep;
+      ep.bias = w.f1b; ep.act = act;
+      ep.out = X.f; ep.ldo = F;
+      EPD_TRY(gemm_f32(X.xn, D, w.f1w, D, M, F, D, ep, s));
+    }
+    {
+      EpiF32 ep;
+      ep.bias = w.f2b; ep.lscale = w.ls2;
+      ep.accumulate = 1;
+      ep.out = X.h; ep.ldo = D;
+      EPD_TRY(gemm_f32(X.f, F, w.f2w, F, M, D, F, ep, s));
+    }
+  }
+  if (!internvl) {
+    EPD_TRY(layernorm_f32_check(X.h, D, X.xn, D, W.post_w, W.post_b, M, D, eps, nullptr, 1, s));
+    {
+      EpiF32 ep;
+      ep.out = X.f; ep.ldo = E;
+      EPD_TRY(gemm_f32(X.xn, D, W.r_kv, D, M, E, D, ep, s));
+    }
+    EPD_TRY(layernorm_f32_check(X.f, E, X.r2, E, W.r_lnkv_w, W.r_lnkv_b, M, E, 1e-6f, nullptr, 1, s));
+    {
+      EpiF32 ep;
+      ep.mode = EPI_HEADS;
+      ep.bias = W.r_kvin_b;
+      ep.resid = W.r_posk; ep.ldr = 2 * RH * RDp; ep.r_mod = T;
+      ep.H = RH; ep.Dp = RDp; ep.T = T; ep.sec_cols = RH * RDp;
+      ep.sec_out[0] = X.rk; ep.sec_out[1] = X.rv;
+      EPD_TRY(gemm_f32(X.r2, E, W.r_kvin, E, M, 2 * RH * RDp, E, ep, s));
+    }
+    EPD_TRY(attention_f32(W.r_qheads, X.rk, X.rv, X.rao, nt, RH, Q, T, RDp, rdh, E, 1, 1.f / std::sqrt((float)rdh), s));
+    {
+      EpiF32 ep;
+      ep.bias = W.r_ob;
+      ep.out = X.rr; ep.ldo = E;
+      EPD_TRY(gemm_f32(X.rao, E, W.r_ow, E, nt * Q, E, E, ep, s));
+    }
+    EPD_TRY(layernorm_f32_check(X.rr, E, X.rao, E, W.r_lnp_w, W.r_lnp_b, nt * Q, E, 1e-6f, nullptr, 1, s));
+    {
+      EpiF32 ep;
+      ep.out = out; ep.ldo = E;
+      EPD_TRY(gemm_f32(X.rao, E, W.r_projT, E, nt * Q, E, E, ep, s));
+    }
+  } else {
+    const int C4 = 4 * D;
+    EPD_TRY(layernorm_f32_check(X.h, D, X.r2, C4, W.m_ln_w, W.m_ln_b, nt * Q, C4, 1e-5f, W.ps_idx, 4, s));
+    {
+      EpiF32 ep;
+      ep.bias = W.m_f1b; ep.act = ACT_GELU_ERF;
+      ep.out = X.rr; ep.ldo = E;
+      EPD_TRY(gemm_f32(X.r2, C4, W.m_f1w, C4, nt * Q, E, C4, ep, s));
+    }
+    {
+      EpiF32 ep;
+      ep.bias = W.m_f2b;
+      ep.out = out; ep.ldo = E;
+      EPD_TRY(gemm_f32(X.rr, E, W.m_f2w, E, nt * Q, E, E, ep, s));
     }
   }
   return 0;

@@ -23,27 +23,39 @@ struct LayerSlots {
   int ls1 = -1, ln2w = -1, ln2b = -1, f1w = -1, f1b = -1, f2w = -1, f2b = -1, ls2 = -1;
 };
 
-struct LayerW {
-  bf16 *ln1w = nullptr, *ln1b = nullptr, *qkv = nullptr, *qkvb = nullptr, *ow = nullptr, *ob = nullptr;
-  bf16 *ls1 = nullptr, *ln2w = nullptr, *ln2b = nullptr, *f1w = nullptr, *f1b = nullptr;
-  bf16 *f2w = nullptr, *f2b = nullptr, *ls2 = nullptr;
+// Device weight pointers; T = bf16 for the tensor-core path, float for the
+// fp32 check mode (same B200 layouts, no rounding).
+template <typename T>
+struct LayerWT {
+  T *ln1w = nullptr, *ln1b = nullptr, *qkv = nullptr, *qkvb = nullptr, *ow = nullptr, *ob = nullptr;
+  T *ls1 = nullptr, *ln2w = nullptr, *ln2b = nullptr, *f1w = nullptr, *f1b = nullptr;
+  T *f2w = nullptr, *f2b = nullptr, *ls2 = nullptr;
 };
+using LayerW = LayerWT<bf16>;
 
-struct GlobalW {
-  bf16 *pe = nullptr, *pe_b = nullptr, *pos = nullptr, *post_w = nullptr, *post_b = nullptr;
-  bf16 *r_kv = nullptr, *r_lnkv_w = nullptr, *r_lnkv_b = nullptr, *r_kvin = nullptr, *r_kvin_b = nullptr;
-  bf16 *r_ow = nullptr, *r_ob = nullptr, *r_lnp_w = nullptr, *r_lnp_b = nullptr, *r_projT = nullptr;
-  bf16 *r_qheads = nullptr, *r_posk = nullptr;
-  bf16 *m_ln_w = nullptr, *m_ln_b = nullptr, *m_f1w = nullptr, *m_f1b = nullptr, *m_f2w = nullptr,
-       *m_f2b = nullptr;
+template <typename T>
+struct GlobalWT {
+  T *pe = nullptr, *pe_b = nullptr, *pos = nullptr, *post_w = nullptr, *post_b = nullptr;
+  T *r_kv = nullptr, *r_lnkv_w = nullptr, *r_lnkv_b = nullptr, *r_kvin = nullptr, *r_kvin_b = nullptr;
+  T *r_ow = nullptr, *r_ob = nullptr, *r_lnp_w = nullptr, *r_lnp_b = nullptr, *r_projT = nullptr;
+  T *r_qheads = nullptr, *r_posk = nullptr;
+  T *m_ln_w = nullptr, *m_ln_b = nullptr, *m_f1w = nullptr, *m_f1b = nullptr, *m_f2w = nullptr,
+    *m_f2b = nullptr;
   int32_t* ps_idx = nullptr;
 };
+using GlobalW = GlobalWT<bf16>;
 
 struct Workspace {
   float* h = nullptr;  // fp32 residual stream
   bf16 *xp = nullptr, *xn = nullptr, *ao = nullptr, *q = nullptr, *k = nullptr,
        *vt = nullptr, *f = nullptr;
   bf16 *r1 = nullptr, *r2 = nullptr, *rk = nullptr, *rvt = nullptr, *rao = nullptr, *rr = nullptr;
+};
+
+// fp32 check-mode workspace (allocated on first use, chunks of f32_chunk tiles).
+struct Workspace32 {
+  float *xp = nullptr, *h = nullptr, *xn = nullptr, *ao = nullptr, *q = nullptr, *k = nullptr, *v = nullptr,
+        *f = nullptr, *r2 = nullptr, *rk = nullptr, *rv = nullptr, *rao = nullptr, *rr = nullptr;
 };
 
 enum ProfClass : int { PROF_PATCHIFY = 0, PROF_GEMM = 1, PROF_ATTN = 2, PROF_LN = 3, PROF_OTHER = 4, PROF_NCLASS = 5 };
@@ -62,6 +74,9 @@ class Encoder {
   std::string validate_and_build_schema();
   int finalize(cudaStream_t stream, std::string& err);
   int encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std::string& err);
+  // fp32 check mode (enable before finalize): same pipeline on fp32 CUDA cores.
+  int encode_f32(const uint8_t* tiles, int n, float* out, cudaStream_t s, std::string& err);
+  bool check_f32 = false;
   int launches(int n) const;
   double flops_per_tile() const;
   int64_t numel(int i) const;
@@ -79,6 +94,7 @@ class Encoder {
   const float* host(int i) const;
   int forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
   int forward_graph(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
+  int forward_f32(const uint8_t* tiles, int nt, float* out, cudaStream_t s);
   std::map<int, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
   uint8_t* in_buf = nullptr;
@@ -105,6 +121,13 @@ class Encoder {
   GlobalW dw;
   std::vector<LayerW> dl;
   Workspace ws;
+  // fp32 check mode state
+  void* blob32 = nullptr;
+  void* work32 = nullptr;
+  int f32_chunk = 0;
+  GlobalWT<float> dw32;
+  std::vector<LayerWT<float>> dl32;
+  Workspace32 ws32;
 };
 
 }  // namespace epd

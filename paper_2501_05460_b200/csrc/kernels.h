@@ -89,4 +89,32 @@ int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int 
 int gather_records(const void* src_base, const int32_t* index, int n, size_t bytes, void* dst,
                    cudaStream_t stream);
 
+// ---- fp32 check mode (check_f32.cu): CUDA-core fp32 twins of the kernels above.
+// Epilogue: x = act(acc + bias[n]) * lscale[n] + resid[row % r_mod][n]; ROWS writes
+// (or, with accumulate, adds to) out[row*ldo + n]; HEADS scatters like EpiParams
+// (natural [b*H+h][T][Dp] layout for every section).
+struct EpiF32 {
+  int mode = EPI_ROWS;
+  int act = ACT_NONE;
+  const float* bias = nullptr;
+  const float* lscale = nullptr;
+  const float* resid = nullptr;
+  int ldr = 0;
+  int r_mod = 0x7fffffff;
+  int accumulate = 0;
+  float* out = nullptr;
+  int ldo = 0;
+  int H = 0, Dp = 0, T = 0, sec_cols = 0;
+  float* sec_out[3] = {nullptr, nullptr, nullptr};
+};
+int gemm_f32(const float* A, int lda, const float* W, int ldw, int M, int N, int K, const EpiF32& ep,
+             cudaStream_t s);
+int attention_f32(const float* q, const float* k, const float* v, float* out, int B, int H, int Tq, int Tk,
+                  int Dp, int Dv, int ldo, int q_shared, float scale, cudaStream_t s);
+int layernorm_f32_check(const float* in, int ld_in, float* out, int ld_out, const float* gamma,
+                        const float* beta, int rows, int D, float eps, const int32_t* gidx, int segs,
+                        cudaStream_t s);
+int patchify_f32(const uint8_t* tiles, int n, int S, int C, int p, int Kdim, int row_offset, int rows_per_tile,
+                 const float* mean, const float* stdv, float* out, cudaStream_t s);
+
 }  // namespace epd

@@ -91,11 +91,14 @@ class VisionEncoder(EncoderSchema):
     """One GPU's encoder: bf16 weights + workspace owned by libepd.
 
     ``encode(tiles)`` maps device uint8 tiles [n, S, S, C] to MM tokens
-    [n, out_tokens, out_dim] (bf16) in tile order.
+    [n, out_tokens, out_dim] (bf16) in tile order. With ``check_fp32=True`` the
+    library also keeps fp32 weight images and ``encode_f32(tiles)`` runs the same
+    pipeline in fp32 on CUDA cores (the north star's 1e-4 check mode).
     """
 
     def __init__(self, cfg: EncoderConfig, device: torch.device | int = 0, max_tiles: int = 16,
-                 weights: dict[str, torch.Tensor] | None = None, seed: int = SEED):
+                 weights: dict[str, torch.Tensor] | None = None, seed: int = SEED,
+                 check_fp32: bool = False):
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         if self.device.type != "cuda":
             raise ValueError("VisionEncoder runs on a CUDA device only (no CPU fallback)")
@@ -109,24 +112,41 @@ class VisionEncoder(EncoderSchema):
             if tuple(t.shape) != shape:
                 raise ValueError(f"weight {name}: shape {tuple(t.shape)} != {shape}")
             call("epd_encoder_set_weight", self._h, i, C.c_void_p(t.data_ptr()), t.numel())
+        self.check_fp32 = check_fp32
+        if check_fp32:
+            call("epd_encoder_enable_fp32_check", self._h)
         with torch.cuda.device(self.device):
             stream = torch.cuda.current_stream(self.device)
             call("epd_encoder_finalize", self._h, C.c_void_p(stream.cuda_stream))
 
-    def encode(self, tiles: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def _check_io(self, tiles: torch.Tensor, out: torch.Tensor | None, dtype: torch.dtype) -> torch.Tensor:
         if tiles.device != self.device or tiles.dtype != torch.uint8:
             raise ValueError("tiles must be uint8 on the encoder's device")
-        n = tiles.shape[0]
         c = self.cfg
         if tuple(tiles.shape[1:]) != (c.image_size, c.image_size, c.channels):
             raise ValueError(f"tiles must be [n, {c.image_size}, {c.image_size}, {c.channels}]")
         if out is None:
-            out = torch.empty(n, c.out_tokens, c.out_dim, dtype=torch.bfloat16, device=self.device)
+            out = torch.empty(tiles.shape[0], c.out_tokens, c.out_dim, dtype=dtype, device=self.device)
+        if out.dtype != dtype or tuple(out.shape) != (tiles.shape[0], c.out_tokens, c.out_dim):
+            raise ValueError(f"out must be {dtype} [n, {c.out_tokens}, {c.out_dim}]")
         if not tiles.is_contiguous() or not out.is_contiguous():
             raise ValueError("tiles and out must be contiguous")
+        return out
+
+    def encode(self, tiles: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        out = self._check_io(tiles, out, torch.bfloat16)
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        call("epd_encode_tiles", self._h, C.c_void_p(tiles.data_ptr()), n, C.c_void_p(out.data_ptr()),
-             C.c_void_p(stream))
+        call("epd_encode_tiles", self._h, C.c_void_p(tiles.data_ptr()), tiles.shape[0],
+             C.c_void_p(out.data_ptr()), C.c_void_p(stream))
+        return out
+
+    def encode_f32(self, tiles: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if not self.check_fp32:
+            raise RuntimeError("encode_f32 needs VisionEncoder(check_fp32=True)")
+        out = self._check_io(tiles, out, torch.float32)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        call("epd_encode_tiles_f32", self._h, C.c_void_p(tiles.data_ptr()), tiles.shape[0],
+             C.c_void_p(out.data_ptr()), C.c_void_p(stream))
         return out
 
     # -- reference-shaped latency provider ------------------------------------------

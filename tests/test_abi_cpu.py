@@ -72,6 +72,19 @@ def test_encoder_rejects_unsupported_shapes():
         EncoderSchema(replace(INTERNVIT_300M, out_tokens=64))
 
 
+def test_fp32_check_mode_host_state():
+    """Opting into the fp32 check mode is host-only; encoding before finalize fails
+    with the reference's RuntimeError mapping, not a crash."""
+    import ctypes as C
+
+    from paper_2501_05460_b200.encoder import EncoderSchema
+    s = EncoderSchema(TINY_VIT, 1)
+    _lib.call("epd_encoder_enable_fp32_check", s._h)
+    with pytest.raises(RuntimeError):
+        _lib.call("epd_encode_tiles_f32", s._h, C.c_void_p(1), 1, C.c_void_p(1), C.c_void_p(0))
+    s.close()
+
+
 def test_weights_deterministic_and_shaped():
     import torch
 

@@ -89,3 +89,42 @@ def test_encoder_rejects_bad_input(cuda):
     with pytest.raises(ValueError):
         enc.encode_latency(None, -1)
     assert enc.encode_latency(None, 0) == 0.0
+
+
+# ---- fp32 check mode (north star: <= 1e-4 for an fp32 check mode) -----------------
+TOL_FP32 = 1e-4
+
+
+@pytest.mark.parametrize("cfg,n", [
+    (TINY_VIT, 4),
+    (SIGLIP_MINICPM.with_layers(2), 2),
+    (INTERNVIT_300M.with_layers(2), 2),
+    (SIGLIP_MINICPM, 1),
+    (INTERNVIT_300M, 1),
+])
+def test_fp32_check_mode_matches_oracle(cuda, cfg, n):
+    """The fp32 check path runs the deployed layouts and fusions (head padding, fused
+    QKV, folded key positions / CLS row, pixel-shuffle gather) without rounding; it
+    must match the fp32 oracle on the fp32 weights to 1e-4."""
+    import oracle.encoders as oe
+    from paper_2501_05460_b200.encoder import VisionEncoder, canonical_weights
+    w = canonical_weights(cfg, SEED)
+    enc = VisionEncoder(cfg, cuda, max_tiles=4, weights=w, check_fp32=True)
+    tiles = _tiles(cfg, n, seed=SEED + 100 + n)
+    y = enc.encode_f32(tiles.to(cuda))
+    yb = enc.encode(tiles.to(cuda))
+    torch.cuda.synchronize()
+    ref = oe.encode(cfg, w, tiles)
+    err = oe.relerr(y, ref)
+    errb = oe.relerr(yb, oe.encode(cfg, oe.bf16_weights(w), tiles))
+    print(f"{cfg.name}: fp32 check relerr={err:.3e}, bf16 path relerr={errb:.3e}")
+    assert y.dtype == torch.float32 and y.shape == (n, cfg.out_tokens, cfg.out_dim)
+    assert err <= TOL_FP32
+    assert errb <= TOL_BF16
+    enc.close()
+
+
+def test_fp32_check_mode_requires_opt_in(cuda):
+    _, enc = _setup(TINY_VIT, cuda)
+    with pytest.raises(RuntimeError):
+        enc.encode_f32(torch.zeros(1, TINY_VIT.image_size, TINY_VIT.image_size, 3, dtype=torch.uint8, device=cuda))
