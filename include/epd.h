@@ -117,6 +117,11 @@ epd_status_t epd_encoder_profile(epd_encoder_t* enc, int32_t on);
  * milliseconds, algorithmic FLOPs, algorithmic bytes and launch counts. */
 epd_status_t epd_encoder_profile_read(epd_encoder_t* enc, double* ms, double* flops, double* bytes,
                                       int64_t* launches, int32_t nclass);
+/* Per-launch view of the profile last drained by epd_encoder_profile_read, in
+ * issue order: class, device ms, algorithmic FLOPs. Copies min(n, cap) records
+ * and returns n (-1 for a null encoder). */
+int32_t epd_encoder_profile_launches(const epd_encoder_t* enc, int32_t* cls, float* ms, double* flops,
+                                     int32_t cap);
 
 /* ------------------------------------------------------------------ MM-token cache
  * Stands behind blocks.BlockManager(CacheKind.MM) (blocks.py:14-61) as the
@@ -195,9 +200,14 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
 /* O = softmax(Q K^T * scale) V per (batch, head); see csrc/kernels.h AttnParams.
  * q: [q_shared ? H : B*H][Tq][Dp], k and v: [B*H][Tk][Dp],
  * out[(b*Tq + i)*ldo + h*Dv + d]. Dp in {64, 80, 128}. */
+/* flags: EPD_ATTN_Q_SHARED (q is [H][Tq][Dp], shared by every batch entry);
+ * EPD_ATTN_V_ONES_COL (caller guarantees v[..., Dv] == 1 with Dv < Dp: the row
+ * sums come out of the PV MMA instead of the softmax warps). */
+#define EPD_ATTN_Q_SHARED 1
+#define EPD_ATTN_V_ONES_COL 2
 epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, void* out, int32_t B,
                                 int32_t H, int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv,
-                                int32_t ldo, int32_t q_shared, float scale, void* stream);
+                                int32_t ldo, int32_t flags, float scale, void* stream);
 epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
                                 const void* beta, int32_t rows, int32_t D, float eps, void* stream);
 /* uint8 HWC tiles [n][S][S][C] -> bf16 rows [n*rows_per_tile][Kpad], patch rows start at

@@ -1,27 +1,54 @@
-// Fused multi-head attention (bidirectional) for sm_100a, FA4-style.
+// Fused multi-head attention (bidirectional) for sm_100a.
 //
-// One CTA = NQ (1 or 2) tiles of 128 query rows of one (batch, head); the
-// tiles share every K/V block. Per 128-key block j and query tile g:
-//   S_g  = Q_g K_j^T          tcgen05.mma (A, B from smem)  M=128 N=128 K=Dp -> TMEM fp32
-//   P_g  = exp2(S_g*c - m_g)  softmax warps: TMEM -> regs -> bf16 P written back to TMEM,
-//                             aliasing the first 64 columns of S_g (no smem round trip)
-//   O_g += P_g V_j            tcgen05.mma (A = P from TMEM, B = V from smem, MN-major)
-// The running max m_g is only raised (and O_g rescaled in TMEM) when a row's
-// max grows by more than 2^8, so most blocks need no correction pass. Because
-// S_g(j+1) is issued after PV_g(j), the arrival of S_g(j) also means O_g is
-// stable and P_g(j-1) has been consumed. While one tile runs its softmax the
-// tensor core works on the other tile's PV and S.
+// One CTA = NQ (1 or 2) tiles of 128 query rows of one (batch, head); the tiles
+// share every K/V block. Per 64-key block j and query tile g:
+//   S_g(j) = Q_g K_j^T        tcgen05.mma, A = Q_g resident in TMEM, B = K from smem,
+//                             M=128 N=64 K=Dp -> fp32 S in TMEM buffer j & 1
+//   P_g(j) = exp2(S*c - m_g)  softmax warps (one thread per query row): TMEM -> regs ->
+//                             bf16 P written back over the first 32 columns of S
+//   O_g   += P_g(j) V_j       tcgen05.mma, A = P from TMEM, B = V from smem (MN-major)
+// S is double-buffered per tile, so S_g(j+1) is computed while the softmax of
+// block j runs and the softmax warps never wait for the tensor core. (With one S
+// buffer -- FA4's layout, right for head dim 128 -- a head dim of 72..80 leaves
+// the softmax -> PV -> S chain serial and the tensor pipe ~60% idle.) TMEM:
+// 4 x 64 columns of S, then O_g and Q_g in a 128-column slot each.
+// The softmax is MUFU-bound: a quarter of the exponentials run as a cubic on the
+// FMA pipe. The running max m_g is only raised (and O_g rescaled, after waiting
+// for the in-flight PV) when a row max grows by more than 2^8. With a ones column
+// in V's head padding (v_ones_col) the PV MMA also produces the row sums.
 //
-// Warps: 0 TMA (lane 0: Q, K; lane 1: V), 1 TMEM alloc + MMA issue,
-// 2..9 softmax tile 0, 10..17 tile 1 (two warps per TMEM lane quarter, each
-// owning half of the key columns and half of the head dims).
-// Layouts: Q, K, V all [bh][T][Dp] bf16 (Dp = head dim zero-padded to a
-// multiple of 16). Q/K are K-major smem operands (64-wide SW128 atoms + a
-// 16-wide SW32 tail when Dp % 64 != 0); V is the MN-major B operand from
-// 16-wide SW32 atoms (LBO = 4 KB between atoms, SBO = 256 B between 8-key groups).
+// Warps: 0 TMA (lane 0: Q, K; lane 1: V), 1 MMA issue (whole warp, elected lane),
+// 2..5 softmax tile 0, 6..9 tile 1.
+// Layouts: Q, K, V all [bh][T][Dp] bf16 (Dp = head dim zero-padded to a multiple
+// of 16). Q/K are K-major smem operands (64-wide SW128 atoms + a 16-wide SW32 tail
+// when Dp % 64 != 0); V is the MN-major B operand from 16-wide SW32 atoms
+// (LBO = 2 KB between atoms, SBO = 256 B between 8-key groups).
 #include "common.cuh"
 #include "kernels.h"
 #include "tmap.h"
+
+#ifdef EPD_ATTN_TRACE
+// Experiment-only timeline of one CTA (tools/attn_trace.py): %clock stamps in fixed
+// shared-memory slots [code 0..31][j 0..15][g 0..1], flushed to global at exit.
+__device__ unsigned int g_attn_trace[32 * 16 * 2];
+__shared__ unsigned int s_attn_trace[32 * 16 * 2];
+#define ATTN_TRACE_ON (blockIdx.x == 1 && blockIdx.y == 5 && blockIdx.z == 5)
+#define ATTN_TRACE(code, j, g)                                               \
+  do {                                                                       \
+    unsigned _c;                                                             \
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(_c));                        \
+    if ((j) < 16) s_attn_trace[((code) * 16 + (j)) * 2 + (g)] = _c;          \
+  } while (0)
+extern "C" int epd_debug_trace(unsigned int* host, int cap) {
+  const int n = cap < 1024 ? cap : 1024;
+  cudaMemcpyFromSymbol(host, g_attn_trace, n * sizeof(unsigned int));
+  return n;
+}
+#else
+#define ATTN_TRACE(code, j, g) \
+  do {                         \
+  } while (0)
+#endif
 
 namespace epd {
 
@@ -31,6 +58,32 @@ EPD_DEVICE float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (FA4's MUFU offload): round-to-nearest split x = k + f,
+// f in [-0.5, 0.5], cubic minimax for 2^f (max rel err 7.5e-5, far below the bf16
+// rounding of P), k added straight into the exponent bits. Inputs below -126 clamp
+// (the result is then ~1e-38, i.e. zero for P).
+EPD_DEVICE float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05517133f, f, 0.2426105f), f, 0.693261f), f, 0.9999281f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+#ifndef EPD_POLY_EIGHTHS
+#define EPD_POLY_EIGHTHS 2  // pairs (of every 8) whose exponentials run on the FMA pipe
+#endif
+
+EPD_DEVICE float fmax3(float a, float b, float c) {
+  float m;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(m) : "f"(a), "f"(b), "f"(c));  // FMNMX3
+  return m;
+}
+EPD_DEVICE uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  return r;
 }
 
 EPD_DEVICE void tmem_ld8(uint32_t taddr, uint32_t* r) {
@@ -57,6 +110,27 @@ EPD_DEVICE void tmem_st32(uint32_t taddr, const uint32_t* r) {
 EPD_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 EPD_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// Warp-wide issue helpers: every lane executes the call with identical (warp-uniform)
+// operands, so the compiler keeps them in uniform registers; elect.sync picks the one
+// lane that issues. (A single-lane `if (lane == 0)` issuer instead costs two R2UR moves
+// plus an elect loop per MMA -- ~70-80 issue cycles, more than a 64-key MMA executes in.)
+EPD_DEVICE void umma_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+EPD_DEVICE void tc_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // D[tmem] (+)= A[tmem] * B[smem]^T (A operand from tensor memory).
 EPD_DEVICE void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -69,26 +143,32 @@ EPD_DEVICE void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, u
 
 template <int DP, int NQ>
 struct Cfg {
-  static constexpr int KB = 128;                       // keys per block
-  static constexpr int KS = 3;                         // K pipeline stages
-  static constexpr int KVS = DP <= 80 ? 3 : 2;         // V pipeline stages (smem permitting)
+  static constexpr int KB = 64;                        // keys per block
+  static constexpr int KS = 4;                         // K pipeline stages
+  static constexpr int KVS = 4;                        // V pipeline stages
   static constexpr int MAIN = DP / 64;                 // 64-wide SW128 atoms of Q/K
   static constexpr bool TAIL = (DP % 64) != 0;         // 16-wide SW32 tail (DP % 64 == 16)
-  static constexpr int QK_ATOM = 128 * 128;            // 128 rows x 128 B
-  static constexpr int QK_BYTES = 128 * DP * 2;
-  static constexpr int QK_AL = (QK_BYTES + 1023) / 1024 * 1024;
-  static constexpr int V_ATOM = 128 * 32;              // 128 keys x 16 dims x 2 B
+  static constexpr int Q_ATOM = 128 * 128;             // 128 rows x 128 B
+  static constexpr int Q_AL = (128 * DP * 2 + 1023) / 1024 * 1024;
+  static constexpr int K_ATOM = KB * 128;              // 64 keys x 128 B
+  static constexpr int K_BYTES = KB * DP * 2;
+  static constexpr int K_AL = (K_BYTES + 1023) / 1024 * 1024;
+  static constexpr int V_ATOM = KB * 32;               // 64 keys x 16 dims x 2 B
   static constexpr int V_BYTES = (DP / 16) * V_ATOM;
+  static constexpr int V_AL = (V_BYTES + 1023) / 1024 * 1024;
   static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + NQ * QK_AL;
-  static constexpr int OFF_V = OFF_K + KS * QK_AL;
-  static constexpr int OFF_RED = OFF_V + KVS * V_BYTES;     // [NQ][2][2][128] fp32 row exchange
-  static constexpr int OFF_BAR = OFF_RED + NQ * 2 * 2 * 128 * 4;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;
-  static constexpr int THREADS = 64 + NQ * 256;
-  // TMEM column of Q_0 (bf16 pairs, DP/2 columns) right after O_0; Q_g at QT_COL + 128 g
-  static constexpr int QT_COL = 256 + DP;
+  static constexpr int OFF_K = OFF_Q + NQ * Q_AL;
+  static constexpr int OFF_V = OFF_K + KS * K_AL;
+  static constexpr int OFF_BAR = OFF_V + KVS * V_AL;
+  static constexpr int SMEM = OFF_BAR + 256 + 1024;  // 31 mbarriers + TMEM holder in the 256 B
+  static constexpr int THREADS = 64 + NQ * 128;
+  // TMEM columns: S_{g,b} (fp32, 64 wide) at (2g + b) * 64, P_{g,b} = bf16 pairs in its first
+  // 32 columns; O_g at 256 + 128 g (DP wide); Q_g (bf16 pairs, DP/2 wide) right after O_g.
+  __host__ __device__ static constexpr uint32_t s_col(int g, int b) { return (uint32_t)((2 * g + b) * 64); }
+  __host__ __device__ static constexpr uint32_t o_col(int g) { return (uint32_t)(256 + 128 * g); }
+  __host__ __device__ static constexpr uint32_t q_col(int g) { return (uint32_t)(256 + 128 * g + DP); }
   static_assert(DP + DP / 2 <= 128 || NQ == 1, "O_g and Q_g must share a 128-column slot");
+  static_assert(DP + DP / 2 <= 256, "O and Q must fit above the S buffers");
 };
 
 template <int DP, int NQ>
@@ -102,14 +182,20 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars + 0;
   uint64_t* k_full = bars + 1;    // [KS]
-  uint64_t* k_empty = bars + 4;   // [KS]
-  uint64_t* v_full = bars + 7;    // [KVS]
-  uint64_t* v_empty = bars + 10;  // [KVS]
-  uint64_t* s_full = bars + 13;   // [NQ] S_g(j) in TMEM (and, by issue order, PV_g(j-1) complete)
-  uint64_t* p_ready = bars + 15;  // [NQ] P_g(j) written to TMEM
-  uint64_t* o_done = bars + 17;   // [NQ] last PV_g complete
-  uint64_t* q_tm = bars + 19;     // [NQ] Q_g copied into TMEM
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* k_empty = bars + 5;   // [KS]
+  uint64_t* v_full = bars + 9;    // [KVS]
+  uint64_t* v_empty = bars + 13;  // [KVS]
+  uint64_t* s_full = bars + 17;   // [NQ][2] S_g(j) landed in buffer j & 1
+  // [NQ][2] P_g(j) written to TMEM buffer j & 1. One barrier per buffer: a softmax group
+  // may finish blocks j and j+1 before the MMA warp consumes P_g(j), which would alias
+  // the phase parity of a single barrier.
+  uint64_t* p_ready = bars + 21;
+  uint64_t* pv_done = bars + 25;  // [NQ] PV_g(j) complete (O_g stable up to block j)
+  uint64_t* q_tm = bars + 27;     // [NQ] Q_g copied into TMEM
+  // [NQ] last PV_g complete. (pv_done alone cannot say so: when the softmax reaches the
+  // end only PV_g(nkb-3) is known complete, two phases behind, which aliases the parity.)
+  uint64_t* o_done = bars + 29;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 31);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -133,10 +219,13 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       mbar_init(&v_empty[i], 1);
     }
     for (int g = 0; g < NQ; ++g) {
-      mbar_init(&s_full[g], 1);
-      mbar_init(&p_ready[g], 256);
+      mbar_init(&s_full[2 * g], 1);
+      mbar_init(&s_full[2 * g + 1], 1);
+      mbar_init(&p_ready[2 * g], 128);
+      mbar_init(&p_ready[2 * g + 1], 128);
+      mbar_init(&pv_done[g], 1);
       mbar_init(&o_done[g], 1);
-      mbar_init(&q_tm[g], 256);
+      mbar_init(&q_tm[g], 128);
     }
     fence_barrier_init();
   }
@@ -145,134 +234,130 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  // TMEM columns: S_g / P_g at [g*128, g*128+128) (P = bf16 pairs in the first 64),
-  // O_g at [256 + g*128, 256 + g*128 + DP)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, nq * C::QK_BYTES);
+      mbar_arrive_expect_tx(q_full, nq * 128 * DP * 2);
       for (int g = 0; g < nq; ++g) {
-        uint8_t* qd = smem + C::OFF_Q + g * C::QK_AL;
-        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(qd + a * C::QK_ATOM, &tmQ, q_full, a * 64, q0 + g * 128, qbatch);
-        if (C::TAIL) tma_load_3d(qd + C::MAIN * C::QK_ATOM, &tmQt, q_full, C::MAIN * 64, q0 + g * 128, qbatch);
+        uint8_t* qd = smem + C::OFF_Q + g * C::Q_AL;
+        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(qd + a * C::Q_ATOM, &tmQ, q_full, a * 64, q0 + g * 128, qbatch);
+        if (C::TAIL) tma_load_3d(qd + C::MAIN * C::Q_ATOM, &tmQt, q_full, C::MAIN * 64, q0 + g * 128, qbatch);
       }
       for (int j = 0; j < nkb; ++j) {
         const int s = j % C::KS;
         mbar_wait(&k_empty[s], ((j / C::KS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], C::QK_BYTES);
-        uint8_t* kd = smem + C::OFF_K + s * C::QK_AL;
-        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(kd + a * C::QK_ATOM, &tmK, &k_full[s], a * 64, j * C::KB, bh);
-        if (C::TAIL) tma_load_3d(kd + C::MAIN * C::QK_ATOM, &tmKt, &k_full[s], C::MAIN * 64, j * C::KB, bh);
+        mbar_arrive_expect_tx(&k_full[s], C::K_BYTES);
+        uint8_t* kd = smem + C::OFF_K + s * C::K_AL;
+        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(kd + a * C::K_ATOM, &tmK, &k_full[s], a * 64, j * C::KB, bh);
+        if (C::TAIL) tma_load_3d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], C::MAIN * 64, j * C::KB, bh);
       }
     } else if (lane == 1) {
       for (int j = 0; j < nkb; ++j) {
         const int s = j % C::KVS;
         mbar_wait(&v_empty[s], ((j / C::KVS) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
-        uint8_t* vd = smem + C::OFF_V + s * C::V_BYTES;
+        uint8_t* vd = smem + C::OFF_V + s * C::V_AL;
         for (int a = 0; a < DP / 16; ++a) tma_load_3d(vd + a * C::V_ATOM, &tmV, &v_full[s], a * 16, j * C::KB, bh);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // whole warp: uniform operands, elected issue
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KB);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DP) | (1u << 16);  // B (V) is MN-major
-      mbar_wait(q_full, 0);
       // Descriptors are precomputed: per MMA the issuing thread only adds a constant
-      // (start address >> 4) to a base descriptor -- at N = 80..128 the tensor core
-      // finishes an MMA in 40..64 cycles, so a serial descriptor build would starve it.
+      // (start address >> 4) to a base descriptor.
       const uint64_t k_main0 = make_sdesc(smem_u32(smem + C::OFF_K), 1024, 2);
-      const uint64_t k_tail0 = make_sdesc(smem_u32(smem + C::OFF_K + C::MAIN * C::QK_ATOM), 256, 6);
+      const uint64_t k_tail0 = make_sdesc(smem_u32(smem + C::OFF_K + C::MAIN * C::K_ATOM), 256, 6);
       const uint64_t v_base0 = make_sdesc_lbo(smem_u32(smem + C::OFF_V), C::V_ATOM, 256, 6);
-      // S = Q K^T with Q resident in TMEM (A operand): only K is read from smem, so the
-      // S MMAs are no longer smem-bandwidth bound (A+B from smem = 8 KB per 64 cycles).
+      // S_g(j) = Q_g K_j^T into buffer j & 1; Q_g is the TMEM (A) operand.
       auto issue_s = [&](int g, int j) {
-        const uint64_t ko = (uint64_t)(((j % C::KS) * C::QK_AL) >> 4);
-        const uint32_t d = tmem + g * 128;
-        const uint32_t qa = tmem + C::QT_COL + g * 128;
+        ATTN_TRACE(3, j, g);
+        const uint64_t ko = (uint64_t)(((j % C::KS) * C::K_AL) >> 4);
+        const uint32_t d = tmem + C::s_col(g, j & 1);
+        const uint32_t qa = tmem + C::q_col(g);
 #pragma unroll
         for (int kk = 0; kk < DP / 16; ++kk) {
           const int atom = kk >> 2;
           if (atom < C::MAIN) {
-            const uint64_t off = (uint64_t)((atom * C::QK_ATOM + (kk & 3) * 32) >> 4);
-            umma_bf16_ts(d, qa + kk * 8, k_main0 + ko + off, idesc_s, kk != 0);
+            const uint64_t off = (uint64_t)((atom * C::K_ATOM + (kk & 3) * 32) >> 4);
+            umma_ts_warp(d, qa + kk * 8, k_main0 + ko + off, idesc_s, kk != 0);
           } else {
-            umma_bf16_ts(d, qa + kk * 8, k_tail0 + ko, idesc_s, kk != 0);
+            umma_ts_warp(d, qa + kk * 8, k_tail0 + ko, idesc_s, kk != 0);
           }
         }
-        tc_commit(&s_full[g]);
+        tc_commit_warp(&s_full[2 * g + (j & 1)]);
+        ATTN_TRACE(4, j, g);
       };
-      mbar_wait(&k_full[0], 0);
+      mbar_wait(q_full, 0);
       for (int g = 0; g < nq; ++g) mbar_wait(&q_tm[g], 0);
-      tc_fence_after();
-      for (int g = 0; g < nq; ++g) issue_s(g, 0);
-      tc_commit(&k_empty[0]);
+      // two blocks of S in flight per query tile: softmax(j) overlaps S(j+1)
+      for (int j = 0; j < 2 && j < nkb; ++j) {
+        mbar_wait(&k_full[j % C::KS], (j / C::KS) & 1);
+        tc_fence_after();
+        for (int g = 0; g < nq; ++g) issue_s(g, j);
+        tc_commit_warp(&k_empty[j % C::KS]);
+      }
       for (int j = 0; j < nkb; ++j) {
         const int sv = j % C::KVS;
         for (int g = 0; g < nq; ++g) {
-          mbar_wait(&p_ready[g], j & 1);
+          ATTN_TRACE(5, j, g);
+          mbar_wait(&p_ready[2 * g + (j & 1)], (j >> 1) & 1);
+          ATTN_TRACE(6, j, g);
           if (g == 0) mbar_wait(&v_full[sv], (j / C::KVS) & 1);
           tc_fence_after();
-          const uint64_t vb = v_base0 + (uint64_t)((sv * C::V_BYTES) >> 4);
-          const uint32_t od = tmem + 256 + g * 128, pa = tmem + g * 128;
+          ATTN_TRACE(7, j, g);
+          const uint64_t vb = v_base0 + (uint64_t)((sv * C::V_AL) >> 4);
+          const uint32_t od = tmem + C::o_col(g), pa = tmem + C::s_col(g, j & 1);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
+          for (int kk = 0; kk < C::KB / 16; ++kk) {
             // A = P from TMEM: keys 16kk..16kk+15 are bf16 pairs in columns 8kk..8kk+7
-            // B = V, MN-major SW32: key row kk*16 (512 B), LBO = 4 KB (next 16 dims), SBO = 256 B
-            umma_bf16_ts(od, pa + kk * 8, vb + (uint64_t)(kk * 32), idesc_o, (j | kk) != 0);
+            // B = V, MN-major SW32: key row kk*16 (512 B), LBO = 2 KB (next 16 dims), SBO = 256 B
+            umma_ts_warp(od, pa + kk * 8, vb + (uint64_t)(kk * 32), idesc_o, (j | kk) != 0);
           }
-          if (j + 1 == nkb) {
-            tc_commit(&o_done[g]);
-          } else {
-            // S_g(j+1) overwrites P_g(j) only after PV_g(j) (in-order tensor pipe)
-            if (g == 0) mbar_wait(&k_full[(j + 1) % C::KS], ((j + 1) / C::KS) & 1);
+          tc_commit_warp(&pv_done[g]);
+          if (j + 1 == nkb) tc_commit_warp(&o_done[g]);
+          ATTN_TRACE(8, j, g);
+          if (j + 2 < nkb) {
+            // S_g(j+2) overwrites P_g(j) only after PV_g(j) (in-order tensor pipe)
+            if (g == 0) mbar_wait(&k_full[(j + 2) % C::KS], ((j + 2) / C::KS) & 1);
             tc_fence_after();
-            issue_s(g, j + 1);
+            issue_s(g, j + 2);
           }
         }
-        tc_commit(&v_empty[sv]);
-        if (j + 1 < nkb) tc_commit(&k_empty[(j + 1) % C::KS]);
+        tc_commit_warp(&v_empty[sv]);
+        if (j + 2 < nkb) tc_commit_warp(&k_empty[(j + 2) % C::KS]);
       }
     }
   } else {
-    // ---------------- softmax: per query tile g, 8 warps = 2 per TMEM lane quarter;
-    // thread (row r, half hf) owns key columns [hf*64, hf*64+64) of S and head dims
-    // [hf*DP/2, (hf+1)*DP/2) of O. Row maxima are combined through smem each block.
+    // ---------------- softmax: 4 warps per query tile, one thread per query row (TMEM lane)
     const int wi = warp - 2;
-    const int g = wi >> 3;
-    const int hf = (wi >> 2) & 1;
-    const int qq = warp & 3;
+    const int g = wi >> 2;
+    const int qq = warp & 3;  // TMEM lane quarter this warp may access
     const int r = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
-    const uint32_t s_tm = tmem + lane_off + g * 128 + hf * 64;
-    const uint32_t p_tm = tmem + lane_off + g * 128 + hf * 32;
-    constexpr int OH = DP / 2;  // O columns per half (multiple of 8)
-    const uint32_t o_tm = tmem + lane_off + 256 + g * 128 + hf * OH;
-    // [2 block parity][2 hf][128]: row-max exchange; the final row sums reuse a slot
-    float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + g * (2 * 2 * 128);
+    const uint32_t o_tm = tmem + lane_off + C::o_col(g);
     const float c = p.scale * 1.4426950408889634f;
-    const int bar_id = 1 + g;
+    const bool ones_col = p.v_ones_col != 0;
     if (g < nq) {
       {
-        // copy this thread's half of its Q row (K-major swizzled smem) into TMEM as bf16
-        // pairs: column c of Q_g holds head dims 2c, 2c+1 (the TS-MMA A-operand layout)
+        // copy this thread's Q row (K-major swizzled smem) into TMEM as bf16 pairs:
+        // column c of Q_g holds head dims 2c, 2c+1 (the TS-MMA A-operand layout)
         mbar_wait(q_full, 0);
-        const uint8_t* qs = smem + C::OFF_Q + g * C::QK_AL;
-        const uint32_t q_tm_addr = tmem + lane_off + C::QT_COL + g * 128 + hf * (DP / 4);
+        const uint8_t* qs = smem + C::OFF_Q + g * C::Q_AL;
+        const uint32_t q_tm_addr = tmem + lane_off + C::q_col(g);
 #pragma unroll
-        for (int c8 = 0; c8 < DP / 16; ++c8) {  // 8-dim chunks of this half
-          const int d = hf * (DP / 2) + c8 * 8;
+        for (int c8 = 0; c8 < DP / 8; ++c8) {
+          const int d = c8 * 8;
           uint4 u;
           if (d < C::MAIN * 64) {
             const int atom = d >> 6, ch = (d & 63) >> 3;
-            u = *reinterpret_cast<const uint4*>(qs + atom * C::QK_ATOM + r * 128 + ((ch ^ (r & 7)) * 16));
+            u = *reinterpret_cast<const uint4*>(qs + atom * C::Q_ATOM + r * 128 + ((ch ^ (r & 7)) * 16));
           } else {
             const int ch = (d - C::MAIN * 64) >> 3;
-            u = *reinterpret_cast<const uint4*>(qs + C::MAIN * C::QK_ATOM + r * 32 + ((ch ^ ((r >> 2) & 1)) * 16));
+            u = *reinterpret_cast<const uint4*>(qs + C::MAIN * C::Q_ATOM + r * 32 + ((ch ^ ((r >> 2) & 1)) * 16));
           }
-          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
           asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(q_tm_addr + c8 * 4),
-                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                       "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
                        : "memory");
         }
         tmem_st_wait();
@@ -281,46 +366,56 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       }
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < nkb; ++j) {
-        const int kvalid = p.Tk - j * C::KB - hf * 64;  // valid keys among this thread's 64
-        mbar_wait(&s_full[g], j & 1);
+        const bool tr = wi == 4 * g && lane == 0;
+        if (tr) ATTN_TRACE(9, j, g);
+        const int kvalid = p.Tk - j * C::KB;
+        mbar_wait(&s_full[2 * g + (j & 1)], (j >> 1) & 1);
         tc_fence_after();
+        if (tr) ATTN_TRACE(10, j, g);
+        const uint32_t s_tm = tmem + lane_off + C::s_col(g, j & 1);
         uint32_t sv[64];
         tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
         tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
         tmem_ld_wait();
-        float mx = -INFINITY;
-        if (kvalid >= 64) {
+        if (tr) ATTN_TRACE(11, j, g);
+        if (kvalid < 64) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) mx = fmaxf(mx, __uint_as_float(sv[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 64; ++i) {
+          for (int i = 0; i < 64; ++i)
             if (i >= kvalid) sv[i] = __float_as_uint(-INFINITY);
-            mx = fmaxf(mx, __uint_as_float(sv[i]));
-          }
         }
-        float* rb = red + (j & 1) * 256;
-        rb[hf * 128 + r] = mx;
-        // Both halves have read their S columns before either writes P over them.
-        named_bar_sync(bar_id, 256);
-        mx = fmaxf(mx, rb[(hf ^ 1) * 128 + r]);
+        float mx;
+        {
+          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+          for (int i = 0; i < 64; i += 8)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              m4[u] = fmax3(m4[u], __uint_as_float(sv[i + 2 * u]), __uint_as_float(sv[i + 2 * u + 1]));
+          mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
+        }
+        if (tr) ATTN_TRACE(12, j, g);
         const float m_new = fmaxf(m_used, mx * c);
         if (j == 0) {
           m_used = m_new;
         } else {
-          // S_g(j) was issued after PV_g(j-1): O_g is stable here.
+          // Lazy rescale: only when a row max grows by more than 2^8. PV_g(j-1) may still
+          // be accumulating into O_g, so wait for it first (rare path).
           const bool need = m_new > m_used + 8.f;
           if (__any_sync(0xffffffffu, need)) {
+            mbar_wait(&pv_done[g], (j - 1) & 1);
+            tc_fence_after();
             const float alpha = need ? ex2(m_used - m_new) : 1.f;
 #pragma unroll
-            for (int c0 = 0; c0 < OH; c0 += 8) {
-              uint32_t o[8];
-              tmem_ld8(o_tm + c0, o);
+            for (int c0 = 0; c0 < DP; c0 += 16) {
+              uint32_t o[16];
+              tmem_ld16(o_tm + c0, o);
               tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 8; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
               tmem_st8(o_tm + c0, o);
+              tmem_st8(o_tm + c0 + 8, o + 8);
             }
+            tmem_st_wait();
             if (need) {
               l *= alpha;
               m_used = m_new;
@@ -332,42 +427,51 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 64; i += 2) {
-          const float e0 = ex2(fmaf(__uint_as_float(sv[i]), c, nm));
-          const float e1 = ex2(fmaf(__uint_as_float(sv[i + 1]), c, nm));
-          rs0 += e0;
-          rs1 += e1;
+          // The softmax is MUFU-bound (16 ex2/clk/SM): a share of the pairs goes to the FMA pipe.
+          const bool poly = ((i >> 1) & 7) < EPD_POLY_EIGHTHS;
+          const float a0 = fmaf(__uint_as_float(sv[i]), c, nm), a1 = fmaf(__uint_as_float(sv[i + 1]), c, nm);
+          const float e0 = poly ? ex2_poly(a0) : ex2(a0);
+          const float e1 = poly ? ex2_poly(a1) : ex2(a1);
+          if (!ones_col) {
+            rs0 += e0;
+            rs1 += e1;
+          }
           pk[i >> 1] = pack_bf16x2(e0, e1);
         }
-        tmem_st32(p_tm, pk);
+        if (tr) ATTN_TRACE(14, j, g);
+        tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
         tmem_st_wait();
-        l += rs0 + rs1;
+        if (!ones_col) l += rs0 + rs1;
         tc_fence_before();
-        mbar_arrive(&p_ready[g]);
+        mbar_arrive(&p_ready[2 * g + (j & 1)]);
+        if (tr) ATTN_TRACE(15, j, g);
       }
-      // combine the two halves' row sums
-      // the parity slot of block nkb was last read during block nkb-2's exchange, which
-      // every thread of the group has passed (block nkb-1's barrier): safe to reuse
-      float* lb = red + (nkb & 1) * 256;
-      lb[hf * 128 + r] = l;
-      named_bar_sync(bar_id, 256);
-      l += lb[(hf ^ 1) * 128 + r];
       mbar_wait(&o_done[g], 0);
       tc_fence_after();
+      if (ones_col) {
+        // O[:, Dv] = sum_k P[k] * 1: the row sum of the (bf16) P the MMA actually used
+        l = __uint_as_float(tmem_ld1(o_tm + p.Dv));
+        tmem_ld_wait();
+      }
       const int qrow = q0 + g * 128 + r;
       const float inv = 1.f / l;
-      bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv + hf * OH;
+      bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv;
 #pragma unroll
-      for (int c0 = 0; c0 < OH; c0 += 8) {
-        uint32_t o[8];
-        tmem_ld8(o_tm + c0, o);
+      for (int c0 = 0; c0 < DP; c0 += 16) {
+        uint32_t o[16];
+        tmem_ld16(o_tm + c0, o);
         tmem_ld_wait();
-        if (qrow < p.Tq && hf * OH + c0 < p.Dv) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv);
-          v.y = pack_bf16x2(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv);
-          v.z = pack_bf16x2(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv);
-          v.w = pack_bf16x2(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c0) = v;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (qrow < p.Tq && c0 + hh * 8 < p.Dv) {
+            const uint32_t* oo = o + hh * 8;
+            uint4 v;
+            v.x = pack_bf16x2(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv);
+            v.y = pack_bf16x2(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv);
+            v.z = pack_bf16x2(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv);
+            v.w = pack_bf16x2(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv);
+            *reinterpret_cast<uint4*>(dst + c0 + hh * 8) = v;
+          }
         }
       }
     }
@@ -375,6 +479,10 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+#ifdef EPD_ATTN_TRACE
+  if (ATTN_TRACE_ON)
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) g_attn_trace[i] = s_attn_trace[i];
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -389,10 +497,10 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
   const uint64_t pitch = (uint64_t)DP * 2;
   CUtensorMap mq, mqt, mk, mkt, mv;
   int rc = make_tmap_3d(&mq, p.q, DP, p.Tq, Bq, pitch, pitch * p.Tq, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = make_tmap_3d(&mk, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_3d(&mk, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 64, C::KB, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!rc) rc = make_tmap_3d(&mqt, p.q, DP, p.Tq, Bq, pitch, pitch * p.Tq, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
-  if (!rc) rc = make_tmap_3d(&mkt, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
-  if (!rc) rc = make_tmap_3d(&mv, p.v, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_3d(&mkt, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, C::KB, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_3d(&mv, p.v, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, C::KB, 1, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
@@ -411,6 +519,7 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
 int attention_bf16(const AttnParams& p, cudaStream_t stream) {
   if (p.B <= 0 || p.H <= 0 || p.Tq <= 0 || p.Tk <= 0 || p.Dv <= 0 || p.Dv > p.Dp) return 1001;
   if ((p.ldo % 8) != 0 || (p.Dv % 8) != 0) return 1002;
+  if (p.v_ones_col && p.Dv >= p.Dp) return 1005;
   const bool two = p.Tq > 128;
   switch (p.Dp) {
     case 64: return two ? launch_attn<64, 2>(p, stream) : launch_attn<64, 1>(p, stream);

@@ -221,6 +221,18 @@ epd_status_t epd_encoder_profile_read(epd_encoder_t* enc, double* ms, double* fl
   return cuda_status(enc->impl.prof_read(ms, flops, bytes, launches, nclass), "profile_read");
 }
 
+int32_t epd_encoder_profile_launches(const epd_encoder_t* enc, int32_t* cls, float* ms, double* flops, int32_t cap) {
+  if (!enc) return -1;
+  const auto& v = enc->impl.prof_last;
+  const int32_t n = (int32_t)v.size();
+  for (int32_t i = 0; i < n && i < cap; ++i) {
+    if (cls) cls[i] = v[i].cls;
+    if (ms) ms[i] = v[i].ms;
+    if (flops) flops[i] = v[i].flops;
+  }
+  return n;
+}
+
 // ------------------------------------------------------------------ cache
 
 epd_status_t epd_hash_records(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
@@ -414,14 +426,15 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
 
 epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, void* out, int32_t B, int32_t H,
                                 int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv, int32_t ldo,
-                                int32_t q_shared, float scale, void* stream) {
+                                int32_t flags, float scale, void* stream) {
   epd::AttnParams p;
   p.q = reinterpret_cast<const epd::bf16*>(q);
   p.k = reinterpret_cast<const epd::bf16*>(k);
   p.v = reinterpret_cast<const epd::bf16*>(v);
   p.out = reinterpret_cast<epd::bf16*>(out);
   p.B = B; p.H = H; p.Tq = Tq; p.Tk = Tk; p.Dp = Dp; p.Dv = Dv; p.ldo = ldo;
-  p.q_shared = q_shared;
+  p.q_shared = (flags & EPD_ATTN_Q_SHARED) != 0;
+  p.v_ones_col = (flags & EPD_ATTN_V_ONES_COL) != 0;
   p.scale = scale;
   return cuda_status(epd::attention_bf16(p, S(stream)), "attention_bf16");
 }

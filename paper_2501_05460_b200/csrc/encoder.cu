@@ -78,6 +78,7 @@ std::string Encoder::validate_and_build_schema() {
   Dp = dh <= 64 ? 64 : (dh <= 80 ? 80 : (dh <= 128 ? 128 : 0));
   if (!Dp) return "head_dim > 128 is not supported";
   if (dh % 8) return "head_dim must be a multiple of 8";
+  v_ones = dh < Dp;
   Kreal = x.channels * x.patch_size * x.patch_size;
   Kpad = (Kreal + 63) / 64 * 64;
   F = x.mlp;
@@ -266,6 +267,10 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
       headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.qw, D}, {s.qw, 2 * D}}, H, dh, Dp, D);
       headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.qb, D}, {s.qb, 2 * D}}, H, dh, Dp);
     }
+    // V's first padded head dim becomes a constant 1 (zero weight row, bias 1): the PV
+    // MMA then produces the softmax row sums in O[:, dh] (AttnParams::v_ones_col).
+    if (v_ones)
+      for (int hh = 0; hh < H; ++hh) images.back().v[(size_t)(2 * H + hh) * Dp + dh] = 1.f;
     plain(EPD_L(ow), s.ow);
     plain(EPD_L(ob), s.ob);
     plain(EPD_L(ln2w), s.ln2w);
@@ -636,10 +641,12 @@ int Encoder::prof_read(double* ms, double* flops, double* bytes, int64_t* count,
     cudaError_t e = cudaEventSynchronize(prof_events[prof_recs.back().ev + 1]);
     if (e != cudaSuccess) return (int)e;
   }
+  prof_last.clear();
   for (const auto& r : prof_recs) {
-    if (r.cls < 0 || r.cls >= nclass) continue;
     float t = 0.f;
     cudaEventElapsedTime(&t, prof_events[r.ev], prof_events[r.ev + 1]);
+    prof_last.push_back({r.cls, t, r.flops});
+    if (r.cls < 0 || r.cls >= nclass) continue;
     ms[r.cls] += t;
     flops[r.cls] += r.flops;
     bytes[r.cls] += r.bytes;
@@ -692,6 +699,7 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
       ap.B = nt; ap.H = H; ap.Tq = T; ap.Tk = T; ap.Dp = Dp; ap.Dv = dh;
       ap.ldo = D;
       ap.scale = 1.f / std::sqrt((float)dh);
+      ap.v_ones_col = v_ones;
       EPD_LAUNCH(PROF_ATTN, 4.0 * nt * dT * dT * dD, 0, attention_bf16(ap, s));
     }
     {

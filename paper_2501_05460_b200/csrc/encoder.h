@@ -81,6 +81,13 @@ class Encoder {
   double flops_per_tile() const;
   int64_t numel(int i) const;
   int prof_read(double* ms, double* flops, double* bytes, int64_t* count, int nclass);
+  // Per-launch records of the last drained profile: (class, ms, flops).
+  struct ProfLaunch {
+    int cls;
+    float ms;
+    double flops;
+  };
+  std::vector<ProfLaunch> prof_last;
   bool prof_on = false;
   bool use_graphs = true;
 
@@ -108,6 +115,7 @@ class Encoder {
   // geometry
   int grid = 0, npatch = 0, T = 0, Tpad = 0, D = 0, H = 0, dh = 0, Dp = 0, F = 0;
   int Kreal = 0, Kpad = 0, E = 0, Q = 0, RH = 0, rdh = 0, RDp = 0;
+  bool v_ones = false;  // V carries a ones column at head dim dh (needs dh < Dp)
   // schema indices
   int w_pe = -1, b_pe = -1, w_cls = -1, w_pos = -1, w_post_w = -1, w_post_b = -1;
   int r_query = -1, r_kv = -1, r_lnq_w = -1, r_lnq_b = -1, r_lnkv_w = -1, r_lnkv_b = -1;

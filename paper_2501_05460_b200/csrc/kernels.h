@@ -58,6 +58,10 @@ struct AttnParams {
   int B = 0, H = 0, Tq = 0, Tk = 0, Dp = 0, Dv = 0, ldo = 0;
   int q_shared = 0;
   float scale = 1.f;
+  // Caller guarantees V[..., Dv] == 1 (a zero-padded head dim set to one, Dv < Dp):
+  // the PV MMA then yields the softmax row sums in O[:, Dv] and the softmax warps
+  // skip their per-element sums.
+  int v_ones_col = 0;
 };
 int attention_bf16(const AttnParams& p, cudaStream_t stream);
 

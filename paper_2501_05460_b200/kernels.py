@@ -77,14 +77,18 @@ def linear_heads(a: torch.Tensor, w: torch.Tensor, H: int, Dp: int, T: int, sect
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
-              Dv: int, scale: float, q_shared: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Fused MHA; q [Bq,Tq,Dp], k and v [B*H,Tk,Dp] -> out [B*Tq, H*Dv]."""
+              Dv: int, scale: float, q_shared: bool = False, out: torch.Tensor | None = None,
+              v_ones_col: bool = False) -> torch.Tensor:
+    """Fused MHA; q [Bq,Tq,Dp], k and v [B*H,Tk,Dp] -> out [B*Tq, H*Dv].
+
+    ``v_ones_col``: v[..., Dv] is all ones (Dv < Dp), so the kernel takes the softmax
+    row sums from the PV product."""
     _need_cuda(q, k, v, out)
     Dp = q.shape[-1]
     if out is None:
         out = torch.empty(B * Tq, H * Dv, dtype=torch.bfloat16, device=q.device)
     call("epd_attention_bf16", q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, H, Tq, Tk,
-         Dp, Dv, out.stride(0), int(q_shared), float(scale), _stream(q))
+         Dp, Dv, out.stride(0), int(q_shared) | (2 if v_ones_col else 0), float(scale), _stream(q))
     return out
 
 

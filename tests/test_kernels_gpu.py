@@ -124,6 +124,33 @@ def test_attention(cuda, B, H, Tq, Tk, Dv, Dp, q_shared, qscale):
     assert relerr(y, o) <= TOL
 
 
+@pytest.mark.parametrize("B,H,Tq,Tk,qscale", [(2, 16, 1024, 1024, 1.0), (1, 4, 256, 1000, 6.0), (1, 2, 100, 37, 1.0)])
+def test_attention_row_sums_from_v_ones_column(cuda, B, H, Tq, Tk, qscale):
+    """EPD_ATTN_V_ONES_COL: v[..., Dv] == 1 turns O[:, Dv] into the softmax row sums (SigLIP's
+    72 -> 80 head padding); the result must match the plain softmax, including ragged key
+    blocks and the lazy rescale."""
+    from paper_2501_05460_b200 import kernels
+    Dv, Dp = 72, 80
+    g = torch.Generator(device=cuda).manual_seed(B + H + Tq + Tk)
+    q, k, v = _attn_inputs(B, H, Tq, Tk, Dv, Dp, False, g, qscale)
+    v[..., Dv] = 1.0
+    scale = 1.0 / math.sqrt(Dv)
+    y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, v_ones_col=True)
+    y0 = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale)
+    torch.cuda.synchronize()
+    p = torch.softmax(q[..., :Dv].float() @ k[..., :Dv].float().transpose(1, 2) * scale, dim=-1)
+    o = (p @ v[..., :Dv].float()).reshape(B, H, Tq, Dv).permute(0, 2, 1, 3).reshape(B * Tq, H * Dv)
+    assert relerr(y, o) <= TOL
+    assert relerr(y, y0) <= TOL
+
+
+def test_attention_v_ones_needs_padding(cuda):
+    from paper_2501_05460_b200 import kernels
+    q = torch.zeros(1, 128, 64, dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(ValueError):
+        kernels.attention(q, q, q, 1, 1, 128, 128, 64, 0.125, v_ones_col=True)
+
+
 @pytest.mark.parametrize("rows,D", [(1000, 1152), (64, 3584), (8, 4096), (5, 8)])
 def test_layernorm(cuda, rows, D):
     from paper_2501_05460_b200 import kernels

@@ -55,6 +55,11 @@ def main():
         ms = timeit(lambda: kernels.attention(q, k, v, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out))
         fl = 4 * B * H * Tq * T * Dv
         print(f"attn B={B} H={H} Tq={Tq} Tk={T} Dv={Dv}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s (algorithmic)")
+        if Dv < Dp:
+            v[..., Dv] = 1.0
+            ms = timeit(lambda: kernels.attention(q, k, v, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out,
+                                                  v_ones_col=True))
+            print(f"attn (v ones col) B={B} H={H} Tq={Tq}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
     x = torch.randn(M, 1152, device=dev).to(torch.bfloat16)
     g = torch.ones(1152, device=dev, dtype=torch.bfloat16)
     y = torch.empty_like(x)
