@@ -108,6 +108,19 @@ EPD_DEVICE void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 // Arrive on an mbarrier once all prior tcgen05.mma of this thread complete.
+// One lane of a converged warp (elect.sync). Issue roles run warp-wide with uniform
+// operands and guard each async instruction with this, so the compiler keeps the
+// operands in uniform registers instead of an R2UR + elect loop per instruction.
+EPD_DEVICE bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 EPD_DEVICE void tc_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

@@ -20,6 +20,7 @@ namespace epd {
 namespace {
 
 constexpr int kBM = 128;
+
 constexpr int kBK = 64;
 
 EPD_DEVICE void load8(const bf16* src, float* x) {
@@ -29,6 +30,21 @@ EPD_DEVICE void load8(const bf16* src, float* x) {
   x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
   x[4] = c.x; x[5] = c.y; x[6] = d.x; x[7] = d.y;
 }
+
+// erf via Abramowitz & Stegun 7.1.26 (|abs err| <= 1.5e-7) with MUFU rcp/ex2: ~14
+// instructions against libdevice erff's ~30, which made the GELU-erf epilogue (InternViT
+// fc1) slower than its MMAs.
+EPD_DEVICE float erf_fast(float x) {
+  const float ax = fabsf(x);
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, ax, 1.f)));
+  const float y = t * fmaf(fmaf(fmaf(fmaf(1.061405429f, t, -1.453152027f), t, 1.421413741f), t, -0.284496736f), t,
+                           0.254829592f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(ax * ax * -1.4426950408889634f));
+  return copysignf(fmaf(-y, e, 1.f), x);
+}
+EPD_DEVICE float gelu_erf_fast(float x) { return 0.5f * x * (1.f + erf_fast(x * 0.7071067811865476f)); }
 
 EPD_DEVICE float gelu_tanh_fast(float x) {
   const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
@@ -41,14 +57,10 @@ EPD_DEVICE float gelu_tanh_fast(float x) {
 //   ROWS_BF16 : out bf16 row-major                 (TMA store, 64 B rows, SW64, 32-col chunks)
 //   ROWS_F32  : out fp32 row-major                 (TMA store, 128 B rows, SW128, 32-col chunks)
 //   ACC_F32   : out fp32 += result (residual stream, in place)  (TMA reduce-add, SW128)
-//   HEADS     : per-head Q/K [bh][T][Dp] (SW32) or keys-major V^T [bh][Dp][Tpad] (no swizzle),
-//               16-col chunks, 3-D TMA stores; tiles that straddle two images store twice.
+//   HEADS     : per-head Q/K/V [bh][T][Dp] (SW32) or keys-major V^T [bh][Dp][Tpad] (no swizzle):
+//               each 32-column chunk leaves as two 16-column 3-D TMA boxes; tiles that
+//               straddle two images store from registers.
 enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS = 3 };
-
-template <int KIND>
-struct EpiCfg {
-  static constexpr int CW = KIND == EK_HEADS ? 16 : 32;
-};
 
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
 
@@ -147,7 +159,6 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
                      const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
                      const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep) {
   using Cfg = GemmCfg<BN, CG>;
-  constexpr int CW = EpiCfg<KIND>::CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -193,14 +204,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   const int nk = (K + kBK - 1) / kBK;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = pid; tile < num_tiles; tile += npid) {
-        const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
-        const int n0 = (tile % num_n) * BN + crank * (BN / CG);
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+    // TMA producer: the whole warp walks the schedule (uniform operands), one elected lane issues
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = pid; tile < num_tiles; tile += npid) {
+      const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
+      const int n0 = (tile % num_n) * BN + crank * (BN / CG);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
           if (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
@@ -210,14 +222,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
             tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
           }
-          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && crank == 0) {
+    if (crank == 0) {
+      // MMA issuer: whole warp, elected lane issues (see elect_one)
       constexpr uint32_t idesc_full = make_idesc_bf16(kBM * CG, BN);
       constexpr uint32_t idesc_half = make_idesc_bf16(kBM, BN / 2);
+      const uint64_t a0 = make_sdesc(smem_u32(sA), 1024, 2);
+      const uint64_t b0 = make_sdesc(smem_u32(sB), 1024, 2);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
@@ -233,19 +249,23 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint64_t ao = a0 + (uint64_t)((stage * Cfg::A_BYTES) >> 4);
+          const uint64_t bo = b0 + (uint64_t)((stage * Cfg::B_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t adesc = make_sdesc(a_addr + k * 32, 1024, 2);
-            const uint64_t bdesc = make_sdesc(b_addr + k * 32, 1024, 2);
-            if (CG == 2) umma_bf16_pair(dtmem, adesc, bdesc, idesc, (kb | k) != 0);
-            else umma_bf16(dtmem, adesc, bdesc, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              if (CG == 2) umma_bf16_pair(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
+              else umma_bf16(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
+            }
+            if (CG == 2) tc_commit_pair(&empty[stage]); else tc_commit(&empty[stage]);
           }
-          if (CG == 2) tc_commit_pair(&empty[stage]); else tc_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (CG == 2) tc_commit_pair(&tfull[as]); else tc_commit(&tfull[as]);
+        if (elect_one()) {
+          if (CG == 2) tc_commit_pair(&tfull[as]); else tc_commit(&tfull[as]);
+        }
+        __syncwarp();
       }
     }
   } else {
@@ -264,36 +284,52 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
       const int n0 = (tile % num_n) * BN;
       const int row = m0 + r;
+      // Heads bookkeeping, once per tile-half (no divisions inside the chunk loop):
+      // section / head / head-dim of this half's first column, image and token of m0.
+      int hsec = 0, hh = 0, hd = 0, img0 = 0, tok0 = 0;
+      bool straddle = false;
+      if (KIND == EK_HEADS) {
+        const int nn = n0 + half * (BN / 2);
+        hsec = nn / ep.sec_cols;
+        const int within = nn - hsec * ep.sec_cols;
+        hh = within / ep.Dp;
+        hd = within - hh * ep.Dp;
+        img0 = m0 / ep.T;
+        tok0 = m0 - img0 * ep.T;
+        // a tile that straddles two images (T % 128 != 0) cannot be one TMA box
+        straddle = tok0 + kBM > ep.T;
+      }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += CW) {
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
         const int n = n0 + c;
         if (n >= N) break;  // warp-uniform
-        uint32_t v[32];
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c;
-        if (CW == 32) tmem_ld32(taddr, v); else tmem_ld16(taddr, v);
-        tmem_ld_wait();
-        float x[CW];
+        float x[32];
+        {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < CW; ++j) x[j] = __uint_as_float(v[j]);
+          for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(v[j]);
+        }
 #pragma unroll
-        for (int g = 0; g < CW / 8; ++g) {
+        for (int g = 0; g < 4; ++g) {
           const int col = n + g * 8;
           float* xg = x + g * 8;
           if (col < N) {
             if (ep.bias) {
-              float b[8];
-              load8(ep.bias + col, b);
+              float bb[8];
+              load8(ep.bias + col, bb);
 #pragma unroll
-              for (int j = 0; j < 8; ++j) xg[j] += b[j];
+              for (int j = 0; j < 8; ++j) xg[j] += bb[j];
             }
             if (ep.act == ACT_GELU_TANH) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) xg[j] = gelu_tanh_fast(xg[j]);
             } else if (ep.act == ACT_GELU_ERF) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) xg[j] = gelu_erf(xg[j]);
+              for (int j = 0; j < 8; ++j) xg[j] = gelu_erf_fast(xg[j]);
             }
             if (ep.lscale) {
               float s8[8];
@@ -309,39 +345,45 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
             }
           }
         }
-        if (KIND == EK_HEADS &&
-            ((m0 % ep.T) + kBM > ep.T ||
-             (((m0 % ep.T) & 7) && (n / ep.sec_cols == 0 ? ep.sec_trans[0]
-                                    : (n / ep.sec_cols == 1 ? ep.sec_trans[1] : ep.sec_trans[2]))))) {
-          // Tile straddles an image boundary (T % 128 != 0), or a keys-major V^T chunk would
-          // start at a token offset that is not 16-byte aligned: TMA stores take neither
-          // negative nor unaligned inner coordinates, so store from registers.
-          if (row < M) {
-            const int sec = n / ep.sec_cols;
-            const int within = n - sec * ep.sec_cols;
-            const int h = within / ep.Dp;
-            const int d0 = within - h * ep.Dp;
-            const int b = row / ep.T;
-            const int t = row - b * ep.T;
-            const size_t bh = (size_t)b * ep.H + h;
-            bf16* base = sec == 0 ? ep.sec_out[0] : (sec == 1 ? ep.sec_out[1] : ep.sec_out[2]);
-            const int trans = sec == 0 ? ep.sec_trans[0] : (sec == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
-            if (!trans) {
-              bf16* p = base + (bh * ep.T + t) * ep.Dp + d0;
+        // HEADS: the 32 columns are two 16-wide head-dim pieces (Dp % 16 == 0), each with its
+        // own (section, head, dim) -- advanced incrementally -- and its own 4 KB staging slot.
+        int psec[2] = {0, 0}, ph[2] = {0, 0}, pd[2] = {0, 0};
+        bool pon[2] = {false, false}, pdirect[2] = {false, false};
+        if (KIND == EK_HEADS) {
 #pragma unroll
-              for (int j = 0; j < CW / 8; ++j)
-                *reinterpret_cast<uint4*>(p + 8 * j) =
-                    make_uint4(pack_bf16x2(x[8 * j + 0], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
-                               pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
-            } else {
-              bf16* p = base + (bh * ep.Dp + d0) * ep.Tpad + t;
+          for (int sub = 0; sub < 2; ++sub) {
+            pon[sub] = n + sub * 16 < N;
+            psec[sub] = hsec; ph[sub] = hh; pd[sub] = hd;
+            if ((hd += 16) == ep.Dp) {
+              hd = 0;
+              if (++hh == ep.H) { hh = 0; ++hsec; }
+            }
+            const int trans = psec[sub] == 0 ? ep.sec_trans[0] : (psec[sub] == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
+            // a keys-major V^T piece must start at a 16-byte aligned token offset for TMA
+            pdirect[sub] = straddle || ((tok0 & 7) && trans);
+            if (pon[sub] && pdirect[sub] && row < M) {
+              const int bimg = row / ep.T;
+              const int t = row - bimg * ep.T;
+              const size_t bh = (size_t)bimg * ep.H + ph[sub];
+              bf16* base = psec[sub] == 0 ? ep.sec_out[0] : (psec[sub] == 1 ? ep.sec_out[1] : ep.sec_out[2]);
+              const float* xs = x + sub * 16;
+              if (!trans) {
+                bf16* pp = base + (bh * ep.T + t) * ep.Dp + pd[sub];
 #pragma unroll
-              for (int j = 0; j < CW; ++j) p[(size_t)j * ep.Tpad] = __float2bfloat16_rn(x[j]);
+                for (int j = 0; j < 2; ++j)
+                  *reinterpret_cast<uint4*>(pp + 8 * j) =
+                      make_uint4(pack_bf16x2(xs[8 * j + 0], xs[8 * j + 1]), pack_bf16x2(xs[8 * j + 2], xs[8 * j + 3]),
+                                 pack_bf16x2(xs[8 * j + 4], xs[8 * j + 5]), pack_bf16x2(xs[8 * j + 6], xs[8 * j + 7]));
+              } else {
+                bf16* pp = base + (bh * ep.Dp + pd[sub]) * ep.Tpad + t;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) pp[(size_t)j * ep.Tpad] = __float2bfloat16_rn(xs[j]);
+              }
             }
           }
-          continue;
+          if (!(pon[0] && !pdirect[0]) && !(pon[1] && !pdirect[1])) continue;  // nothing staged
         }
-        // previous TMA store must have finished reading the staging buffer
+        // the previous TMA store(s) must have finished reading the staging buffer
         if (leader) bulk_wait_read0();
         named_bar(bar_id, 128);
         if (KIND == EK_ROWS_BF16) {
@@ -359,23 +401,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
             *reinterpret_cast<float4*>(stg + r * 128 + phys * 16) =
                 make_float4(x[4 * j + 0], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
           }
-        }
-        int sec = 0, trans = 0;
-        if (KIND == EK_HEADS) {
-          sec = n / ep.sec_cols;
-          trans = sec == 0 ? ep.sec_trans[0] : (sec == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
-          if (!trans) {
+        } else {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int phys = j ^ ((r >> 2) & 1);
-              *reinterpret_cast<uint4*>(stg + r * 32 + phys * 16) =
-                  make_uint4(pack_bf16x2(x[8 * j + 0], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
-                             pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
+          for (int sub = 0; sub < 2; ++sub) {
+            if (!pon[sub] || pdirect[sub]) continue;
+            uint8_t* slot = stg + sub * 4096;
+            const float* xs = x + sub * 16;
+            const int trans = psec[sub] == 0 ? ep.sec_trans[0] : (psec[sub] == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
+            if (!trans) {
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int phys = j ^ ((r >> 2) & 1);
+                *reinterpret_cast<uint4*>(slot + r * 32 + phys * 16) =
+                    make_uint4(pack_bf16x2(xs[8 * j + 0], xs[8 * j + 1]), pack_bf16x2(xs[8 * j + 2], xs[8 * j + 3]),
+                               pack_bf16x2(xs[8 * j + 4], xs[8 * j + 5]), pack_bf16x2(xs[8 * j + 6], xs[8 * j + 7]));
+              }
+            } else {
+              bf16* t16 = reinterpret_cast<bf16*>(slot);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) t16[j * 128 + r] = __float2bfloat16_rn(xs[j]);
             }
-          } else {
-            bf16* t16 = reinterpret_cast<bf16*>(stg);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) t16[j * 128 + r] = __float2bfloat16_rn(x[j]);
           }
         }
         fence_proxy_async_smem();
@@ -386,19 +431,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           } else if (KIND == EK_ACC_F32) {
             tma_reduce_add_2d(&tmO0, stg, n, m0);
           } else {
-            auto st3 = [&](int c0, int c1, int c2) {
-              if (sec == 0) tma_store_3d(&tmO0, stg, c0, c1, c2);
-              else if (sec == 1) tma_store_3d(&tmO1, stg, c0, c1, c2);
-              else tma_store_3d(&tmO2, stg, c0, c1, c2);
-            };
-            const int within = n - sec * ep.sec_cols;
-            const int h = within / ep.Dp;
-            const int d0 = within - h * ep.Dp;
-            const int b0 = m0 / ep.T;
-            const int t0 = m0 - b0 * ep.T;
-            const int bh = b0 * ep.H + h;
-            if (!trans) st3(d0, t0, bh);
-            else st3(t0, d0, bh);
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {
+              if (!pon[sub] || pdirect[sub]) continue;
+              uint8_t* slot = stg + sub * 4096;
+              const int trans = psec[sub] == 0 ? ep.sec_trans[0] : (psec[sub] == 1 ? ep.sec_trans[1] : ep.sec_trans[2]);
+              const int bh = img0 * ep.H + ph[sub];
+              const int c0 = trans ? tok0 : pd[sub], c1 = trans ? pd[sub] : tok0;
+              if (psec[sub] == 0) tma_store_3d(&tmO0, slot, c0, c1, bh);
+              else if (psec[sub] == 1) tma_store_3d(&tmO1, slot, c0, c1, bh);
+              else tma_store_3d(&tmO2, slot, c0, c1, bh);
+            }
           }
           bulk_commit();
         }
