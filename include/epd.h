@@ -210,6 +210,10 @@ epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, voi
                                 int32_t ldo, int32_t flags, float scale, void* stream);
 epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
                                 const void* beta, int32_t rows, int32_t D, float eps, void* stream);
+/* Residual-stream LayerNorm: fp32 rows in, bf16 rows out (the encoder's pre-attention /
+ * pre-MLP normalisation of its fp32 residual stream). */
+epd_status_t epd_layernorm_f32_bf16(const float* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
+                                    const void* beta, int32_t rows, int32_t D, float eps, void* stream);
 /* uint8 HWC tiles [n][S][S][C] -> bf16 rows [n*rows_per_tile][Kpad], patch rows start at
  * row_offset within each tile's block; columns in (c, ky, kx) order, zero padded. */
 epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t S, int32_t C, int32_t p, int32_t Kpad,

@@ -84,6 +84,7 @@ _SIGS = {
     "epd_attention_bf16": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
                                   C.c_float, _vp]),
     "epd_layernorm_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _i32, C.c_float, _vp]),
+    "epd_layernorm_f32_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _i32, C.c_float, _vp]),
     "epd_patchify_u8": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }
 

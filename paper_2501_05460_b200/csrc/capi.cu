@@ -448,6 +448,15 @@ epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_
                      "layernorm_bf16");
 }
 
+epd_status_t epd_layernorm_f32_bf16(const float* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
+                                    const void* beta, int32_t rows, int32_t D, float eps, void* stream) {
+  return cuda_status(epd::layernorm_f32in(in, ld_in, reinterpret_cast<epd::bf16*>(out), ld_out,
+                                          reinterpret_cast<const epd::bf16*>(gamma),
+                                          reinterpret_cast<const epd::bf16*>(beta), rows, D, eps, nullptr, 1,
+                                          S(stream)),
+                     "layernorm_f32_bf16");
+}
+
 epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t Sz, int32_t C, int32_t p, int32_t Kpad,
                              int32_t row_offset, int32_t rows_per_tile, const float* mean3, const float* std3,
                              void* out, void* stream) {

@@ -4,6 +4,7 @@
 // packing) and the pixel-shuffle gather used by the InternVL projector.
 #include "common.cuh"
 #include "kernels.h"
+#include "tmap.h"
 
 namespace epd {
 
@@ -102,6 +103,85 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const Tin* __restrict__ 
   }
 }
 
+// Residual-stream LayerNorm (fp32 in, bf16 out, no gather): gamma/beta are staged once
+// per block in shared memory and the grid is one resident wave of warps striding over
+// rows, so no row waits on a dependent gamma/beta load and there is no partial wave.
+// RPW rows per warp are processed together (their loads in flight at once).
+template <int MAXV, int RPW>
+__global__ void __launch_bounds__(256) layernorm_resid_kernel(const float* __restrict__ in, int ld_in,
+                                                              bf16* __restrict__ out, int ld_out,
+                                                              const bf16* __restrict__ gamma,
+                                                              const bf16* __restrict__ beta, int rows, int D,
+                                                              float eps) {
+  extern __shared__ uint4 gb[];  // [2][D/8] gamma then beta, 8 bf16 per uint4
+  const int nvec = D >> 3;
+  for (int i = threadIdx.x; i < nvec; i += blockDim.x) {
+    gb[i] = reinterpret_cast<const uint4*>(gamma)[i];
+    gb[nvec + i] = reinterpret_cast<const uint4*>(beta)[i];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const float inv_d = 1.f / (float)D;
+  for (int row0 = (blockIdx.x * wpb + warp) * RPW; row0 < rows; row0 += gridDim.x * wpb * RPW) {
+    float x[RPW][MAXV][8];
+    float sum[RPW];
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      sum[rr] = 0.f;
+      const int row = row0 + rr;
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        const int v = lane + i * 32;
+        if (v < nvec && row < rows) load_row8<float>(in + (size_t)row * ld_in + v * 8, x[rr][i]);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i)
+        if (lane + i * 32 < nvec)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sum[rr] += x[rr][i][j];
+    float mean[RPW], var[RPW];
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      mean[rr] = warp_sum(sum[rr]) * inv_d;
+      var[rr] = 0.f;
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i)
+        if (lane + i * 32 < nvec)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float t = x[rr][i][j] - mean[rr];
+            var[rr] += t * t;
+          }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      const int row = row0 + rr;
+      const float rstd = rsqrtf(warp_sum(var[rr]) * inv_d + eps);
+      if (row >= rows) continue;
+#pragma unroll
+      for (int i = 0; i < MAXV; ++i) {
+        const int v = lane + i * 32;
+        if (v < nvec) {
+          const uint4 ug = gb[v], ub = gb[nvec + v];
+          const uint32_t gw[4] = {ug.x, ug.y, ug.z, ug.w}, bw[4] = {ub.x, ub.y, ub.z, ub.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 g2 = unpack_bf16x2(gw[j]), b2 = unpack_bf16x2(bw[j]);
+            o[j] = pack_bf16x2((x[rr][i][2 * j] - mean[rr]) * rstd * g2.x + b2.x,
+                               (x[rr][i][2 * j + 1] - mean[rr]) * rstd * g2.y + b2.y);
+          }
+          *reinterpret_cast<uint4*>(out + (size_t)row * ld_out + v * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    }
+  }
+}
+
 // One block per (tile, patch row). Stage p image rows in smem, then emit
 // S/p patches x Kpad columns in (c, ky, kx) order.
 __global__ void patchify_kernel(const uint8_t* __restrict__ tiles, int S, int C, int p, int Kpad,
@@ -177,9 +257,33 @@ int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, cons
   return layernorm_any<bf16>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs, stream);
 }
 
+#ifndef EPD_LN_RPW
+#define EPD_LN_RPW 1
+#endif
+
+template <int MAXV, int RPW>
+int launch_ln_resid(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma, const bf16* beta,
+                    int rows, int D, float eps, cudaStream_t stream) {
+  auto k = layernorm_resid_kernel<MAXV, RPW>;
+  const size_t smem = (size_t)2 * D * 2;
+  static int resident = 0;  // blocks per SM at this register/smem footprint
+  if (!resident) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k, 256, smem);
+    if (resident < 1) resident = 1;
+  }
+  const int need = (rows + 8 * RPW - 1) / (8 * RPW);
+  const int grid = need < resident * num_sms() ? need : resident * num_sms();
+  k<<<grid, 256, smem, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps);
+  return (int)cudaGetLastError();
+}
+
 int layernorm_f32in(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
                     const bf16* beta, int rows, int D, float eps, const int32_t* gidx, int segs,
                     cudaStream_t stream) {
+#if EPD_LN_RPW > 0
+  if (!gidx && D % 8 == 0 && ld_in % 4 == 0 && ld_out % 8 == 0 && rows > 0 && D / 8 <= 32 * 5)
+    return launch_ln_resid<5, EPD_LN_RPW>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, stream);
+#endif
   return layernorm_any<float>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs, stream);
 }
 

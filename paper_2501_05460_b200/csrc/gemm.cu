@@ -572,7 +572,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
       if (cost < best) { best = cost; bn = c; }
     }
   }
+#ifndef EPD_CG2_BN128
   if (cg == 2 && bn == 128) cg = 1;
+#endif
   int kind;
   if (ep.mode == EPI_HEADS) {
     if (ep.Dp % 16 || ep.sec_cols % ep.Dp || ep.T <= 0) return 1005;
@@ -592,6 +594,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
     switch (bn) {
       case 256: return launch_kind<256, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
       case 192: return launch_kind<192, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+#ifdef EPD_CG2_BN128
+      case 128: return launch_kind<128, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+#endif
       default: return 1004;
     }
   }

@@ -103,6 +103,20 @@ def layernorm(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: flo
     return out
 
 
+def layernorm_f32(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps: float,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 rows -> LayerNorm -> bf16 rows (the residual-stream normalisation)."""
+    _need_cuda(x, gamma, beta, out)
+    if x.dtype != torch.float32:
+        raise ValueError("layernorm_f32 takes fp32 rows")
+    rows, D = x.shape
+    if out is None:
+        out = torch.empty(rows, D, dtype=torch.bfloat16, device=x.device)
+    call("epd_layernorm_f32_bf16", x.data_ptr(), x.stride(0), out.data_ptr(), out.stride(0), gamma.data_ptr(),
+         beta.data_ptr(), rows, D, float(eps), _stream(x))
+    return out
+
+
 def patchify(tiles: torch.Tensor, patch: int, kpad: int, mean, std, row_offset: int = 0,
              rows_per_tile: int | None = None) -> torch.Tensor:
     """uint8 [n,S,S,C] -> bf16 [n*rows_per_tile, kpad] normalised im2col rows."""

@@ -164,6 +164,19 @@ def test_layernorm(cuda, rows, D):
     assert relerr(y, ref) <= TOL
 
 
+@pytest.mark.parametrize("rows,D", [(10240, 1152), (12300, 1024), (7, 4096), (3, 8)])
+def test_layernorm_f32_input(cuda, rows, D):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(rows * 3 + D)
+    x = torch.randn(rows, D, device=cuda, generator=g) * 4.0 + 2.5
+    gm = _bf(D, gen=g)
+    bt = _bf(D, gen=g)
+    y = kernels.layernorm_f32(x, gm, bt, 1e-6)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.layer_norm(x, (D,), gm.float(), bt.float(), 1e-6)
+    assert relerr(y, ref) <= TOL
+
+
 def test_patchify(cuda):
     from paper_2501_05460_b200 import kernels
     g = torch.Generator(device=cuda).manual_seed(3)

@@ -23,6 +23,8 @@ def timeit(fn, iters=30, warm=5):
 
 
 tag = Path(os.environ.get("EPD_LIB_PATH", "libepd.so")).stem
+BN = int(os.environ.get("BN", "0"))
+tag += f"/bn{BN}"
 dev = torch.device("cuda")
 M = 10240
 line = []
@@ -34,10 +36,10 @@ for (N, K, act, name, acc) in [(3840, 1152, "none", "qkv", False), (1152, 1152, 
     b = torch.randn(N, device=dev).to(torch.bfloat16)
     if acc:
         h = torch.zeros(M, N, device=dev)
-        ms = timeit(lambda: kernels.linear_acc(a, w, h, bias=b))
+        ms = timeit(lambda: kernels.linear_acc(a, w, h, bias=b, bn=BN))
     else:
         out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-        ms = timeit(lambda: kernels.linear(a, w, bias=b, act=act, out=out))
+        ms = timeit(lambda: kernels.linear(a, w, bias=b, act=act, out=out, bn=BN))
     line.append(f"{name} {ms * 1e3:6.1f}us {2 * M * N * K / ms / 1e9:6.0f}TF")
 # QKV in heads mode (SigLIP: H=16, Dp=80, T=1024), natural layouts for all sections
 from paper_2501_05460_b200._lib import call  # noqa: E402

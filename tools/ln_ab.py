@@ -1,0 +1,29 @@
+"""Residual-stream LayerNorm timing (fp32 in, bf16 out) for A/B runs (library from EPD_LIB_PATH)."""
+import os
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2501_05460_b200 import kernels  # noqa: E402
+
+tag = Path(os.environ.get("EPD_LIB_PATH", "libepd.so")).stem
+dev = torch.device("cuda")
+res = []
+for rows, D in [(10240, 1152), (12300, 1024)]:
+    x = torch.randn(rows, D, device=dev)
+    g = torch.ones(D, device=dev, dtype=torch.bfloat16)
+    y = torch.empty(rows, D, device=dev, dtype=torch.bfloat16)
+    for _ in range(5):
+        kernels.layernorm_f32(x, g, g, 1e-6, out=y)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(50):
+        kernels.layernorm_f32(x, g, g, 1e-6, out=y)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / 50
+    res.append(f"{rows}x{D}: {ms * 1e3:6.1f} us {rows * D * 6 / ms / 1e6:6.0f} GB/s")
+print(f"{tag:6s} " + " | ".join(res))
