@@ -25,6 +25,7 @@
 // (LBO = 2 KB between atoms, SBO = 256 B between 8-key groups).
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.h"
 #include "tmap.h"
 
 #ifdef EPD_ATTN_TRACE
@@ -234,6 +235,8 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  pdl_trigger();
+  pdl_wait();  // Q, K, V come from the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -510,8 +513,8 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
     attr_set = true;
   }
   dim3 grid((p.Tq + NQ * 128 - 1) / (NQ * 128), p.H, p.B);
-  attention_kernel<DP, NQ><<<grid, C::THREADS, C::SMEM, stream>>>(mq, mqt, mk, mkt, mv, p);
-  return (int)cudaGetLastError();
+  return launch_kernel(attention_kernel<DP, NQ>, grid, dim3(C::THREADS), C::SMEM, stream, 1, mq, mqt, mk, mkt, mv,
+                       p);
 }
 
 }  // namespace

@@ -108,6 +108,11 @@ EPD_DEVICE void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 // Arrive on an mbarrier once all prior tcgen05.mma of this thread complete.
+// Programmatic dependent launch (see launch.h): wait for the previous kernel in the
+// stream to complete (a no-op without PDL), and allow the next one to be scheduled.
+EPD_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+EPD_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // One lane of a converged warp (elect.sync). Issue roles run warp-wide with uniform
 // operands and guard each async instruction with this, so the compiler keeps the
 // operands in uniform registers instead of an R2UR + elect loop per instruction.

@@ -4,6 +4,7 @@
 // packing) and the pixel-shuffle gather used by the InternVL projector.
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.h"
 #include "tmap.h"
 
 namespace epd {
@@ -37,6 +38,8 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const Tin* __restrict__ 
                                                         const bf16* __restrict__ beta, int rows,
                                                         int D, float eps,
                                                         const int32_t* __restrict__ gidx, int segs) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + warp;
   if (row >= rows) return;
@@ -119,6 +122,8 @@ __global__ void __launch_bounds__(256) layernorm_resid_kernel(const float* __res
     gb[i] = reinterpret_cast<const uint4*>(gamma)[i];
     gb[nvec + i] = reinterpret_cast<const uint4*>(beta)[i];
   }
+  pdl_trigger();
+  pdl_wait();  // gamma/beta are weights; the rows come from the previous kernel
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
@@ -188,6 +193,8 @@ __global__ void patchify_kernel(const uint8_t* __restrict__ tiles, int S, int C,
                                 int row_offset, int rows_per_tile, float m0, float m1, float m2,
                                 float s0, float s1, float s2, bf16* __restrict__ out) {
   extern __shared__ uint8_t strip[];  // p * S * C bytes
+  pdl_trigger();
+  pdl_wait();
   const int tile = blockIdx.y;
   const int py = blockIdx.x;
   const int np = S / p;
@@ -243,12 +250,12 @@ int layernorm_any(const Tin* in, int ld_in, bf16* out, int ld_out, const bf16* g
   const dim3 block(256);
   const dim3 grid((rows + 7) / 8);
   if (nvec <= 32 * 5)
-    layernorm_kernel<5, Tin><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
+    return launch_kernel(layernorm_kernel<5, Tin>, grid, block, 0, stream, 1, in, ld_in, out, ld_out, gamma, beta, rows,
+                         D, eps, gidx, segs);
   else if (nvec <= 32 * 16)
-    layernorm_kernel<16, Tin><<<grid, block, 0, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps, gidx, segs);
-  else
-    return 1004;
-  return (int)cudaGetLastError();
+    return launch_kernel(layernorm_kernel<16, Tin>, grid, block, 0, stream, 1, in, ld_in, out, ld_out, gamma, beta,
+                         rows, D, eps, gidx, segs);
+  return 1004;
 }
 
 int layernorm_bf16_gather(const bf16* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
@@ -273,8 +280,7 @@ int launch_ln_resid(const float* in, int ld_in, bf16* out, int ld_out, const bf1
   }
   const int need = (rows + 8 * RPW - 1) / (8 * RPW);
   const int grid = need < resident * num_sms() ? need : resident * num_sms();
-  k<<<grid, 256, smem, stream>>>(in, ld_in, out, ld_out, gamma, beta, rows, D, eps);
-  return (int)cudaGetLastError();
+  return launch_kernel(k, dim3(grid), dim3(256), smem, stream, 1, in, ld_in, out, ld_out, gamma, beta, rows, D, eps);
 }
 
 int layernorm_f32in(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma,
@@ -299,11 +305,9 @@ int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int 
   if (S % p || C > 3 || Kpad < C * p * p) return 1002;
   const size_t smem = (size_t)p * S * C;
   dim3 grid(S / p, n);
-  patchify_kernel<<<grid, 256, smem, stream>>>(tiles, S, C, p, Kpad, row_offset, rows_per_tile,
-                                               mean[0], C > 1 ? mean[1] : 0.f, C > 2 ? mean[2] : 0.f,
-                                               stdv[0], C > 1 ? stdv[1] : 1.f, C > 2 ? stdv[2] : 1.f,
-                                               out);
-  return (int)cudaGetLastError();
+  return launch_kernel(patchify_kernel, grid, dim3(256), smem, stream, 1, tiles, S, C, p, Kpad, row_offset,
+                       rows_per_tile, mean[0], C > 1 ? mean[1] : 0.f, C > 2 ? mean[2] : 0.f, stdv[0],
+                       C > 1 ? stdv[1] : 1.f, C > 2 ? stdv[2] : 1.f, out);
 }
 
 int gather_records(const void* src_base, const int32_t* index, int n, size_t bytes, void* dst,

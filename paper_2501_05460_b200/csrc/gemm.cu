@@ -13,6 +13,7 @@
 // The epilogue of tile i overlaps the MMAs of tile i+1 (two TMEM accumulators).
 #include "common.cuh"
 #include "kernels.h"
+#include "launch.h"
 #include "tmap.h"
 
 namespace epd {
@@ -197,6 +198,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   if (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();
+  pdl_wait();  // A, the residual stream and the outputs belong to the previous kernels
 
   const int num_m = (M + kBM * CG - 1) / (kBM * CG);
   const int num_n = (N + BN - 1) / BN;
@@ -511,24 +514,9 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   const int tiles = ((M + kBM * CG - 1) / (kBM * CG)) * ((N + BN - 1) / BN);
   int units = num_sms() / CG;
   if (tiles < units) units = tiles;
-  if (CG == 1) {
-    gemm_bf16_kernel<BN, KIND, 1><<<units, Cfg::THREADS, Cfg::SMEM, stream>>>(ta, tb, t0, t1, t2, M, N, K, ep);
-  } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(units * CG);
-    cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN, KIND, CG>, ta, tb, t0, t1, t2, M, N, K, ep);
-    if (e != cudaSuccess) return (int)e;
-  }
+  const int rc2 = launch_kernel(gemm_bf16_kernel<BN, KIND, CG>, dim3(units * CG), dim3(Cfg::THREADS), Cfg::SMEM,
+                                stream, CG, ta, tb, t0, t1, t2, M, N, K, ep);
+  if (rc2) return rc2;
   return (int)cudaGetLastError();
 }
 
