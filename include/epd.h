@@ -200,14 +200,16 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
 /* O = softmax(Q K^T * scale) V per (batch, head); see csrc/kernels.h AttnParams.
  * q: [q_shared ? H : B*H][Tq][Dp], k and v: [B*H][Tk][Dp],
  * out[(b*Tq + i)*ldo + h*Dv + d]. Dp in {64, 80, 128}. */
-/* flags: EPD_ATTN_Q_SHARED (q is [H][Tq][Dp], shared by every batch entry);
- * EPD_ATTN_V_ONES_COL (caller guarantees v[..., Dv] == 1 with Dv < Dp: the row
- * sums come out of the PV MMA instead of the softmax warps). */
+/* Fused multi-head attention read in place from row-major projection outputs:
+ *   Q: q[(b*Tq + t)*ldq + h*head_stride + d]  (EPD_ATTN_Q_SHARED: q[t*ldq + h*head_stride + d],
+ *      one query set shared by every batch entry), K and V likewise with ldk / ldv and Tk,
+ *   out[(b*Tq + t)*ldo + h*Dv + d], d < Dv.
+ * Dp (64, 80 or 128) is the MMA width, Dv rounded up to 16; head_stride >= Dv. */
 #define EPD_ATTN_Q_SHARED 1
-#define EPD_ATTN_V_ONES_COL 2
-epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, void* out, int32_t B,
-                                int32_t H, int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv,
-                                int32_t ldo, int32_t flags, float scale, void* stream);
+epd_status_t epd_attention_bf16(const void* q, int32_t ldq, const void* k, int32_t ldk, const void* v,
+                                int32_t ldv, void* out, int32_t ldo, int32_t B, int32_t H, int32_t Tq,
+                                int32_t Tk, int32_t Dp, int32_t Dv, int32_t head_stride, int32_t flags,
+                                float scale, void* stream);
 epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
                                 const void* beta, int32_t rows, int32_t D, float eps, void* stream);
 /* Residual-stream LayerNorm: fp32 rows in, bf16 rows out (the encoder's pre-attention /

@@ -81,8 +81,8 @@ _SIGS = {
     "epd_linear_acc_f32": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
     "epd_linear_heads_bf16": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _i32, _i32,
                                      _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
-    "epd_attention_bf16": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
-                                  C.c_float, _vp]),
+    "epd_attention_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                  _i32, _i32, C.c_float, _vp]),
     "epd_layernorm_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _i32, C.c_float, _vp]),
     "epd_layernorm_f32_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _i32, C.c_float, _vp]),
     "epd_patchify_u8": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),

@@ -14,15 +14,15 @@
 // 4 x 64 columns of S, then O_g and Q_g in a 128-column slot each.
 // The softmax is MUFU-bound: a quarter of the exponentials run as a cubic on the
 // FMA pipe. The running max m_g is only raised (and O_g rescaled, after waiting
-// for the in-flight PV) when a row max grows by more than 2^8. With a ones column
-// in V's head padding (v_ones_col) the PV MMA also produces the row sums.
+// for the in-flight PV) when a row max grows by more than 2^8.
 //
 // Warps: 0 TMA (lane 0: Q, K; lane 1: V), 1 MMA issue (whole warp, elected lane),
 // 2..5 softmax tile 0, 6..9 tile 1.
-// Layouts: Q, K, V all [bh][T][Dp] bf16 (Dp = head dim zero-padded to a multiple
-// of 16). Q/K are K-major smem operands (64-wide SW128 atoms + a 16-wide SW32 tail
-// when Dp % 64 != 0); V is the MN-major B operand from 16-wide SW32 atoms
-// (LBO = 2 KB between atoms, SBO = 256 B between 8-key groups).
+// Layouts: Q, K, V are read in place from the row-major projection outputs through
+// 2-D tensor maps (head h = columns [h*hs, h*hs + Dp) of the section; see AttnParams).
+// Q/K are K-major smem operands (64-wide SW128 atoms + a 16-wide SW32 tail when
+// Dp % 64 != 0); V is the MN-major B operand from 16-wide SW32 atoms (LBO = 2 KB
+// between atoms, SBO = 256 B between 8-key groups).
 #include "common.cuh"
 #include "kernels.h"
 #include "launch.h"
@@ -81,17 +81,7 @@ EPD_DEVICE float fmax3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(m) : "f"(a), "f"(b), "f"(c));  // FMNMX3
   return m;
 }
-EPD_DEVICE uint32_t tmem_ld1(uint32_t taddr) {
-  uint32_t r;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
-  return r;
-}
 
-EPD_DEVICE void tmem_ld8(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
 EPD_DEVICE void tmem_st8(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
@@ -108,7 +98,6 @@ EPD_DEVICE void tmem_st32(uint32_t taddr, const uint32_t* r) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
-EPD_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 EPD_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // Warp-wide issue helpers: every lane executes the call with identical (warp-uniform)
@@ -132,15 +121,6 @@ EPD_DEVICE void tc_commit_warp(uint64_t* bar) {
       : "memory");
 }
 
-// D[tmem] (+)= A[tmem] * B[smem]^T (A operand from tensor memory).
-EPD_DEVICE void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 
 template <int DP, int NQ>
 struct Cfg {
@@ -202,8 +182,9 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   const int lane = lane_id();
   const int h = blockIdx.y;
   const int b = blockIdx.z;
-  const int bh = b * p.H + h;
-  const int qbatch = p.q_shared ? h : bh;
+  const int hcol = h * p.hs;                             // head h's first column
+  const int qrow0 = p.q_shared ? 0 : b * p.Tq;            // image b's first query row
+  const int krow0 = b * p.Tk;                             // and first key row
   const int q0 = blockIdx.x * (NQ * 128);
   const int rem = p.Tq - q0;
   const int nq = rem > 128 ? NQ : 1;  // query tiles with at least one valid row
@@ -243,16 +224,17 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       mbar_arrive_expect_tx(q_full, nq * 128 * DP * 2);
       for (int g = 0; g < nq; ++g) {
         uint8_t* qd = smem + C::OFF_Q + g * C::Q_AL;
-        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(qd + a * C::Q_ATOM, &tmQ, q_full, a * 64, q0 + g * 128, qbatch);
-        if (C::TAIL) tma_load_3d(qd + C::MAIN * C::Q_ATOM, &tmQt, q_full, C::MAIN * 64, q0 + g * 128, qbatch);
+        const int qr = qrow0 + q0 + g * 128;
+        for (int a = 0; a < C::MAIN; ++a) tma_load_2d(qd + a * C::Q_ATOM, &tmQ, q_full, hcol + a * 64, qr);
+        if (C::TAIL) tma_load_2d(qd + C::MAIN * C::Q_ATOM, &tmQt, q_full, hcol + C::MAIN * 64, qr);
       }
       for (int j = 0; j < nkb; ++j) {
         const int s = j % C::KS;
         mbar_wait(&k_empty[s], ((j / C::KS) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[s], C::K_BYTES);
         uint8_t* kd = smem + C::OFF_K + s * C::K_AL;
-        for (int a = 0; a < C::MAIN; ++a) tma_load_3d(kd + a * C::K_ATOM, &tmK, &k_full[s], a * 64, j * C::KB, bh);
-        if (C::TAIL) tma_load_3d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], C::MAIN * 64, j * C::KB, bh);
+        for (int a = 0; a < C::MAIN; ++a) tma_load_2d(kd + a * C::K_ATOM, &tmK, &k_full[s], hcol + a * 64, krow0 + j * C::KB);
+        if (C::TAIL) tma_load_2d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], hcol + C::MAIN * 64, krow0 + j * C::KB);
       }
     } else if (lane == 1) {
       for (int j = 0; j < nkb; ++j) {
@@ -260,7 +242,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         mbar_wait(&v_empty[s], ((j / C::KVS) & 1) ^ 1);
         mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
         uint8_t* vd = smem + C::OFF_V + s * C::V_AL;
-        for (int a = 0; a < DP / 16; ++a) tma_load_3d(vd + a * C::V_ATOM, &tmV, &v_full[s], a * 16, j * C::KB, bh);
+        for (int a = 0; a < DP / 16; ++a) tma_load_2d(vd + a * C::V_ATOM, &tmV, &v_full[s], hcol + a * 16, krow0 + j * C::KB);
       }
     }
   } else if (warp == 1) {
@@ -340,7 +322,6 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     const uint32_t o_tm = tmem + lane_off + C::o_col(g);
     const float c = p.scale * 1.4426950408889634f;
-    const bool ones_col = p.v_ones_col != 0;
     if (g < nq) {
       {
         // copy this thread's Q row (K-major swizzled smem) into TMEM as bf16 pairs:
@@ -351,8 +332,9 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
 #pragma unroll
         for (int c8 = 0; c8 < DP / 8; ++c8) {
           const int d = c8 * 8;
-          uint4 u;
-          if (d < C::MAIN * 64) {
+          uint4 u = make_uint4(0u, 0u, 0u, 0u);  // dims >= Dv (the neighbouring head's columns) -> 0
+          if (d >= p.Dv) {
+          } else if (d < C::MAIN * 64) {
             const int atom = d >> 6, ch = (d & 63) >> 3;
             u = *reinterpret_cast<const uint4*>(qs + atom * C::Q_ATOM + r * 128 + ((ch ^ (r & 7)) * 16));
           } else {
@@ -435,27 +417,20 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
           const float a0 = fmaf(__uint_as_float(sv[i]), c, nm), a1 = fmaf(__uint_as_float(sv[i + 1]), c, nm);
           const float e0 = poly ? ex2_poly(a0) : ex2(a0);
           const float e1 = poly ? ex2_poly(a1) : ex2(a1);
-          if (!ones_col) {
-            rs0 += e0;
-            rs1 += e1;
-          }
+          rs0 += e0;
+          rs1 += e1;
           pk[i >> 1] = pack_bf16x2(e0, e1);
         }
         if (tr) ATTN_TRACE(14, j, g);
         tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
         tmem_st_wait();
-        if (!ones_col) l += rs0 + rs1;
+        l += rs0 + rs1;
         tc_fence_before();
         mbar_arrive(&p_ready[2 * g + (j & 1)]);
         if (tr) ATTN_TRACE(15, j, g);
       }
       mbar_wait(&o_done[g], 0);
       tc_fence_after();
-      if (ones_col) {
-        // O[:, Dv] = sum_k P[k] * 1: the row sum of the (bf16) P the MMA actually used
-        l = __uint_as_float(tmem_ld1(o_tm + p.Dv));
-        tmem_ld_wait();
-      }
       const int qrow = q0 + g * 128 + r;
       const float inv = 1.f / l;
       bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv;
@@ -495,15 +470,17 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
 template <int DP, int NQ>
 int launch_attn(const AttnParams& p, cudaStream_t stream) {
   using C = Cfg<DP, NQ>;
-  const uint64_t Bq = p.q_shared ? p.H : (uint64_t)p.B * p.H;
-  const uint64_t Bk = (uint64_t)p.B * p.H;
-  const uint64_t pitch = (uint64_t)DP * 2;
+  // 2-D maps over each section (H heads x hs columns); rows = tokens of all images. Boxes
+  // that run past the last head or the last row are zero-filled by the TMA.
+  const uint64_t width = (uint64_t)p.H * p.hs;
+  const uint64_t qrows = p.q_shared ? p.Tq : (uint64_t)p.B * p.Tq;
+  const uint64_t krows = (uint64_t)p.B * p.Tk;
   CUtensorMap mq, mqt, mk, mkt, mv;
-  int rc = make_tmap_3d(&mq, p.q, DP, p.Tq, Bq, pitch, pitch * p.Tq, 64, 128, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = make_tmap_3d(&mk, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 64, C::KB, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = make_tmap_3d(&mqt, p.q, DP, p.Tq, Bq, pitch, pitch * p.Tq, 16, 128, 1, CU_TENSOR_MAP_SWIZZLE_32B);
-  if (!rc) rc = make_tmap_3d(&mkt, p.k, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, C::KB, 1, CU_TENSOR_MAP_SWIZZLE_32B);
-  if (!rc) rc = make_tmap_3d(&mv, p.v, DP, p.Tk, Bk, pitch, pitch * p.Tk, 16, C::KB, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  int rc = make_tmap_2d(&mq, p.q, width, qrows, (uint64_t)p.ldq * 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_2d(&mqt, p.q, width, qrows, (uint64_t)p.ldq * 2, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_2d(&mk, p.k, width, krows, (uint64_t)p.ldk * 2, 64, C::KB, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_2d(&mkt, p.k, width, krows, (uint64_t)p.ldk * 2, 16, C::KB, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_2d(&mv, p.v, width, krows, (uint64_t)p.ldv * 2, 16, C::KB, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
@@ -522,7 +499,9 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
 int attention_bf16(const AttnParams& p, cudaStream_t stream) {
   if (p.B <= 0 || p.H <= 0 || p.Tq <= 0 || p.Tk <= 0 || p.Dv <= 0 || p.Dv > p.Dp) return 1001;
   if ((p.ldo % 8) != 0 || (p.Dv % 8) != 0) return 1002;
-  if (p.v_ones_col && p.Dv >= p.Dp) return 1005;
+  if (p.hs < p.Dv || p.ldq % 8 || p.ldk % 8 || p.ldv % 8 || p.hs % 8) return 1002;
+  if ((reinterpret_cast<uintptr_t>(p.q) | reinterpret_cast<uintptr_t>(p.k) | reinterpret_cast<uintptr_t>(p.v)) & 15)
+    return 1003;
   const bool two = p.Tq > 128;
   switch (p.Dp) {
     case 64: return two ? launch_attn<64, 2>(p, stream) : launch_attn<64, 1>(p, stream);

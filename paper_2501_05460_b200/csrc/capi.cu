@@ -424,17 +424,18 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
   return cuda_status(rc, "linear_heads_bf16");
 }
 
-epd_status_t epd_attention_bf16(const void* q, const void* k, const void* v, void* out, int32_t B, int32_t H,
-                                int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv, int32_t ldo,
-                                int32_t flags, float scale, void* stream) {
+epd_status_t epd_attention_bf16(const void* q, int32_t ldq, const void* k, int32_t ldk, const void* v,
+                                int32_t ldv, void* out, int32_t ldo, int32_t B, int32_t H, int32_t Tq,
+                                int32_t Tk, int32_t Dp, int32_t Dv, int32_t head_stride, int32_t flags,
+                                float scale, void* stream) {
   epd::AttnParams p;
   p.q = reinterpret_cast<const epd::bf16*>(q);
   p.k = reinterpret_cast<const epd::bf16*>(k);
   p.v = reinterpret_cast<const epd::bf16*>(v);
   p.out = reinterpret_cast<epd::bf16*>(out);
+  p.ldq = ldq; p.ldk = ldk; p.ldv = ldv; p.hs = head_stride;
   p.B = B; p.H = H; p.Tq = Tq; p.Tk = Tk; p.Dp = Dp; p.Dv = Dv; p.ldo = ldo;
   p.q_shared = (flags & EPD_ATTN_Q_SHARED) != 0;
-  p.v_ones_col = (flags & EPD_ATTN_V_ONES_COL) != 0;
   p.scale = scale;
   return cuda_status(epd::attention_bf16(p, S(stream)), "attention_bf16");
 }

@@ -62,7 +62,8 @@ __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__
       } else {
         const int s = col / ep.sec_cols;
         const int within = col - s * ep.sec_cols;
-        const int h = within / ep.Dp, d = within - h * ep.Dp;
+        const int hw = ep.dh ? ep.dh : ep.Dp;
+        const int h = within / hw, d = within - h * hw;
         const int b = row / ep.T, t = row - b * ep.T;
         ep.sec_out[s][(((size_t)b * ep.H + h) * ep.T + t) * ep.Dp + d] = x;
       }

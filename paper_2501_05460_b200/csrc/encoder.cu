@@ -78,7 +78,6 @@ std::string Encoder::validate_and_build_schema() {
   Dp = dh <= 64 ? 64 : (dh <= 80 ? 80 : (dh <= 128 ? 128 : 0));
   if (!Dp) return "head_dim > 128 is not supported";
   if (dh % 8) return "head_dim must be a multiple of 8";
-  v_ones = dh < Dp;
   Kreal = x.channels * x.patch_size * x.patch_size;
   Kpad = (Kreal + 63) / 64 * 64;
   F = x.mlp;
@@ -260,17 +259,15 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
     auto& o32 = dl32[l];
     plain(EPD_L(ln1w), s.ln1w);
     plain(EPD_L(ln1b), s.ln1b);
+    // Fused QKV [3*H*dh, D] with packed heads: the projection computes no padding and
+    // writes row-major [M][3*H*dh]; attention reads its heads in place.
     if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
-      headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.kw, 0}, {s.vw, 0}}, H, dh, Dp, D);
-      headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.kb, 0}, {s.vb, 0}}, H, dh, Dp);
+      headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.kw, 0}, {s.vw, 0}}, H, dh, dh, D);
+      headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.kb, 0}, {s.vb, 0}}, H, dh, dh);
     } else {
-      headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.qw, D}, {s.qw, 2 * D}}, H, dh, Dp, D);
-      headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.qb, D}, {s.qb, 2 * D}}, H, dh, Dp);
+      headpad_w(EPD_L(qkv), {{s.qw, 0}, {s.qw, D}, {s.qw, 2 * D}}, H, dh, dh, D);
+      headpad_b(EPD_L(qkvb), {{s.qb, 0}, {s.qb, D}, {s.qb, 2 * D}}, H, dh, dh);
     }
-    // V's first padded head dim becomes a constant 1 (zero weight row, bias 1): the PV
-    // MMA then produces the softmax row sums in O[:, dh] (AttnParams::v_ones_col).
-    if (v_ones)
-      for (int hh = 0; hh < H; ++hh) images.back().v[(size_t)(2 * H + hh) * Dp + dh] = 1.f;
     plain(EPD_L(ow), s.ow);
     plain(EPD_L(ob), s.ob);
     plain(EPD_L(ln2w), s.ln2w);
@@ -402,19 +399,16 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   const size_t o_h = plan(M * D * 4);
   const size_t o_xn = plan(M * D * 2);
   const size_t o_ao = plan(M * D * 2);
-  const size_t o_q = plan(nt * H * T * Dp * 2);
-  const size_t o_k = plan(nt * H * T * Dp * 2);
-  const size_t o_vt = plan(nt * H * T * Dp * 2);
+  const size_t o_qkv = plan(M * 3 * (size_t)H * dh * 2);
   size_t big = M * F * 2;
-  size_t o_r1 = 0, o_r2 = 0, o_rk = 0, o_rvt = 0, o_rao = 0, o_rr = 0;
+  size_t o_r1 = 0, o_r2 = 0, o_rkv = 0, o_rao = 0, o_rr = 0;
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
     big = std::max(big, M * (size_t)E * 2);
   }
   const size_t o_f = plan(big);
   if (d.family == EPD_FAMILY_SIGLIP_RESAMPLER) {
     o_r2 = plan(M * (size_t)E * 2);  // ln_kv output
-    o_rk = plan(nt * RH * T * RDp * 2);
-    o_rvt = plan(nt * RH * T * RDp * 2);
+    o_rkv = plan(M * 2 * (size_t)RH * RDp * 2);
     o_rao = plan(nt * Q * (size_t)E * 2);
     o_rr = plan(nt * Q * (size_t)E * 2);
     o_r1 = o_f;  // kv_proj output reuses the MLP buffer
@@ -436,14 +430,11 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
   ws.h = reinterpret_cast<float*>(wb + o_h);
   ws.xn = reinterpret_cast<bf16*>(wb + o_xn);
   ws.ao = reinterpret_cast<bf16*>(wb + o_ao);
-  ws.q = reinterpret_cast<bf16*>(wb + o_q);
-  ws.k = reinterpret_cast<bf16*>(wb + o_k);
-  ws.vt = reinterpret_cast<bf16*>(wb + o_vt);
+  ws.qkv = reinterpret_cast<bf16*>(wb + o_qkv);
   ws.f = reinterpret_cast<bf16*>(wb + o_f);
   ws.r1 = reinterpret_cast<bf16*>(wb + o_r1);
   ws.r2 = reinterpret_cast<bf16*>(wb + o_r2);
-  ws.rk = reinterpret_cast<bf16*>(wb + o_rk);
-  ws.rvt = reinterpret_cast<bf16*>(wb + o_rvt);
+  ws.rkv = reinterpret_cast<bf16*>(wb + o_rkv);
   ws.rao = reinterpret_cast<bf16*>(wb + o_rao);
   ws.rr = reinterpret_cast<bf16*>(wb + o_rr);
   // Padded head dims / key padding are read by the attention TMA and must be finite.
@@ -456,11 +447,11 @@ int Encoder::finalize(cudaStream_t stream, std::string& err) {
     bf16* qn = ws.f;
     rc = layernorm_bf16(rs.query, E, qn, E, rs.lnq_w, rs.lnq_b, Q, E, 1e-6f, stream);
     if (!rc) {
+      // resampler queries, row-major [Q][RH*RDp] (attention reads them as shared queries)
       EpiParams ep;
-      ep.mode = EPI_HEADS;
       ep.bias = rs.qb;
-      ep.H = RH; ep.Dp = RDp; ep.T = Q; ep.Tpad = Q; ep.sec_cols = RH * RDp;
-      ep.sec_out[0] = dw.r_qheads;
+      ep.out = dw.r_qheads;
+      ep.ldo = RH * RDp;
       rc = gemm_bf16(qn, E, rs.qw, E, Q, RH * RDp, E, ep, stream);
     }
     if (!rc) {
@@ -686,20 +677,18 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     EPD_LAUNCH(PROF_LN, 0, ln_bytes_f32, layernorm_f32in(ws.h, D, ws.xn, D, w.ln1w, w.ln1b, M, D, eps, nullptr, 1, s));
     {
       EpiParams ep;
-      ep.mode = EPI_HEADS;
       ep.bias = w.qkvb;
-      ep.H = H; ep.Dp = Dp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = H * Dp;
-      ep.sec_out[0] = ws.q; ep.sec_out[1] = ws.k; ep.sec_out[2] = ws.vt;
-
-      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * 3 * dD, 0, gemm_bf16(ws.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
+      ep.out = ws.qkv; ep.ldo = 3 * H * dh;
+      EPD_LAUNCH(PROF_GEMM, 2.0 * dM * dD * 3 * dD, 0, gemm_bf16(ws.xn, D, w.qkv, D, M, 3 * H * dh, D, ep, s));
     }
     {
+      // heads read in place from the row-major QKV (columns: Q | K | V, head h at h*dh)
       AttnParams ap;
-      ap.q = ws.q; ap.k = ws.k; ap.v = ws.vt; ap.out = ws.ao;
+      ap.q = ws.qkv; ap.k = ws.qkv + H * dh; ap.v = ws.qkv + 2 * H * dh; ap.out = ws.ao;
+      ap.ldq = ap.ldk = ap.ldv = 3 * H * dh; ap.hs = dh;
       ap.B = nt; ap.H = H; ap.Tq = T; ap.Tk = T; ap.Dp = Dp; ap.Dv = dh;
       ap.ldo = D;
       ap.scale = 1.f / std::sqrt((float)dh);
-      ap.v_ones_col = v_ones;
       EPD_LAUNCH(PROF_ATTN, 4.0 * nt * dT * dT * dD, 0, attention_bf16(ap, s));
     }
     {
@@ -737,18 +726,17 @@ int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     EPD_LAUNCH(PROF_LN, 0, ln_bytes, layernorm_bf16(ws.r1, E, ws.r2, E, dw.r_lnkv_w, dw.r_lnkv_b, M, E, 1e-6f, s));
     {
       // k = (x + pos) Wk^T + bk  ==  x Wk^T + bk + (pos Wk^T)   [pos_k table, rows % T]
+      // row-major [M][K | V] with RH heads of RDp each
       EpiParams ep;
-      ep.mode = EPI_HEADS;
       ep.bias = dw.r_kvin_b;
       ep.resid = dw.r_posk; ep.ldr = 2 * RH * RDp; ep.r_mod = T;
-      ep.H = RH; ep.Dp = RDp; ep.T = T; ep.Tpad = Tpad; ep.sec_cols = RH * RDp;
-      ep.sec_out[0] = ws.rk; ep.sec_out[1] = ws.rvt;
-
+      ep.out = ws.rkv; ep.ldo = 2 * RH * RDp;
       EPD_LAUNCH(PROF_GEMM, 4.0 * dM * dE * dE, 0, gemm_bf16(ws.r2, E, dw.r_kvin, E, M, 2 * RH * RDp, E, ep, s));
     }
     {
       AttnParams ap;
-      ap.q = dw.r_qheads; ap.k = ws.rk; ap.v = ws.rvt; ap.out = ws.rao;
+      ap.q = dw.r_qheads; ap.k = ws.rkv; ap.v = ws.rkv + RH * RDp; ap.out = ws.rao;
+      ap.ldq = RH * RDp; ap.ldk = ap.ldv = 2 * RH * RDp; ap.hs = RDp;
       ap.B = nt; ap.H = RH; ap.Tq = Q; ap.Tk = T; ap.Dp = RDp; ap.Dv = rdh;
       ap.ldo = E; ap.q_shared = 1;
       ap.scale = 1.f / std::sqrt((float)rdh);
@@ -862,9 +850,9 @@ int Encoder::forward_f32(const uint8_t* tiles, int nt, float* out, cudaStream_t 
       EpiF32 ep;
       ep.mode = EPI_HEADS;
       ep.bias = w.qkvb;
-      ep.H = H; ep.Dp = Dp; ep.T = T; ep.sec_cols = H * Dp;
+      ep.H = H; ep.Dp = Dp; ep.T = T; ep.dh = dh; ep.sec_cols = H * dh;  // packed QKV image
       ep.sec_out[0] = X.q; ep.sec_out[1] = X.k; ep.sec_out[2] = X.v;
-      EPD_TRY(gemm_f32(X.xn, D, w.qkv, D, M, 3 * H * Dp, D, ep, s));
+      EPD_TRY(gemm_f32(X.xn, D, w.qkv, D, M, 3 * H * dh, D, ep, s));
     }
     EPD_TRY(attention_f32(X.q, X.k, X.v, X.ao, nt, H, T, T, Dp, dh, D, 0, 1.f / std::sqrt((float)dh), s));
     {

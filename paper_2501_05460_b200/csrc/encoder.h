@@ -38,7 +38,7 @@ struct GlobalWT {
   T *pe = nullptr, *pe_b = nullptr, *pos = nullptr, *post_w = nullptr, *post_b = nullptr;
   T *r_kv = nullptr, *r_lnkv_w = nullptr, *r_lnkv_b = nullptr, *r_kvin = nullptr, *r_kvin_b = nullptr;
   T *r_ow = nullptr, *r_ob = nullptr, *r_lnp_w = nullptr, *r_lnp_b = nullptr, *r_projT = nullptr;
-  T *r_qheads = nullptr, *r_posk = nullptr;
+  T *r_qheads = nullptr, *r_posk = nullptr;  // bf16: r_qheads row-major [Q][RH*RDp]
   T *m_ln_w = nullptr, *m_ln_b = nullptr, *m_f1w = nullptr, *m_f1b = nullptr, *m_f2w = nullptr,
     *m_f2b = nullptr;
   int32_t* ps_idx = nullptr;
@@ -47,9 +47,8 @@ using GlobalW = GlobalWT<bf16>;
 
 struct Workspace {
   float* h = nullptr;  // fp32 residual stream
-  bf16 *xp = nullptr, *xn = nullptr, *ao = nullptr, *q = nullptr, *k = nullptr,
-       *vt = nullptr, *f = nullptr;
-  bf16 *r1 = nullptr, *r2 = nullptr, *rk = nullptr, *rvt = nullptr, *rao = nullptr, *rr = nullptr;
+  bf16 *xp = nullptr, *xn = nullptr, *ao = nullptr, *qkv = nullptr, *f = nullptr;  // qkv: [M][3*H*dh]
+  bf16 *r1 = nullptr, *r2 = nullptr, *rkv = nullptr, *rao = nullptr, *rr = nullptr;   // rkv: [M][2*RH*RDp]
 };
 
 // fp32 check-mode workspace (allocated on first use, chunks of f32_chunk tiles).
@@ -115,7 +114,6 @@ class Encoder {
   // geometry
   int grid = 0, npatch = 0, T = 0, Tpad = 0, D = 0, H = 0, dh = 0, Dp = 0, F = 0;
   int Kreal = 0, Kpad = 0, E = 0, Q = 0, RH = 0, rdh = 0, RDp = 0;
-  bool v_ones = false;  // V carries a ones column at head dim dh (needs dh < Dp)
   // schema indices
   int w_pe = -1, b_pe = -1, w_cls = -1, w_pos = -1, w_post_w = -1, w_post_b = -1;
   int r_query = -1, r_kv = -1, r_lnq_w = -1, r_lnq_b = -1, r_lnkv_w = -1, r_lnkv_b = -1;

@@ -44,24 +44,26 @@ void set_gemm_cta_group(int policy);
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
               const EpiParams& ep, cudaStream_t stream, int bn_hint = 0);
 
-// Fused multi-head attention O = softmax(Q K^T * scale) V on tcgen05.
-//   Q : [Bq][Tq][Dp]   (q batch index = b * H + h, or h when q_shared)
-//   K : [B*H][Tk][Dp]
-//   V : [B*H][Tk][Dp]
-//   O : out[(b * Tq + q) * ldo + h * Dv + d] for d < Dv
-// Dp in {64, 80, 128}; zero-padded head dims contribute nothing.
+// Fused multi-head attention O = softmax(Q K^T * scale) V on tcgen05, reading Q, K, V
+// straight from row-major projection outputs (no per-head relayout):
+//   Q : q[(b * Tq + t) * ldq + h * hs + d]      (q_shared: q[t * ldq + h * hs + d])
+//   K : k[(b * Tk + t) * ldk + h * hs + d]
+//   V : v[(b * Tk + t) * ldv + h * hs + d]        for d < Dv
+//   O : out[(b * Tq + t) * ldo + h * Dv + d]      for d < Dv
+// hs = column stride between heads (Dv for packed heads). The MMAs run Dp = Dv rounded up
+// to a multiple of 16 (64, 80 or 128) dims: dims beyond Dv read the neighbouring head's
+// columns (or TMA zero fill past the last head); the kernel zeroes Q's dims >= Dv, so S is
+// exact, and O's dims >= Dv are never stored. ld* * 2 bytes and the pointers must be
+// 16-byte aligned.
 struct AttnParams {
   const bf16* q = nullptr;
   const bf16* k = nullptr;
   const bf16* v = nullptr;
   bf16* out = nullptr;
+  int ldq = 0, ldk = 0, ldv = 0, hs = 0;
   int B = 0, H = 0, Tq = 0, Tk = 0, Dp = 0, Dv = 0, ldo = 0;
   int q_shared = 0;
   float scale = 1.f;
-  // Caller guarantees V[..., Dv] == 1 (a zero-padded head dim set to one, Dv < Dp):
-  // the PV MMA then yields the softmax row sums in O[:, Dv] and the softmax warps
-  // skip their per-element sums.
-  int v_ones_col = 0;
 };
 int attention_bf16(const AttnParams& p, cudaStream_t stream);
 
@@ -110,6 +112,7 @@ struct EpiF32 {
   int ldo = 0;
   int H = 0, Dp = 0, T = 0, sec_cols = 0;
   float* sec_out[3] = {nullptr, nullptr, nullptr};
+  int dh = 0;  // head width of the columns (0 = Dp): dims [0, dh) of each Dp-wide head
 };
 int gemm_f32(const float* A, int lda, const float* W, int ldw, int M, int N, int K, const EpiF32& ep,
              cudaStream_t s);

@@ -77,18 +77,24 @@ def linear_heads(a: torch.Tensor, w: torch.Tensor, H: int, Dp: int, T: int, sect
 
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
-              Dv: int, scale: float, q_shared: bool = False, out: torch.Tensor | None = None,
-              v_ones_col: bool = False) -> torch.Tensor:
-    """Fused MHA; q [Bq,Tq,Dp], k and v [B*H,Tk,Dp] -> out [B*Tq, H*Dv].
+              Dv: int, scale: float, head_stride: int | None = None, q_shared: bool = False,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    """Fused MHA read in place from row-major projections.
 
-    ``v_ones_col``: v[..., Dv] is all ones (Dv < Dp), so the kernel takes the softmax
-    row sums from the PV product."""
+    q: [B*Tq (or Tq if q_shared), >= H*head_stride] (a column slice of a wider matrix is fine),
+    k, v: [B*Tk, ...]; head h occupies columns [h*head_stride, h*head_stride + Dv).
+    Returns out [B*Tq, H*Dv].
+    """
     _need_cuda(q, k, v, out)
-    Dp = q.shape[-1]
+    hs = head_stride or Dv
+    Dp = 64 if Dv <= 64 else (80 if Dv <= 80 else 128)
+    for t in (q, k, v):
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError("q, k, v must be 2-D row-major (unit column stride)")
     if out is None:
         out = torch.empty(B * Tq, H * Dv, dtype=torch.bfloat16, device=q.device)
-    call("epd_attention_bf16", q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), B, H, Tq, Tk,
-         Dp, Dv, out.stride(0), int(q_shared) | (2 if v_ones_col else 0), float(scale), _stream(q))
+    call("epd_attention_bf16", q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(), v.stride(0),
+         out.data_ptr(), out.stride(0), B, H, Tq, Tk, Dp, Dv, hs, int(q_shared), float(scale), _stream(q))
     return out
 
 

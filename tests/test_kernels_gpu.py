@@ -88,67 +88,48 @@ def test_linear_acc_f32(cuda, M, N, K, bn, ls):
     assert relerr(h, ref) <= 2e-3
 
 
-def _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g, qscale=1.0):
-    Bq = H if q_shared else B * H
-    q = torch.zeros(Bq, Tq, Dp, dtype=torch.bfloat16, device="cuda")
-    k = torch.zeros(B * H, Tk, Dp, dtype=torch.bfloat16, device="cuda")
-    v = torch.zeros(B * H, Tk, Dp, dtype=torch.bfloat16, device="cuda")
-    q[..., :Dv] = _bf(Bq, Tq, Dv, scale=qscale, gen=g)
-    k[..., :Dv] = _bf(B * H, Tk, Dv, gen=g)
-    v[..., :Dv] = _bf(B * H, Tk, Dv, gen=g)
-    return q, k, v
-
-
-@pytest.mark.parametrize("B,H,Tq,Tk,Dv,Dp,q_shared,qscale", [
-    (2, 16, 1024, 1024, 72, 80, False, 1.0),   # SigLIP self-attention
-    (1, 16, 1025, 1025, 64, 64, False, 1.0),   # InternViT (CLS -> ragged last key block)
-    (2, 28, 64, 1024, 128, 128, True, 1.0),    # MiniCPM resampler cross-attention (shared queries)
-    (1, 1, 4, 16, 8, 64, True, 1.0),           # tiny
-    (1, 2, 300, 200, 64, 64, False, 1.0),
-    (1, 4, 256, 1024, 72, 80, False, 6.0),     # peaked scores: exercises the lazy O rescale
-])
-def test_attention(cuda, B, H, Tq, Tk, Dv, Dp, q_shared, qscale):
-    from paper_2501_05460_b200 import kernels
-    g = torch.Generator(device=cuda).manual_seed(B * 100 + H + Tq + Tk)
-    q, k, v = _attn_inputs(B, H, Tq, Tk, Dv, Dp, q_shared, g, qscale)
-    scale = 1.0 / math.sqrt(Dv)
-    y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, q_shared=q_shared)
-    torch.cuda.synchronize()
-    qf = q[..., :Dv].float()
+def _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale):
+    """fp32 reference on the row-major layout (head h = columns [h*hs, h*hs + Dv))."""
+    def heads(x, T, nb):
+        return x.float().reshape(nb, T, -1)[..., :H * hs].reshape(nb, T, H, hs)[..., :Dv].permute(0, 2, 1, 3)
+    qf = heads(q, Tq, 1 if q_shared else B)
     if q_shared:
-        qf = qf.unsqueeze(0).expand(B, H, Tq, Dv).reshape(B * H, Tq, Dv)
-    kf = k[..., :Dv].float()
-    vf = v[..., :Dv].float()
-    p = torch.softmax(qf @ kf.transpose(1, 2) * scale, dim=-1)
-    o = (p @ vf).reshape(B, H, Tq, Dv).permute(0, 2, 1, 3).reshape(B * Tq, H * Dv)
-    assert relerr(y, o) <= TOL
+        qf = qf.expand(B, H, Tq, Dv)
+    kf, vf = heads(k, Tk, B), heads(v, Tk, B)
+    p = torch.softmax(qf @ kf.transpose(-1, -2) * scale, dim=-1)
+    return (p @ vf).permute(0, 2, 1, 3).reshape(B * Tq, H * Dv)
 
 
-@pytest.mark.parametrize("B,H,Tq,Tk,qscale", [(2, 16, 1024, 1024, 1.0), (1, 4, 256, 1000, 6.0), (1, 2, 100, 37, 1.0)])
-def test_attention_row_sums_from_v_ones_column(cuda, B, H, Tq, Tk, qscale):
-    """EPD_ATTN_V_ONES_COL: v[..., Dv] == 1 turns O[:, Dv] into the softmax row sums (SigLIP's
-    72 -> 80 head padding); the result must match the plain softmax, including ragged key
-    blocks and the lazy rescale."""
+@pytest.mark.parametrize("B,H,Tq,Tk,Dv,hs,q_shared,qscale", [
+    (2, 16, 1024, 1024, 72, 72, False, 1.0),   # SigLIP: packed 72-wide heads (Dp 80 reads the next head)
+    (2, 16, 1024, 1024, 72, 80, False, 1.0),   # padded 80-wide heads
+    (1, 16, 1025, 1025, 64, 64, False, 1.0),   # InternViT (CLS -> ragged last key block, rows cross images)
+    (2, 28, 64, 1024, 128, 128, True, 1.0),    # MiniCPM resampler cross-attention (shared queries)
+    (1, 1, 4, 16, 8, 8, True, 1.0),            # tiny
+    (3, 2, 300, 200, 64, 64, False, 1.0),
+    (1, 4, 256, 1024, 72, 72, False, 6.0),     # peaked scores: exercises the lazy O rescale
+])
+def test_attention(cuda, B, H, Tq, Tk, Dv, hs, q_shared, qscale):
     from paper_2501_05460_b200 import kernels
-    Dv, Dp = 72, 80
-    g = torch.Generator(device=cuda).manual_seed(B + H + Tq + Tk)
-    q, k, v = _attn_inputs(B, H, Tq, Tk, Dv, Dp, False, g, qscale)
-    v[..., Dv] = 1.0
+    g = torch.Generator(device=cuda).manual_seed(B * 100 + H + Tq + Tk + hs)
+    # Q, K, V as column sections of one fused projection matrix, as the encoder lays them out
+    qkv = _bf(B * max(Tq, Tk), 3 * H * hs, gen=g)
+    q = (_bf(Tq, H * hs, scale=qscale, gen=g) if q_shared else qkv[:B * Tq, :H * hs] * qscale)
+    k = qkv[:B * Tk, H * hs:2 * H * hs]
+    v = qkv[:B * Tk, 2 * H * hs:]
     scale = 1.0 / math.sqrt(Dv)
-    y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, v_ones_col=True)
-    y0 = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale)
+    y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, head_stride=hs, q_shared=q_shared)
     torch.cuda.synchronize()
-    p = torch.softmax(q[..., :Dv].float() @ k[..., :Dv].float().transpose(1, 2) * scale, dim=-1)
-    o = (p @ v[..., :Dv].float()).reshape(B, H, Tq, Dv).permute(0, 2, 1, 3).reshape(B * Tq, H * Dv)
-    assert relerr(y, o) <= TOL
-    assert relerr(y, y0) <= TOL
+    assert relerr(y, _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale)) <= TOL
 
 
-def test_attention_v_ones_needs_padding(cuda):
+def test_attention_rejects_bad_layouts(cuda):
     from paper_2501_05460_b200 import kernels
-    q = torch.zeros(1, 128, 64, dtype=torch.bfloat16, device=cuda)
+    x = torch.zeros(128, 64, dtype=torch.bfloat16, device=cuda)
     with pytest.raises(ValueError):
-        kernels.attention(q, q, q, 1, 1, 128, 128, 64, 0.125, v_ones_col=True)
+        kernels.attention(x, x, x, 1, 1, 128, 128, 64, 0.125, head_stride=32)  # head_stride < Dv
+    with pytest.raises(ValueError):
+        kernels.attention(x.t(), x, x, 1, 1, 64, 128, 64, 0.125)                # not row-major
 
 
 @pytest.mark.parametrize("rows,D", [(1000, 1152), (64, 3584), (8, 4096), (5, 8)])

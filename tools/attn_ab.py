@@ -22,21 +22,12 @@ def timeit(fn, iters=50, warm=5):
     return s.elapsed_time(e) / iters
 
 
-ones = len(sys.argv) > 1 and sys.argv[1] == "ones"
 tag = Path(os.environ.get("EPD_LIB_PATH", "libepd.so")).stem
 dev = torch.device("cuda")
-for (B, H, T, Dv, Dp) in [(10, 16, 1024, 72, 80), (12, 16, 1025, 64, 64)]:
-    q = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-    k = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-    v = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-    if Dp > Dv:
-        q[..., Dv:] = 0
-        k[..., Dv:] = 0
-        v[..., Dv:] = 0
-    use_ones = ones and Dv < Dp
-    if use_ones:
-        v[..., Dv] = 1.0
+for (B, H, T, Dv) in [(10, 16, 1024, 72), (12, 16, 1025, 64)]:
+    qkv = torch.randn(B * T, 3 * H * Dv, device=dev).to(torch.bfloat16)
+    q, k, v = qkv[:, :H * Dv], qkv[:, H * Dv:2 * H * Dv], qkv[:, 2 * H * Dv:]
     out = torch.empty(B * T, H * Dv, device=dev, dtype=torch.bfloat16)
-    ms = timeit(lambda: kernels.attention(q, k, v, B, H, T, T, Dv, Dv ** -0.5, out=out, v_ones_col=use_ones))
+    ms = timeit(lambda: kernels.attention(q, k, v, B, H, T, T, Dv, Dv ** -0.5, out=out))
     fl = 4 * B * H * T * T * Dv
-    print(f"{tag:6s} ones={int(use_ones)} B={B} T={T} Dv={Dv}: {ms * 1e3:7.1f} us {fl / ms / 1e9:6.1f} TF/s")
+    print(f"{tag:6s} B={B} T={T} Dv={Dv}: {ms * 1e3:7.1f} us {fl / ms / 1e9:6.1f} TF/s")

@@ -13,11 +13,11 @@ def main():
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
     dev = torch.device("cuda")
-    for (B, H, T, Dv, Dp, Tq, qs) in [(10, 16, 1024, 72, 80, 1024, False), (10, 16, 1025, 64, 64, 1025, False),
-                                      (10, 28, 1024, 128, 128, 64, True)]:
-        q = torch.randn(H if qs else B * H, Tq, Dp, device=dev).to(torch.bfloat16)
-        k = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-        v = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
+    for (B, H, T, Dv, Tq, qs) in [(10, 16, 1024, 72, 1024, False), (10, 16, 1025, 64, 1025, False),
+                                  (10, 28, 1024, 128, 64, True)]:
+        kv = torch.randn(B * T, 2 * H * Dv, device=dev).to(torch.bfloat16)
+        k, v = kv[:, :H * Dv], kv[:, H * Dv:]
+        q = torch.randn(Tq if qs else B * Tq, H * Dv, device=dev).to(torch.bfloat16)
         out = torch.empty(B * Tq, H * Dv, device=dev, dtype=torch.bfloat16)
         f = lambda: kernels.attention(q, k, v, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out)  # noqa: E731
         for _ in range(50):

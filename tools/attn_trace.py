@@ -12,9 +12,8 @@ from paper_2501_05460_b200 import _lib, kernels  # noqa: E402
 
 dev = torch.device("cuda")
 B, H, T, Dv, Dp = 10, 16, 1024, 72, 80
-q = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-k = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-v = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
+qkv = torch.randn(B * T, 3 * H * Dv, device=dev).to(torch.bfloat16)
+q, k, v = qkv[:, :H * Dv], qkv[:, H * Dv:2 * H * Dv], qkv[:, 2 * H * Dv:]
 out = torch.empty(B * T, H * Dv, device=dev, dtype=torch.bfloat16)
 L = _lib.lib()
 L.epd_debug_trace.argtypes = [C.c_void_p, C.c_int]

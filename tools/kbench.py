@@ -47,19 +47,14 @@ def main():
             for bn in (0, 128, 192, 256):
                 ms = timeit(lambda: kernels.linear_acc(a, w, h, bias=b, bn=bn))
                 print(f"gemm {name}+acc_f32 bn={bn:3d}: {ms*1e3:8.1f} us  {2*M*N*K/ms/1e9:7.1f} TFLOP/s")
-    for (B, H, T, Dv, Dp, Tq, qs) in [(10, 16, 1024, 72, 80, 1024, False), (10, 28, 1024, 128, 128, 64, True)]:
-        q = torch.randn(H if qs else B * H, Tq, Dp, device=dev).to(torch.bfloat16)
-        k = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
-        v = torch.randn(B * H, T, Dp, device=dev).to(torch.bfloat16)
+    for (B, H, T, Dv, Tq, qs) in [(10, 16, 1024, 72, 1024, False), (10, 28, 1024, 128, 64, True)]:
+        kv = torch.randn(B * T, 2 * H * Dv, device=dev).to(torch.bfloat16)
+        k, v = kv[:, :H * Dv], kv[:, H * Dv:]
+        q = torch.randn(Tq if qs else B * Tq, H * Dv, device=dev).to(torch.bfloat16)
         out = torch.empty(B * Tq, H * Dv, device=dev, dtype=torch.bfloat16)
         ms = timeit(lambda: kernels.attention(q, k, v, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out))
         fl = 4 * B * H * Tq * T * Dv
         print(f"attn B={B} H={H} Tq={Tq} Tk={T} Dv={Dv}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s (algorithmic)")
-        if Dv < Dp:
-            v[..., Dv] = 1.0
-            ms = timeit(lambda: kernels.attention(q, k, v, B, H, Tq, T, Dv, Dv ** -0.5, q_shared=qs, out=out,
-                                                  v_ones_col=True))
-            print(f"attn (v ones col) B={B} H={H} Tq={Tq}: {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
     x = torch.randn(M, 1152, device=dev).to(torch.bfloat16)
     g = torch.ones(1152, device=dev, dtype=torch.bfloat16)
     y = torch.empty_like(x)
