@@ -44,9 +44,9 @@ def summarize(rep):
                     v *= 1e6
                 elif u in ("Gbyte", "GB"):
                     v *= 1e9
-                elif u == "usecond":
+                elif u in ("usecond", "us"):
                     v *= 1e3
-                elif u == "msecond":
+                elif u in ("msecond", "ms"):
                     v *= 1e6
             except ValueError:
                 pass
