@@ -28,28 +28,6 @@
 #include "launch.h"
 #include "tmap.h"
 
-#ifdef EPD_ATTN_TRACE
-// Experiment-only timeline of one CTA (tools/attn_trace.py): %clock stamps in fixed
-// shared-memory slots [code 0..31][j 0..15][g 0..1], flushed to global at exit.
-__device__ unsigned int g_attn_trace[32 * 16 * 2];
-__shared__ unsigned int s_attn_trace[32 * 16 * 2];
-#define ATTN_TRACE_ON (blockIdx.x == 1 && blockIdx.y == 5 && blockIdx.z == 5)
-#define ATTN_TRACE(code, j, g)                                               \
-  do {                                                                       \
-    unsigned _c;                                                             \
-    asm volatile("mov.u32 %0, %%clock;" : "=r"(_c));                        \
-    if ((j) < 16) s_attn_trace[((code) * 16 + (j)) * 2 + (g)] = _c;          \
-  } while (0)
-extern "C" int epd_debug_trace(unsigned int* host, int cap) {
-  const int n = cap < 1024 ? cap : 1024;
-  cudaMemcpyFromSymbol(host, g_attn_trace, n * sizeof(unsigned int));
-  return n;
-}
-#else
-#define ATTN_TRACE(code, j, g) \
-  do {                         \
-  } while (0)
-#endif
 
 namespace epd {
 
@@ -137,8 +115,8 @@ struct Cfg {
   static constexpr int V_ATOM = KB * 32;               // 64 keys x 16 dims x 2 B
   static constexpr int V_BYTES = (DP / 16) * V_ATOM;
   static constexpr int V_AL = (V_BYTES + 1023) / 1024 * 1024;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + NQ * Q_AL;
+  static constexpr int OFF_Q = 0;                      // [2 buffers][NQ tiles]: next item's Q prefetched
+  static constexpr int OFF_K = OFF_Q + 2 * NQ * Q_AL;
   static constexpr int OFF_V = OFF_K + KS * K_AL;
   static constexpr int OFF_BAR = OFF_V + KVS * V_AL;
   static constexpr int SMEM = OFF_BAR + 256 + 1024;  // 31 mbarriers + TMEM holder in the 256 B
@@ -150,8 +128,48 @@ struct Cfg {
   __host__ __device__ static constexpr uint32_t q_col(int g) { return (uint32_t)(256 + 128 * g + DP); }
   static_assert(DP + DP / 2 <= 128 || NQ == 1, "O_g and Q_g must share a 128-column slot");
   static_assert(DP + DP / 2 <= 256, "O and Q must fit above the S buffers");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
+// Work items: (query-tile pair, head, image), consecutive pairs sharing (image, head).
+// Pairs that would form a last, partial round over the persistent CTAs are split into
+// single 128-row tiles, so that round takes about half as long; a single tile past Tq
+// is an empty item (nq = 0) that every role skips without touching a barrier.
+struct AttnItem {
+  int b, h, q0, nq;
+};
+template <int NQ>
+EPD_DEVICE AttnItem attn_item(const AttnParams& p, int w, int nqp, int npairs_main) {
+  int pair = w, half = -1;
+  if (w >= npairs_main) {
+    pair = npairs_main + ((w - npairs_main) >> 1);
+    half = (w - npairs_main) & 1;
+  }
+  AttnItem it;
+  const int qp = pair % nqp;
+  const int bh = pair / nqp;
+  it.h = bh % p.H;
+  it.b = bh / p.H;
+  it.q0 = qp * (NQ * 128);
+  if (half < 0 || NQ == 1) {
+    it.nq = p.Tq - it.q0 > 128 ? NQ : 1;  // query tiles with at least one valid row
+    if (NQ == 1 && half > 0) it.nq = 0;
+  } else {
+    it.q0 += half * 128;
+    it.nq = p.Tq > it.q0 ? 1 : 0;
+  }
+  return it;
+}
+// Number of items and pairs kept whole for a persistent grid of G CTAs.
+__host__ __device__ inline void attn_sched(int npairs, int G, int nq_max, int* main_pairs, int* nitems) {
+  const int m = nq_max > 1 ? (npairs / G) * G : npairs;
+  *main_pairs = m;
+  *nitems = m + 2 * (npairs - m);
+}
+
+// Persistent: one CTA per SM loops over the work items. Barrier phases are tracked per
+// role and per (tile, buffer) so that tail items with a single query tile keep both sides
+// of every barrier in step.
 template <int DP, int NQ>
 __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     attention_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQt,
@@ -161,37 +179,34 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [KS]
-  uint64_t* k_empty = bars + 5;   // [KS]
-  uint64_t* v_full = bars + 9;    // [KVS]
-  uint64_t* v_empty = bars + 13;  // [KVS]
-  uint64_t* s_full = bars + 17;   // [NQ][2] S_g(j) landed in buffer j & 1
+  uint64_t* q_full = bars + 0;    // [2] Q buffer landed
+  uint64_t* q_empty = bars + 2;   // [2] Q buffer copied into TMEM by every softmax thread
+  uint64_t* k_full = bars + 4;    // [KS]
+  uint64_t* k_empty = bars + 8;   // [KS]
+  uint64_t* v_full = bars + 12;   // [KVS]
+  uint64_t* v_empty = bars + 16;  // [KVS]
+  uint64_t* s_full = bars + 20;   // [NQ][2] S_g(j) landed in buffer j & 1
   // [NQ][2] P_g(j) written to TMEM buffer j & 1. One barrier per buffer: a softmax group
   // may finish blocks j and j+1 before the MMA warp consumes P_g(j), which would alias
   // the phase parity of a single barrier.
-  uint64_t* p_ready = bars + 21;
-  uint64_t* pv_done = bars + 25;  // [NQ] PV_g(j) complete (O_g stable up to block j)
-  uint64_t* q_tm = bars + 27;     // [NQ] Q_g copied into TMEM
-  // [NQ] last PV_g complete. (pv_done alone cannot say so: when the softmax reaches the
-  // end only PV_g(nkb-3) is known complete, two phases behind, which aliases the parity.)
-  uint64_t* o_done = bars + 29;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 31);
+  uint64_t* p_ready = bars + 24;
+  uint64_t* pv_done = bars + 28;  // [NQ] PV_g(j) complete (O_g stable up to block j)
+  uint64_t* q_tm = bars + 30;     // [NQ] Q_g copied into TMEM
+  uint64_t* o_done = bars + 32;   // [NQ] the item's last PV_g complete
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 34);
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int h = blockIdx.y;
-  const int b = blockIdx.z;
-  const int hcol = h * p.hs;                             // head h's first column
-  const int qrow0 = p.q_shared ? 0 : b * p.Tq;            // image b's first query row
-  const int krow0 = b * p.Tk;                             // and first key row
-  const int q0 = blockIdx.x * (NQ * 128);
-  const int rem = p.Tq - q0;
-  const int nq = rem > 128 ? NQ : 1;  // query tiles with at least one valid row
+  const int nqp = (p.Tq + NQ * 128 - 1) / (NQ * 128);
+  int pmain, nitems;
+  attn_sched(nqp * p.H * p.B, gridDim.x, NQ, &pmain, &nitems);
   const int nkb = (p.Tk + C::KB - 1) / C::KB;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], NQ * 128);
+    }
     for (int i = 0; i < C::KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -221,43 +236,61 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, nq * 128 * DP * 2);
-      for (int g = 0; g < nq; ++g) {
-        uint8_t* qd = smem + C::OFF_Q + g * C::Q_AL;
-        const int qr = qrow0 + q0 + g * 128;
-        for (int a = 0; a < C::MAIN; ++a) tma_load_2d(qd + a * C::Q_ATOM, &tmQ, q_full, hcol + a * 64, qr);
-        if (C::TAIL) tma_load_2d(qd + C::MAIN * C::Q_ATOM, &tmQt, q_full, hcol + C::MAIN * 64, qr);
-      }
-      for (int j = 0; j < nkb; ++j) {
-        const int s = j % C::KS;
-        mbar_wait(&k_empty[s], ((j / C::KS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], C::K_BYTES);
-        uint8_t* kd = smem + C::OFF_K + s * C::K_AL;
-        for (int a = 0; a < C::MAIN; ++a) tma_load_2d(kd + a * C::K_ATOM, &tmK, &k_full[s], hcol + a * 64, krow0 + j * C::KB);
-        if (C::TAIL) tma_load_2d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], hcol + C::MAIN * 64, krow0 + j * C::KB);
+      // Q of each item (double-buffered, so the next item's Q is fetched during this one)
+      // followed by its K blocks; the K ring runs on across items.
+      int kc = 0, it = 0;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
+        const int qb = it & 1;
+        const int hcol = x.h * p.hs;
+        mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], x.nq * 128 * DP * 2);
+        for (int g = 0; g < x.nq; ++g) {
+          uint8_t* qd = smem + C::OFF_Q + (qb * NQ + g) * C::Q_AL;
+          const int qr = (p.q_shared ? 0 : x.b * p.Tq) + x.q0 + g * 128;
+          for (int a = 0; a < C::MAIN; ++a) tma_load_2d(qd + a * C::Q_ATOM, &tmQ, &q_full[qb], hcol + a * 64, qr);
+          if (C::TAIL) tma_load_2d(qd + C::MAIN * C::Q_ATOM, &tmQt, &q_full[qb], hcol + C::MAIN * 64, qr);
+        }
+        if (x.nq == 0) continue;  // empty item: Q buffer handed over with no bytes, no K blocks
+        const int krow0 = x.b * p.Tk;
+        for (int j = 0; j < nkb; ++j, ++kc) {
+          const int s = kc % C::KS;
+          mbar_wait(&k_empty[s], ((kc / C::KS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&k_full[s], C::K_BYTES);
+          uint8_t* kd = smem + C::OFF_K + s * C::K_AL;
+          for (int a = 0; a < C::MAIN; ++a)
+            tma_load_2d(kd + a * C::K_ATOM, &tmK, &k_full[s], hcol + a * 64, krow0 + j * C::KB);
+          if (C::TAIL) tma_load_2d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], hcol + C::MAIN * 64, krow0 + j * C::KB);
+        }
       }
     } else if (lane == 1) {
-      for (int j = 0; j < nkb; ++j) {
-        const int s = j % C::KVS;
-        mbar_wait(&v_empty[s], ((j / C::KVS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
-        uint8_t* vd = smem + C::OFF_V + s * C::V_AL;
-        for (int a = 0; a < DP / 16; ++a) tma_load_2d(vd + a * C::V_ATOM, &tmV, &v_full[s], hcol + a * 16, krow0 + j * C::KB);
+      int vc = 0;
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
+        if (x.nq == 0) continue;
+        const int hcol = x.h * p.hs, krow0 = x.b * p.Tk;
+        for (int j = 0; j < nkb; ++j, ++vc) {
+          const int s = vc % C::KVS;
+          mbar_wait(&v_empty[s], ((vc / C::KVS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
+          uint8_t* vd = smem + C::OFF_V + s * C::V_AL;
+          for (int a = 0; a < DP / 16; ++a)
+            tma_load_2d(vd + a * C::V_ATOM, &tmV, &v_full[s], hcol + a * 16, krow0 + j * C::KB);
+        }
       }
     }
   } else if (warp == 1) {
     {  // whole warp: uniform operands, elected issue
       constexpr uint32_t idesc_s = make_idesc_bf16(128, C::KB);
       constexpr uint32_t idesc_o = make_idesc_bf16(128, DP) | (1u << 16);  // B (V) is MN-major
-      // Descriptors are precomputed: per MMA the issuing thread only adds a constant
-      // (start address >> 4) to a base descriptor.
       const uint64_t k_main0 = make_sdesc(smem_u32(smem + C::OFF_K), 1024, 2);
       const uint64_t k_tail0 = make_sdesc(smem_u32(smem + C::OFF_K + C::MAIN * C::K_ATOM), 256, 6);
       const uint64_t v_base0 = make_sdesc_lbo(smem_u32(smem + C::OFF_V), C::V_ATOM, 256, 6);
-      // S_g(j) = Q_g K_j^T into buffer j & 1; Q_g is the TMEM (A) operand.
-      auto issue_s = [&](int g, int j) {
-        ATTN_TRACE(3, j, g);
-        const uint64_t ko = (uint64_t)(((j % C::KS) * C::K_AL) >> 4);
+      int kc = 0, vc = 0;
+      uint32_t qtm_ph = 0, pr_ph = 0;  // phase bits: q_tm bit g, p_ready bit 2g + buffer
+      // S_g(j) = Q_g K_j^T into buffer j & 1; K block j sits in ring slot kslot.
+      auto issue_s = [&](int g, int j, int kslot) {
+        const uint64_t ko = (uint64_t)((kslot * C::K_AL) >> 4);
         const uint32_t d = tmem + C::s_col(g, j & 1);
         const uint32_t qa = tmem + C::q_col(g);
 #pragma unroll
@@ -271,46 +304,54 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
           }
         }
         tc_commit_warp(&s_full[2 * g + (j & 1)]);
-        ATTN_TRACE(4, j, g);
       };
-      mbar_wait(q_full, 0);
-      for (int g = 0; g < nq; ++g) mbar_wait(&q_tm[g], 0);
-      // two blocks of S in flight per query tile: softmax(j) overlaps S(j+1)
-      for (int j = 0; j < 2 && j < nkb; ++j) {
-        mbar_wait(&k_full[j % C::KS], (j / C::KS) & 1);
-        tc_fence_after();
-        for (int g = 0; g < nq; ++g) issue_s(g, j);
-        tc_commit_warp(&k_empty[j % C::KS]);
-      }
-      for (int j = 0; j < nkb; ++j) {
-        const int sv = j % C::KVS;
-        for (int g = 0; g < nq; ++g) {
-          ATTN_TRACE(5, j, g);
-          mbar_wait(&p_ready[2 * g + (j & 1)], (j >> 1) & 1);
-          ATTN_TRACE(6, j, g);
-          if (g == 0) mbar_wait(&v_full[sv], (j / C::KVS) & 1);
-          tc_fence_after();
-          ATTN_TRACE(7, j, g);
-          const uint64_t vb = v_base0 + (uint64_t)((sv * C::V_AL) >> 4);
-          const uint32_t od = tmem + C::o_col(g), pa = tmem + C::s_col(g, j & 1);
-#pragma unroll
-          for (int kk = 0; kk < C::KB / 16; ++kk) {
-            // A = P from TMEM: keys 16kk..16kk+15 are bf16 pairs in columns 8kk..8kk+7
-            // B = V, MN-major SW32: key row kk*16 (512 B), LBO = 2 KB (next 16 dims), SBO = 256 B
-            umma_ts_warp(od, pa + kk * 8, vb + (uint64_t)(kk * 32), idesc_o, (j | kk) != 0);
-          }
-          tc_commit_warp(&pv_done[g]);
-          if (j + 1 == nkb) tc_commit_warp(&o_done[g]);
-          ATTN_TRACE(8, j, g);
-          if (j + 2 < nkb) {
-            // S_g(j+2) overwrites P_g(j) only after PV_g(j) (in-order tensor pipe)
-            if (g == 0) mbar_wait(&k_full[(j + 2) % C::KS], ((j + 2) / C::KS) & 1);
-            tc_fence_after();
-            issue_s(g, j + 2);
-          }
+      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+        const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
+        if (x.nq == 0) continue;
+        for (int g = 0; g < x.nq; ++g) {
+          mbar_wait(&q_tm[g], (qtm_ph >> g) & 1);
+          qtm_ph ^= 1u << g;
         }
-        tc_commit_warp(&v_empty[sv]);
-        if (j + 2 < nkb) tc_commit_warp(&k_empty[(j + 2) % C::KS]);
+        tc_fence_after();
+        // two blocks of S in flight per query tile: softmax(j) overlaps S(j+1)
+        for (int j = 0; j < 2 && j < nkb; ++j) {
+          const int ks = (kc + j) % C::KS;
+          mbar_wait(&k_full[ks], ((kc + j) / C::KS) & 1);
+          tc_fence_after();
+          for (int g = 0; g < x.nq; ++g) issue_s(g, j, ks);
+          tc_commit_warp(&k_empty[ks]);
+        }
+        for (int j = 0; j < nkb; ++j) {
+          const int sv = (vc + j) % C::KVS;
+          for (int g = 0; g < x.nq; ++g) {
+            const int pb = 2 * g + (j & 1);
+            mbar_wait(&p_ready[pb], (pr_ph >> pb) & 1);
+            pr_ph ^= 1u << pb;
+            if (g == 0) mbar_wait(&v_full[sv], ((vc + j) / C::KVS) & 1);
+            tc_fence_after();
+            const uint64_t vb = v_base0 + (uint64_t)((sv * C::V_AL) >> 4);
+            const uint32_t od = tmem + C::o_col(g), pa = tmem + C::s_col(g, j & 1);
+#pragma unroll
+            for (int kk = 0; kk < C::KB / 16; ++kk) {
+              // A = P from TMEM: keys 16kk..16kk+15 are bf16 pairs in columns 8kk..8kk+7
+              // B = V, MN-major SW32: key row kk*16 (512 B), LBO = 2 KB (next 16 dims), SBO = 256 B
+              umma_ts_warp(od, pa + kk * 8, vb + (uint64_t)(kk * 32), idesc_o, (j | kk) != 0);
+            }
+            tc_commit_warp(&pv_done[g]);
+            if (j + 1 == nkb) tc_commit_warp(&o_done[g]);
+            if (j + 2 < nkb) {
+              // S_g(j+2) overwrites P_g(j) only after PV_g(j) (in-order tensor pipe)
+              const int ks = (kc + j + 2) % C::KS;
+              if (g == 0) mbar_wait(&k_full[ks], ((kc + j + 2) / C::KS) & 1);
+              tc_fence_after();
+              issue_s(g, j + 2, ks);
+            }
+          }
+          tc_commit_warp(&v_empty[sv]);
+          if (j + 2 < nkb) tc_commit_warp(&k_empty[(kc + j + 2) % C::KS]);
+        }
+        kc += nkb;
+        vc += nkb;
       }
     }
   } else {
@@ -322,12 +363,17 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
     const uint32_t o_tm = tmem + lane_off + C::o_col(g);
     const float c = p.scale * 1.4426950408889634f;
-    if (g < nq) {
-      {
-        // copy this thread's Q row (K-major swizzled smem) into TMEM as bf16 pairs:
-        // column c of Q_g holds head dims 2c, 2c+1 (the TS-MMA A-operand layout)
-        mbar_wait(q_full, 0);
-        const uint8_t* qs = smem + C::OFF_Q + g * C::Q_AL;
+    uint32_t sf_ph = 0, od_ph = 0;  // s_full phase bit per buffer
+    int pv_count = 0;  // PV_g commits so far (pv_done phase bookkeeping)
+    // Wait for item `it`'s Q buffer; tiles of this warp's group copy their Q rows into TMEM
+    // as bf16 pairs (column c = head dims 2c, 2c+1: the TS-MMA A layout), zeroing dims >= Dv.
+    // Every thread releases the buffer. Called only once all S MMAs of the previous item
+    // are complete (its last s_full was observed).
+    auto take_q = [&](int it, int nq) {
+      const int qb = it & 1;
+      mbar_wait(&q_full[qb], (it >> 1) & 1);
+      if (g < nq) {
+        const uint8_t* qs = smem + C::OFF_Q + (qb * NQ + g) * C::Q_AL;
         const uint32_t q_tm_addr = tmem + lane_off + C::q_col(g);
 #pragma unroll
         for (int c8 = 0; c8 < DP / 8; ++c8) {
@@ -349,118 +395,128 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         tc_fence_before();
         mbar_arrive(&q_tm[g]);
       }
-      float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkb; ++j) {
-        const bool tr = wi == 4 * g && lane == 0;
-        if (tr) ATTN_TRACE(9, j, g);
-        const int kvalid = p.Tk - j * C::KB;
-        mbar_wait(&s_full[2 * g + (j & 1)], (j >> 1) & 1);
-        tc_fence_after();
-        if (tr) ATTN_TRACE(10, j, g);
-        const uint32_t s_tm = tmem + lane_off + C::s_col(g, j & 1);
-        uint32_t sv[64];
-        tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
-        tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
-        tmem_ld_wait();
-        if (tr) ATTN_TRACE(11, j, g);
-        if (kvalid < 64) {
+      mbar_arrive(&q_empty[qb]);
+    };
+    int it = 0;
+    if ((int)blockIdx.x < nitems) take_q(0, attn_item<NQ>(p, blockIdx.x, nqp, pmain).nq);
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+      const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
+      float l = 0.f;
+      if (g < x.nq) {
+        float m_used = -INFINITY;
+        for (int j = 0; j < nkb; ++j) {
+          const int kvalid = p.Tk - j * C::KB;
+          mbar_wait(&s_full[2 * g + (j & 1)], (sf_ph >> (j & 1)) & 1);
+          sf_ph ^= 1u << (j & 1);
+          tc_fence_after();
+          const uint32_t s_tm = tmem + lane_off + C::s_col(g, j & 1);
+          uint32_t sv[64];
+          tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
+          tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
+          tmem_ld_wait();
+          if (kvalid < 64) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (i >= kvalid) sv[i] = __float_as_uint(-INFINITY);
-        }
-        float mx;
-        {
-          float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            for (int i = 0; i < 64; ++i)
+              if (i >= kvalid) sv[i] = __float_as_uint(-INFINITY);
+          }
+          float mx;
+          {
+            float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int i = 0; i < 64; i += 8)
+            for (int i = 0; i < 64; i += 8)
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-              m4[u] = fmax3(m4[u], __uint_as_float(sv[i + 2 * u]), __uint_as_float(sv[i + 2 * u + 1]));
-          mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
-        }
-        if (tr) ATTN_TRACE(12, j, g);
-        const float m_new = fmaxf(m_used, mx * c);
-        if (j == 0) {
-          m_used = m_new;
-        } else {
-          // Lazy rescale: only when a row max grows by more than 2^8. PV_g(j-1) may still
-          // be accumulating into O_g, so wait for it first (rare path).
-          const bool need = m_new > m_used + 8.f;
-          if (__any_sync(0xffffffffu, need)) {
-            mbar_wait(&pv_done[g], (j - 1) & 1);
-            tc_fence_after();
-            const float alpha = need ? ex2(m_used - m_new) : 1.f;
+              for (int u = 0; u < 4; ++u)
+                m4[u] = fmax3(m4[u], __uint_as_float(sv[i + 2 * u]), __uint_as_float(sv[i + 2 * u + 1]));
+            mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
+          }
+          const float m_new = fmaxf(m_used, mx * c);
+          if (j == 0) {
+            m_used = m_new;
+          } else {
+            // Lazy rescale: only when a row max grows by more than 2^8. PV_g(j-1) may still
+            // be accumulating into O_g, so wait for it first (rare path).
+            const bool need = m_new > m_used + 8.f;
+            if (__any_sync(0xffffffffu, need)) {
+              mbar_wait(&pv_done[g], (pv_count - 1) & 1);
+              tc_fence_after();
+              const float alpha = need ? ex2(m_used - m_new) : 1.f;
 #pragma unroll
-            for (int c0 = 0; c0 < DP; c0 += 16) {
-              uint32_t o[16];
-              tmem_ld16(o_tm + c0, o);
-              tmem_ld_wait();
+              for (int c0 = 0; c0 < DP; c0 += 16) {
+                uint32_t o[16];
+                tmem_ld16(o_tm + c0, o);
+                tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st8(o_tm + c0, o);
-              tmem_st8(o_tm + c0 + 8, o + 8);
-            }
-            tmem_st_wait();
-            if (need) {
-              l *= alpha;
-              m_used = m_new;
+                for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                tmem_st8(o_tm + c0, o);
+                tmem_st8(o_tm + c0 + 8, o + 8);
+              }
+              tmem_st_wait();
+              if (need) {
+                l *= alpha;
+                m_used = m_new;
+              }
             }
           }
-        }
-        const float nm = -m_used;
-        float rs0 = 0.f, rs1 = 0.f;
-        uint32_t pk[32];
+          const float nm = -m_used;
+          float rs0 = 0.f, rs1 = 0.f;
+          uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          // The softmax is MUFU-bound (16 ex2/clk/SM): a share of the pairs goes to the FMA pipe.
-          const bool poly = ((i >> 1) & 7) < EPD_POLY_EIGHTHS;
-          const float a0 = fmaf(__uint_as_float(sv[i]), c, nm), a1 = fmaf(__uint_as_float(sv[i + 1]), c, nm);
-          const float e0 = poly ? ex2_poly(a0) : ex2(a0);
-          const float e1 = poly ? ex2_poly(a1) : ex2(a1);
-          rs0 += e0;
-          rs1 += e1;
-          pk[i >> 1] = pack_bf16x2(e0, e1);
+          for (int i = 0; i < 64; i += 2) {
+            // The softmax is MUFU-bound (16 ex2/clk/SM): a share of the pairs goes to the FMA pipe.
+            const bool poly = ((i >> 1) & 7) < EPD_POLY_EIGHTHS;
+            const float a0 = fmaf(__uint_as_float(sv[i]), c, nm), a1 = fmaf(__uint_as_float(sv[i + 1]), c, nm);
+            const float e0 = poly ? ex2_poly(a0) : ex2(a0);
+            const float e1 = poly ? ex2_poly(a1) : ex2(a1);
+            rs0 += e0;
+            rs1 += e1;
+            pk[i >> 1] = pack_bf16x2(e0, e1);
+          }
+          tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
+          tmem_st_wait();
+          l += rs0 + rs1;
+          tc_fence_before();
+          mbar_arrive(&p_ready[2 * g + (j & 1)]);
+          ++pv_count;
         }
-        if (tr) ATTN_TRACE(14, j, g);
-        tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
-        tmem_st_wait();
-        l += rs0 + rs1;
-        tc_fence_before();
-        mbar_arrive(&p_ready[2 * g + (j & 1)]);
-        if (tr) ATTN_TRACE(15, j, g);
       }
-      mbar_wait(&o_done[g], 0);
-      tc_fence_after();
-      const int qrow = q0 + g * 128 + r;
-      const float inv = 1.f / l;
-      bf16* dst = p.out + ((size_t)b * p.Tq + qrow) * p.ldo + (size_t)h * p.Dv;
+      // All S MMAs of this item are complete: hand the next item's Q to the tensor core
+      // before the O epilogue, so its first S blocks overlap the epilogue.
+      const int wn = w + gridDim.x;
+      if (wn < nitems) take_q(it + 1, attn_item<NQ>(p, wn, nqp, pmain).nq);
+      if (g < x.nq) {
+        mbar_wait(&o_done[g], od_ph);
+        od_ph ^= 1;
+        tc_fence_after();
+        const int qrow = x.q0 + g * 128 + r;
+        const float inv = 1.f / l;
+        bf16* dst = p.out + ((size_t)x.b * p.Tq + qrow) * p.ldo + (size_t)x.h * p.Dv;
 #pragma unroll
-      for (int c0 = 0; c0 < DP; c0 += 16) {
-        uint32_t o[16];
-        tmem_ld16(o_tm + c0, o);
-        tmem_ld_wait();
+        for (int c0 = 0; c0 < DP; c0 += 16) {
+          uint32_t o[16];
+          tmem_ld16(o_tm + c0, o);
+          tmem_ld_wait();
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          if (qrow < p.Tq && c0 + hh * 8 < p.Dv) {
-            const uint32_t* oo = o + hh * 8;
-            uint4 v;
-            v.x = pack_bf16x2(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv);
-            v.y = pack_bf16x2(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv);
-            v.z = pack_bf16x2(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv);
-            v.w = pack_bf16x2(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv);
-            *reinterpret_cast<uint4*>(dst + c0 + hh * 8) = v;
+          for (int hh = 0; hh < 2; ++hh) {
+            if (qrow < p.Tq && c0 + hh * 8 < p.Dv) {
+              const uint32_t* oo = o + hh * 8;
+              uint4 v;
+              v.x = pack_bf16x2(__uint_as_float(oo[0]) * inv, __uint_as_float(oo[1]) * inv);
+              v.y = pack_bf16x2(__uint_as_float(oo[2]) * inv, __uint_as_float(oo[3]) * inv);
+              v.z = pack_bf16x2(__uint_as_float(oo[4]) * inv, __uint_as_float(oo[5]) * inv);
+              v.w = pack_bf16x2(__uint_as_float(oo[6]) * inv, __uint_as_float(oo[7]) * inv);
+              *reinterpret_cast<uint4*>(dst + c0 + hh * 8) = v;
+            }
           }
         }
+        // O_g is read: the next item's PV_g(0) (issued after its P_g(0), i.e. after this
+        // thread's next p_ready arrival) may overwrite it.
+        tc_fence_before();
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-#ifdef EPD_ATTN_TRACE
-  if (ATTN_TRACE_ON)
-    for (int i = threadIdx.x; i < 1024; i += blockDim.x) g_attn_trace[i] = s_attn_trace[i];
-#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -489,9 +545,14 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  dim3 grid((p.Tq + NQ * 128 - 1) / (NQ * 128), p.H, p.B);
-  return launch_kernel(attention_kernel<DP, NQ>, grid, dim3(C::THREADS), C::SMEM, stream, 1, mq, mqt, mk, mkt, mv,
-                       p);
+  const int npairs = ((p.Tq + NQ * 128 - 1) / (NQ * 128)) * p.H * p.B;
+  // (the kernel recomputes the same schedule from gridDim.x: with fewer items than SMs,
+  // every pair is split and the grid is the item count)
+  int pmain = 0, nitems = 0;
+  attn_sched(npairs, num_sms(), NQ, &pmain, &nitems);
+  const int grid = nitems < num_sms() ? nitems : num_sms();
+  return launch_kernel(attention_kernel<DP, NQ>, dim3(grid), dim3(C::THREADS), C::SMEM, stream, 1, mq, mqt, mk, mkt,
+                       mv, p);
 }
 
 }  // namespace
