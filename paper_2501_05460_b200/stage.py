@@ -52,6 +52,7 @@ class RequestResult:
     kinds: list | None = None           # cache classification per tile (hit/miss/dup)
     ep_bytes: int = 0                    # bytes moved to the prefill rank (engine.py:524)
     tokens: torch.Tensor | None = None   # packed [n, tokens_per_tile, hidden] on the prefill rank
+    readback: torch.cuda.Event | None = None  # set when tokens were copied into out_host
 
 
 class EncodeStage:
@@ -76,6 +77,12 @@ class EncodeStage:
         if cache is not None and rank != prefill_rank:
             raise ValueError("the MM-token cache lives on the prefill rank")
         self._staging = None
+        # Host I/O runs on its own streams so consecutive requests pipeline: request i+1's
+        # H2D upload overlaps request i's encode, and request i's D2H readback overlaps
+        # request i+1's encode (PCIe is full duplex; uploads and readbacks never queue
+        # behind one another).
+        self._up = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
+        self._down = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
 
     # ------------------------------------------------------------------ helpers
     def _tokens_shape(self, n: int):
@@ -85,12 +92,41 @@ class EncodeStage:
         return torch.empty(self._tokens_shape(n), dtype=torch.bfloat16, device=self.device)
 
     def _upload(self, tiles_host: torch.Tensor, idx) -> torch.Tensor:
-        if idx is None:
-            return tiles_host.to(self.device, non_blocking=True)
+        """Pinned host tiles -> device on the upload stream; the compute stream waits for it."""
         if isinstance(idx, slice):
-            return tiles_host[idx].to(self.device, non_blocking=True)
-        sel = tiles_host.index_select(0, torch.as_tensor(idx, dtype=torch.int64))
-        return sel.to(self.device, non_blocking=True)
+            host = tiles_host[idx]
+        elif idx is None:
+            host = tiles_host
+        else:
+            host = tiles_host.index_select(0, torch.as_tensor(idx, dtype=torch.int64))
+        if self._up is None:
+            return host.to(self.device, non_blocking=True)
+        compute = torch.cuda.current_stream(self.device)
+        self._up.wait_stream(compute)  # the buffer the allocator hands out may still be read there
+        with torch.cuda.stream(self._up):
+            dev = host.to(self.device, non_blocking=True)
+        compute.wait_stream(self._up)
+        dev.record_stream(compute)
+        return dev
+
+    def _readback(self, tokens: torch.Tensor, out_host: torch.Tensor) -> torch.cuda.Event:
+        """Packed tokens -> pinned host buffer on the download stream, after the compute
+        stream's work so far; returns the event that marks the copy done."""
+        compute = torch.cuda.current_stream(self.device)
+        self._down.wait_stream(compute)
+        with torch.cuda.stream(self._down):
+            out_host.copy_(tokens, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self._down)
+        tokens.record_stream(self._down)
+        return ev
+
+    def join(self) -> None:
+        """Make the caller's stream wait for all host I/O issued so far."""
+        if self._up is not None:
+            compute = torch.cuda.current_stream(self.device)
+            compute.wait_stream(self._up)
+            compute.wait_stream(self._down)
 
     def _gather(self, local: torch.Tensor | None, dest: torch.Tensor | None, ranges) -> None:
         """Shards -> prefill rank at their unit offsets (grouped point-to-point)."""
@@ -110,11 +146,21 @@ class EncodeStage:
                 w.wait()
 
     # ------------------------------------------------------------------ request
-    def process(self, tiles_host: torch.Tensor, rid: int = 0, tiles_dev: torch.Tensor | None = None
-                ) -> RequestResult:
+    def process(self, tiles_host: torch.Tensor, rid: int = 0, tiles_dev: torch.Tensor | None = None,
+                out_host: torch.Tensor | None = None) -> RequestResult:
         """Encode one request. ``tiles_host``: uint8 [n, S, S, C] (pinned for async copies);
         if ``tiles_dev`` (all tiles, already on this rank's device) is given, no H2D copy
-        is made. Returns the packed tokens on the prefill rank."""
+        is made. Returns the packed tokens on the prefill rank; with ``out_host`` (pinned,
+        [n, tokens, hidden] bf16) the prefill rank also reads them back asynchronously and
+        ``result.readback`` is the event to wait on."""
+        res = self._process(tiles_host, rid, tiles_dev)
+        if out_host is not None and res.tokens is not None:
+            res.readback = self._readback(res.tokens, out_host) if self._down is not None else None
+            if res.readback is None:
+                out_host.copy_(res.tokens)
+        return res
+
+    def _process(self, tiles_host, rid, tiles_dev) -> RequestResult:
         n = tiles_host.shape[0] if tiles_host is not None else tiles_dev.shape[0]
         is_sink = self.rank == self.prefill_rank
         res = RequestResult(rid=rid, n_tiles=n, encoded_tiles=0)
