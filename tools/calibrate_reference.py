@@ -1,0 +1,71 @@
+"""Feed measured B200 encode latencies back into the reference.
+
+Runs in the build container only (imports the reference from /root/reference; nothing
+on the product path or the GPU box reads it). Steps:
+  1. fit CostParams with the reference's own costs.calibrate (costs.py:146-176) from
+     profiles/r01/encode_latency_b200.json (tools/measure_encode_latency.py). The
+     prefill/decode samples are drawn from the shipped SYNTHETIC_COSTS polynomials
+     (presets.py:53-66), so only the encode coefficients change;
+  2. rerun the reference's irp_ablation (ablations.py:31-58) with the synthetic and with
+     the B200-calibrated MiniCPM encode costs;
+  3. write profiles/r01/calibration_b200.json.
+"""
+import json
+import sys
+from dataclasses import replace
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from disaggsim import ablations, costs, presets  # noqa: E402
+
+
+def poly_samples(p: costs.CostParams):
+    pre = [(t, costs.prefill_latency(p, t)) for t in (100, 700, 2000, 5000, 12000)]
+    dec = [((b, kv), costs.decode_step_latency(p, b, kv)) for b, kv in ((1, 500), (4, 3000), (16, 20000), (8, 100))]
+    return pre, dec
+
+
+def main():
+    meas = json.loads((ROOT / "profiles" / "r01" / "encode_latency_b200.json").read_text())
+    out = {"source": "profiles/r01/encode_latency_b200.json (" + meas["device"] + ")", "models": {}}
+    calibrated = {}
+    for name, m in meas["models"].items():
+        syn = presets.SYNTHETIC_COSTS[name]
+        pre, dec = poly_samples(syn)
+        enc = [(float(p), float(s)) for p, s in m["samples"]]
+        cal = costs.calibrate(enc, pre, dec)
+        calibrated[name] = cal
+        resid = max(abs(costs.encode_latency(cal, int(p)) - s) / s for p, s in enc)
+        out["models"][name] = {
+            "encoder": m["encoder"],
+            "synthetic": {"enc_base": syn.enc_base, "enc_per_patch": syn.enc_per_patch},
+            "b200_calibrated": {"enc_base": float(cal.enc_base), "enc_per_patch": float(cal.enc_per_patch)},
+            "fit_max_rel_residual": float(resid),
+            "encode_latency_10_tiles_s": {"synthetic": float(costs.encode_latency(syn, 10)),
+                                          "b200_calibrated": float(costs.encode_latency(cal, 10))},
+            "prefill_per_token_refit_rel_err": float(abs(cal.prefill_per_token - syn.prefill_per_token)
+                                                     / syn.prefill_per_token),
+        }
+    # irp_ablation reads SYNTHETIC_COSTS[MINICPM] at call time: run it as shipped, then with
+    # the calibrated entry swapped in (restored afterwards).
+    rows_syn = ablations.irp_ablation()
+    saved = presets.SYNTHETIC_COSTS[presets.MINICPM]
+    try:
+        presets.SYNTHETIC_COSTS[presets.MINICPM] = replace(saved, enc_base=calibrated[presets.MINICPM].enc_base,
+                                                           enc_per_patch=calibrated[presets.MINICPM].enc_per_patch)
+        rows_b200 = ablations.irp_ablation()
+    finally:
+        presets.SYNTHETIC_COSTS[presets.MINICPM] = saved
+    out["irp_ablation"] = {"synthetic_encode_costs": rows_syn, "b200_calibrated_encode_costs": rows_b200,
+                           "note": "reference ablations.irp_ablation (5-worker IRP encode instance vs width-1 "
+                                   "instances, MiniCPM 4K images, Poisson 0.125 req/s, 100 requests); prefill and "
+                                   "decode remain the reference's synthetic calibration"}
+    path = ROOT / "profiles" / "r01" / "calibration_b200.json"
+    path.write_text(json.dumps(out, indent=1))
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
