@@ -202,14 +202,18 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
  * out[(b*Tq + i)*ldo + h*Dv + d]. Dp in {64, 80, 128}. */
 /* Fused multi-head attention read in place from row-major projection outputs:
  *   Q: q[(b*Tq + t)*ldq + h*head_stride + d]  (EPD_ATTN_Q_SHARED: q[t*ldq + h*head_stride + d],
- *      one query set shared by every batch entry), K and V likewise with ldk / ldv and Tk,
+ *      one query set shared by every batch entry),
+ *   K, V: k[(b*Tk + t)*ldk + (h / (H/kv_heads))*head_stride + d] (grouped K/V heads; kv_heads
+ *      = 0 means H), V likewise with ldv,
  *   out[(b*Tq + t)*ldo + h*Dv + d], d < Dv.
- * Dp (64, 80 or 128) is the MMA width, Dv rounded up to 16; head_stride >= Dv. */
+ * EPD_ATTN_CAUSAL: query t sees keys <= t + (Tk - Tq). Dp (64, 80 or 128) is the MMA
+ * width, Dv rounded up to 16; head_stride >= Dv. */
 #define EPD_ATTN_Q_SHARED 1
+#define EPD_ATTN_CAUSAL 2
 epd_status_t epd_attention_bf16(const void* q, int32_t ldq, const void* k, int32_t ldk, const void* v,
-                                int32_t ldv, void* out, int32_t ldo, int32_t B, int32_t H, int32_t Tq,
-                                int32_t Tk, int32_t Dp, int32_t Dv, int32_t head_stride, int32_t flags,
-                                float scale, void* stream);
+                                int32_t ldv, void* out, int32_t ldo, int32_t B, int32_t H, int32_t kv_heads,
+                                int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv, int32_t head_stride,
+                                int32_t flags, float scale, void* stream);
 epd_status_t epd_layernorm_bf16(const void* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
                                 const void* beta, int32_t rows, int32_t D, float eps, void* stream);
 /* Residual-stream LayerNorm: fp32 rows in, bf16 rows out (the encoder's pre-attention /
@@ -221,6 +225,33 @@ epd_status_t epd_layernorm_f32_bf16(const float* in, int32_t ld_in, void* out, i
 epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t S, int32_t C, int32_t p, int32_t Kpad,
                              int32_t row_offset, int32_t rows_per_tile, const float* mean3, const float* std3,
                              void* out, void* stream);
+
+/* ------------------------------------------------------------------ prefill consumer
+ * the LLM prefill on the prefill GPU that consumes the packed MM
+ * tokens (the reference models it as costs.prefill_latency, costs.py:93-99, and
+ * _on_batch_end, engine.py:385-407). Decoder layers use epd_linear_* / epd_attention_bf16
+ * (causal, grouped KV heads); these are the remaining pieces. */
+/* fp32 rows -> RMSNorm (gamma) -> bf16 rows. */
+epd_status_t epd_rmsnorm_f32_bf16(const float* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
+                                  int32_t rows, int32_t D, float eps, void* stream);
+/* In-place rotary embedding (rotate-half) on heads [0, nheads) of width hd starting at column
+ * col0 of each bf16 row; position of row r = pos0 + r, angle = pos * theta^(-2i/hd). */
+epd_status_t epd_rope_bf16(void* x, int32_t ld, int32_t rows, int32_t col0, int32_t nheads, int32_t hd,
+                           int32_t pos0, float theta, void* stream);
+/* out[r][c] = silu(gu[r][c]) * gu[r][F + c]. */
+epd_status_t epd_silu_mul_bf16(const void* gu, int32_t ld_in, void* out, int32_t ld_out, int32_t rows, int32_t F,
+                               void* stream);
+/* Prefill K/V rows into the paged KV pool (handoff.py layout [segments][blocks][block_size*row_elems]):
+ * row t of K (src + t*ld_src) and V (src + t*ld_src + v_off) go to block block_ids[t/block_size],
+ * slot t%block_size of segments seg0 and seg0+1. */
+epd_status_t epd_kv_write_paged(const void* src, int32_t ld_src, int32_t v_off, int32_t rows, int32_t row_elems,
+                                const int32_t* block_ids, int32_t block_size, void* pool, int64_t seg_elems,
+                                int32_t seg0, void* stream);
+/* dst[r][:D] = float(src[index[r]][:D]). */
+epd_status_t epd_gather_rows_f32(const void* src, int32_t ld_src, const int32_t* index, int32_t rows, int32_t D,
+                                 float* dst, int32_t ld_dst, void* stream);
+/* *out = argmax(x[0:n]) (first index on ties). */
+epd_status_t epd_argmax_bf16(const void* x, int32_t n, int32_t* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -136,7 +136,7 @@ struct Cfg {
 // single 128-row tiles, so that round takes about half as long; a single tile past Tq
 // is an empty item (nq = 0) that every role skips without touching a barrier.
 struct AttnItem {
-  int b, h, q0, nq;
+  int b, h, q0, nq, nkb;  // nkb: 64-key blocks this item reads (causal items stop at their last row)
 };
 template <int NQ>
 EPD_DEVICE AttnItem attn_item(const AttnParams& p, int w, int nqp, int npairs_main) {
@@ -158,6 +158,12 @@ EPD_DEVICE AttnItem attn_item(const AttnParams& p, int w, int nqp, int npairs_ma
     it.q0 += half * 128;
     it.nq = p.Tq > it.q0 ? 1 : 0;
   }
+  int kend = p.Tk;
+  if (p.causal) {
+    const int last_row = min(p.Tq, it.q0 + it.nq * 128) - 1;
+    kend = min(p.Tk, last_row + 1 + (p.Tk - p.Tq));
+  }
+  it.nkb = (kend + 63) / 64;
   return it;
 }
 // Number of items and pairs kept whole for a persistent grid of G CTAs.
@@ -200,7 +206,6 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   const int nqp = (p.Tq + NQ * 128 - 1) / (NQ * 128);
   int pmain, nitems;
   attn_sched(nqp * p.H * p.B, gridDim.x, NQ, &pmain, &nitems);
-  const int nkb = (p.Tk + C::KB - 1) / C::KB;
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -253,14 +258,15 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         }
         if (x.nq == 0) continue;  // empty item: Q buffer handed over with no bytes, no K blocks
         const int krow0 = x.b * p.Tk;
-        for (int j = 0; j < nkb; ++j, ++kc) {
+        const int kvcol = (x.h / p.kv_group) * p.hs;
+        for (int j = 0; j < x.nkb; ++j, ++kc) {
           const int s = kc % C::KS;
           mbar_wait(&k_empty[s], ((kc / C::KS) & 1) ^ 1);
           mbar_arrive_expect_tx(&k_full[s], C::K_BYTES);
           uint8_t* kd = smem + C::OFF_K + s * C::K_AL;
           for (int a = 0; a < C::MAIN; ++a)
-            tma_load_2d(kd + a * C::K_ATOM, &tmK, &k_full[s], hcol + a * 64, krow0 + j * C::KB);
-          if (C::TAIL) tma_load_2d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], hcol + C::MAIN * 64, krow0 + j * C::KB);
+            tma_load_2d(kd + a * C::K_ATOM, &tmK, &k_full[s], kvcol + a * 64, krow0 + j * C::KB);
+          if (C::TAIL) tma_load_2d(kd + C::MAIN * C::K_ATOM, &tmKt, &k_full[s], kvcol + C::MAIN * 64, krow0 + j * C::KB);
         }
       }
     } else if (lane == 1) {
@@ -268,8 +274,8 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
       for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
         const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
         if (x.nq == 0) continue;
-        const int hcol = x.h * p.hs, krow0 = x.b * p.Tk;
-        for (int j = 0; j < nkb; ++j, ++vc) {
+        const int hcol = (x.h / p.kv_group) * p.hs, krow0 = x.b * p.Tk;
+        for (int j = 0; j < x.nkb; ++j, ++vc) {
           const int s = vc % C::KVS;
           mbar_wait(&v_empty[s], ((vc / C::KVS) & 1) ^ 1);
           mbar_arrive_expect_tx(&v_full[s], C::V_BYTES);
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         }
         tc_fence_after();
         // two blocks of S in flight per query tile: softmax(j) overlaps S(j+1)
+        const int nkb = x.nkb;
         for (int j = 0; j < 2 && j < nkb; ++j) {
           const int ks = (kc + j) % C::KS;
           mbar_wait(&k_full[ks], ((kc + j) / C::KS) & 1);
@@ -402,10 +409,13 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
       const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
       float l = 0.f;
+      const int nkb = x.nkb;
+      // keys this thread's query row may see (causal: up to its own position)
+      const int klim = p.causal ? min(p.Tk, x.q0 + g * 128 + r + 1 + (p.Tk - p.Tq)) : p.Tk;
       if (g < x.nq) {
         float m_used = -INFINITY;
         for (int j = 0; j < nkb; ++j) {
-          const int kvalid = p.Tk - j * C::KB;
+          const int kvalid = klim - j * C::KB;
           mbar_wait(&s_full[2 * g + (j & 1)], (sf_ph >> (j & 1)) & 1);
           sf_ph ^= 1u << (j & 1);
           tc_fence_after();
@@ -529,14 +539,15 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
   // 2-D maps over each section (H heads x hs columns); rows = tokens of all images. Boxes
   // that run past the last head or the last row are zero-filled by the TMA.
   const uint64_t width = (uint64_t)p.H * p.hs;
+  const uint64_t kv_width = (uint64_t)(p.H / p.kv_group) * p.hs;
   const uint64_t qrows = p.q_shared ? p.Tq : (uint64_t)p.B * p.Tq;
   const uint64_t krows = (uint64_t)p.B * p.Tk;
   CUtensorMap mq, mqt, mk, mkt, mv;
   int rc = make_tmap_2d(&mq, p.q, width, qrows, (uint64_t)p.ldq * 2, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
   if (!rc) rc = make_tmap_2d(&mqt, p.q, width, qrows, (uint64_t)p.ldq * 2, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
-  if (!rc) rc = make_tmap_2d(&mk, p.k, width, krows, (uint64_t)p.ldk * 2, 64, C::KB, CU_TENSOR_MAP_SWIZZLE_128B);
-  if (!rc) rc = make_tmap_2d(&mkt, p.k, width, krows, (uint64_t)p.ldk * 2, 16, C::KB, CU_TENSOR_MAP_SWIZZLE_32B);
-  if (!rc) rc = make_tmap_2d(&mv, p.v, width, krows, (uint64_t)p.ldv * 2, 16, C::KB, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_2d(&mk, p.k, kv_width, krows, (uint64_t)p.ldk * 2, 64, C::KB, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc) rc = make_tmap_2d(&mkt, p.k, kv_width, krows, (uint64_t)p.ldk * 2, 16, C::KB, CU_TENSOR_MAP_SWIZZLE_32B);
+  if (!rc) rc = make_tmap_2d(&mv, p.v, kv_width, krows, (uint64_t)p.ldv * 2, 16, C::KB, CU_TENSOR_MAP_SWIZZLE_32B);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
@@ -561,6 +572,8 @@ int attention_bf16(const AttnParams& p, cudaStream_t stream) {
   if (p.B <= 0 || p.H <= 0 || p.Tq <= 0 || p.Tk <= 0 || p.Dv <= 0 || p.Dv > p.Dp) return 1001;
   if ((p.ldo % 8) != 0 || (p.Dv % 8) != 0) return 1002;
   if (p.hs < p.Dv || p.ldq % 8 || p.ldk % 8 || p.ldv % 8 || p.hs % 8) return 1002;
+  if (p.kv_group < 1 || p.H % p.kv_group) return 1001;
+  if (p.causal && (p.Tk < p.Tq || p.q_shared)) return 1001;
   if ((reinterpret_cast<uintptr_t>(p.q) | reinterpret_cast<uintptr_t>(p.k) | reinterpret_cast<uintptr_t>(p.v)) & 15)
     return 1003;
   const bool two = p.Tq > 128;

@@ -425,9 +425,10 @@ epd_status_t epd_linear_heads_bf16(const void* A, int32_t lda, const void* W, in
 }
 
 epd_status_t epd_attention_bf16(const void* q, int32_t ldq, const void* k, int32_t ldk, const void* v,
-                                int32_t ldv, void* out, int32_t ldo, int32_t B, int32_t H, int32_t Tq,
-                                int32_t Tk, int32_t Dp, int32_t Dv, int32_t head_stride, int32_t flags,
-                                float scale, void* stream) {
+                                int32_t ldv, void* out, int32_t ldo, int32_t B, int32_t H, int32_t kv_heads,
+                                int32_t Tq, int32_t Tk, int32_t Dp, int32_t Dv, int32_t head_stride,
+                                int32_t flags, float scale, void* stream) {
+  if (kv_heads < 0 || (kv_heads > 0 && (H % kv_heads))) return fail(EPD_ERR_VALUE, "attention: H % kv_heads != 0");
   epd::AttnParams p;
   p.q = reinterpret_cast<const epd::bf16*>(q);
   p.k = reinterpret_cast<const epd::bf16*>(k);
@@ -435,7 +436,9 @@ epd_status_t epd_attention_bf16(const void* q, int32_t ldq, const void* k, int32
   p.out = reinterpret_cast<epd::bf16*>(out);
   p.ldq = ldq; p.ldk = ldk; p.ldv = ldv; p.hs = head_stride;
   p.B = B; p.H = H; p.Tq = Tq; p.Tk = Tk; p.Dp = Dp; p.Dv = Dv; p.ldo = ldo;
+  p.kv_group = kv_heads > 0 ? H / kv_heads : 1;
   p.q_shared = (flags & EPD_ATTN_Q_SHARED) != 0;
+  p.causal = (flags & EPD_ATTN_CAUSAL) != 0;
   p.scale = scale;
   return cuda_status(epd::attention_bf16(p, S(stream)), "attention_bf16");
 }
@@ -466,5 +469,49 @@ epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t Sz, int32_
                                       reinterpret_cast<epd::bf16*>(out), S(stream)),
                      "patchify_u8");
 }
+
+// ------------------------------------------------------------------ prefill consumer
+
+epd_status_t epd_rmsnorm_f32_bf16(const float* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
+                                  int32_t rows, int32_t D, float eps, void* stream) {
+  return cuda_status(epd::rmsnorm_f32(in, ld_in, reinterpret_cast<epd::bf16*>(out), ld_out,
+                                      reinterpret_cast<const epd::bf16*>(gamma), rows, D, eps, S(stream)),
+                     "rmsnorm_f32_bf16");
+}
+
+epd_status_t epd_rope_bf16(void* x, int32_t ld, int32_t rows, int32_t col0, int32_t nheads, int32_t hd,
+                           int32_t pos0, float theta, void* stream) {
+  return cuda_status(epd::rope_bf16(reinterpret_cast<epd::bf16*>(x), ld, rows, col0, nheads, hd, pos0, theta,
+                                    S(stream)),
+                     "rope_bf16");
+}
+
+epd_status_t epd_silu_mul_bf16(const void* gu, int32_t ld_in, void* out, int32_t ld_out, int32_t rows, int32_t F,
+                               void* stream) {
+  return cuda_status(epd::silu_mul_bf16(reinterpret_cast<const epd::bf16*>(gu), ld_in,
+                                        reinterpret_cast<epd::bf16*>(out), ld_out, rows, F, S(stream)),
+                     "silu_mul_bf16");
+}
+
+epd_status_t epd_kv_write_paged(const void* src, int32_t ld_src, int32_t v_off, int32_t rows, int32_t row_elems,
+                                const int32_t* block_ids, int32_t block_size, void* pool, int64_t seg_elems,
+                                int32_t seg0, void* stream) {
+  return cuda_status(epd::kv_write_paged(reinterpret_cast<const epd::bf16*>(src), ld_src, v_off, rows, row_elems,
+                                         block_ids, block_size, reinterpret_cast<epd::bf16*>(pool),
+                                         (size_t)seg_elems, seg0, S(stream)),
+                     "kv_write_paged");
+}
+
+epd_status_t epd_gather_rows_f32(const void* src, int32_t ld_src, const int32_t* index, int32_t rows, int32_t D,
+                                 float* dst, int32_t ld_dst, void* stream) {
+  return cuda_status(epd::gather_rows_f32(reinterpret_cast<const epd::bf16*>(src), ld_src, index, rows, D, dst,
+                                          ld_dst, S(stream)),
+                     "gather_rows_f32");
+}
+
+epd_status_t epd_argmax_bf16(const void* x, int32_t n, int32_t* out, void* stream) {
+  return cuda_status(epd::argmax_bf16(reinterpret_cast<const epd::bf16*>(x), n, out, S(stream)), "argmax_bf16");
+}
+
 
 }  // extern "C"

@@ -47,8 +47,8 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
 // Fused multi-head attention O = softmax(Q K^T * scale) V on tcgen05, reading Q, K, V
 // straight from row-major projection outputs (no per-head relayout):
 //   Q : q[(b * Tq + t) * ldq + h * hs + d]      (q_shared: q[t * ldq + h * hs + d])
-//   K : k[(b * Tk + t) * ldk + h * hs + d]
-//   V : v[(b * Tk + t) * ldv + h * hs + d]        for d < Dv
+//   K : k[(b * Tk + t) * ldk + (h / kv_group) * hs + d]
+//   V : v[(b * Tk + t) * ldv + (h / kv_group) * hs + d]        for d < Dv
 //   O : out[(b * Tq + t) * ldo + h * Dv + d]      for d < Dv
 // hs = column stride between heads (Dv for packed heads). The MMAs run Dp = Dv rounded up
 // to a multiple of 16 (64, 80 or 128) dims: dims beyond Dv read the neighbouring head's
@@ -64,6 +64,8 @@ struct AttnParams {
   int B = 0, H = 0, Tq = 0, Tk = 0, Dp = 0, Dv = 0, ldo = 0;
   int q_shared = 0;
   float scale = 1.f;
+  int causal = 0;    // query row t (of Tq) sees keys <= t + (Tk - Tq)
+  int kv_group = 1;  // query heads per K/V head (grouped-query attention): K/V head = h / kv_group
 };
 int attention_bf16(const AttnParams& p, cudaStream_t stream);
 
@@ -94,6 +96,17 @@ int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int 
 // Gather equal-sized byte records: dst[i] = src_base[index[i]] (record = bytes).
 int gather_records(const void* src_base, const int32_t* index, int n, size_t bytes, void* dst,
                    cudaStream_t stream);
+
+// ---- prefill consumer (llm.cu): the LLM layers around the GEMM / attention kernels.
+int rmsnorm_f32(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma, int rows, int D, float eps,
+                cudaStream_t s);
+int rope_bf16(bf16* x, int ld, int rows, int col0, int nheads, int hd, int pos0, float theta, cudaStream_t s);
+int silu_mul_bf16(const bf16* gu, int ld_in, bf16* out, int ld_out, int rows, int F, cudaStream_t s);
+int kv_write_paged(const bf16* src, int ld_src, int v_off, int rows, int row_elems, const int32_t* block_ids,
+                   int block_size, bf16* pool, size_t seg_elems, int seg0, cudaStream_t s);
+int gather_rows_f32(const bf16* src, int ld_src, const int32_t* index, int rows, int D, float* dst, int ld_dst,
+                    cudaStream_t s);
+int argmax_bf16(const bf16* x, int n, int32_t* out, cudaStream_t s);
 
 // ---- fp32 check mode (check_f32.cu): CUDA-core fp32 twins of the kernels above.
 // Epilogue: x = act(acc + bias[n]) * lscale[n] + resid[row % r_mod][n]; ROWS writes

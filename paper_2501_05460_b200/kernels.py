@@ -78,12 +78,13 @@ def linear_heads(a: torch.Tensor, w: torch.Tensor, H: int, Dp: int, T: int, sect
 
 def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, B: int, H: int, Tq: int, Tk: int,
               Dv: int, scale: float, head_stride: int | None = None, q_shared: bool = False,
-              out: torch.Tensor | None = None) -> torch.Tensor:
-    """Fused MHA read in place from row-major projections.
+              out: torch.Tensor | None = None, kv_heads: int | None = None, causal: bool = False) -> torch.Tensor:
+    """Fused MHA / GQA read in place from row-major projections.
 
     q: [B*Tq (or Tq if q_shared), >= H*head_stride] (a column slice of a wider matrix is fine),
-    k, v: [B*Tk, ...]; head h occupies columns [h*head_stride, h*head_stride + Dv).
-    Returns out [B*Tq, H*Dv].
+    k, v: [B*Tk, ...] with ``kv_heads`` heads (query head h uses K/V head h // (H // kv_heads));
+    head h occupies columns [h*head_stride, h*head_stride + Dv). ``causal``: query t sees keys
+    <= t + (Tk - Tq). Returns out [B*Tq, H*Dv].
     """
     _need_cuda(q, k, v, out)
     hs = head_stride or Dv
@@ -93,8 +94,9 @@ def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, B: int, H: int,
             raise ValueError("q, k, v must be 2-D row-major (unit column stride)")
     if out is None:
         out = torch.empty(B * Tq, H * Dv, dtype=torch.bfloat16, device=q.device)
+    flags = (1 if q_shared else 0) | (2 if causal else 0)
     call("epd_attention_bf16", q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(), v.stride(0),
-         out.data_ptr(), out.stride(0), B, H, Tq, Tk, Dp, Dv, hs, int(q_shared), float(scale), _stream(q))
+         out.data_ptr(), out.stride(0), B, H, kv_heads or 0, Tq, Tk, Dp, Dv, hs, flags, float(scale), _stream(q))
     return out
 
 
@@ -136,4 +138,59 @@ def patchify(tiles: torch.Tensor, patch: int, kpad: int, mean, std, row_offset: 
     s = (ctypes.c_float * 3)(*std)
     call("epd_patchify_u8", tiles.data_ptr(), n, S, Cc, patch, kpad, row_offset, rpt,
          ctypes.cast(m, ctypes.c_void_p), ctypes.cast(s, ctypes.c_void_p), out.data_ptr(), _stream(tiles))
+    return out
+
+
+# ---- prefill consumer (llm.cu)
+
+def rmsnorm_f32(x: torch.Tensor, gamma: torch.Tensor, eps: float, out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 rows -> RMSNorm(gamma) -> bf16 rows."""
+    _need_cuda(x, gamma, out)
+    rows, D = x.shape
+    if out is None:
+        out = torch.empty(rows, D, dtype=torch.bfloat16, device=x.device)
+    call("epd_rmsnorm_f32_bf16", x.data_ptr(), x.stride(0), out.data_ptr(), out.stride(0), gamma.data_ptr(), rows, D,
+         float(eps), _stream(x))
+    return out
+
+
+def rope_(x: torch.Tensor, col0: int, nheads: int, head_dim: int, theta: float, pos0: int = 0) -> torch.Tensor:
+    """In-place rotary embedding (rotate-half) on heads [0, nheads) starting at column col0."""
+    _need_cuda(x)
+    call("epd_rope_bf16", x.data_ptr(), x.stride(0), x.shape[0], col0, nheads, head_dim, pos0, float(theta),
+         _stream(x))
+    return x
+
+
+def silu_mul(gu: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """[rows, 2F] (gate | up) -> silu(gate) * up [rows, F]."""
+    _need_cuda(gu, out)
+    rows, F2 = gu.shape
+    if out is None:
+        out = torch.empty(rows, F2 // 2, dtype=torch.bfloat16, device=gu.device)
+    call("epd_silu_mul_bf16", gu.data_ptr(), gu.stride(0), out.data_ptr(), out.stride(0), rows, F2 // 2, _stream(gu))
+    return out
+
+
+def kv_write_paged(k: torch.Tensor, v_off: int, row_elems: int, block_ids: torch.Tensor, block_size: int,
+                   pool: torch.Tensor, layer: int) -> None:
+    """Rows of K (k) and V (k + v_off columns) into the paged pool [2L][blocks][block_size*row_elems]."""
+    _need_cuda(k, block_ids, pool)
+    call("epd_kv_write_paged", k.data_ptr(), k.stride(0), v_off, k.shape[0], row_elems, block_ids.data_ptr(),
+         block_size, pool.data_ptr(), pool.shape[1] * pool.shape[2], 2 * layer, _stream(k))
+
+
+def gather_rows_f32(src: torch.Tensor, index: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """out[r] = float(src[index[r]])."""
+    _need_cuda(src, index, out)
+    call("epd_gather_rows_f32", src.data_ptr(), src.stride(0), index.data_ptr(), index.numel(), out.shape[1],
+         out.data_ptr(), out.stride(0), _stream(src))
+    return out
+
+
+def argmax(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    _need_cuda(x, out)
+    if out is None:
+        out = torch.empty(1, dtype=torch.int32, device=x.device)
+    call("epd_argmax_bf16", x.data_ptr(), x.numel(), out.data_ptr(), _stream(x))
     return out

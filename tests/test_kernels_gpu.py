@@ -88,15 +88,24 @@ def test_linear_acc_f32(cuda, M, N, K, bn, ls):
     assert relerr(h, ref) <= 2e-3
 
 
-def _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale):
+def _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale, kv_heads=None, causal=False):
     """fp32 reference on the row-major layout (head h = columns [h*hs, h*hs + Dv))."""
-    def heads(x, T, nb):
-        return x.float().reshape(nb, T, -1)[..., :H * hs].reshape(nb, T, H, hs)[..., :Dv].permute(0, 2, 1, 3)
-    qf = heads(q, Tq, 1 if q_shared else B)
+    Hk = kv_heads or H
+
+    def heads(x, T, nb, nh):
+        return x.float().reshape(nb, T, -1)[..., :nh * hs].reshape(nb, T, nh, hs)[..., :Dv].permute(0, 2, 1, 3)
+    qf = heads(q, Tq, 1 if q_shared else B, H)
     if q_shared:
         qf = qf.expand(B, H, Tq, Dv)
-    kf, vf = heads(k, Tk, B), heads(v, Tk, B)
-    p = torch.softmax(qf @ kf.transpose(-1, -2) * scale, dim=-1)
+    kf, vf = heads(k, Tk, B, Hk), heads(v, Tk, B, Hk)
+    if Hk != H:
+        kf = kf.repeat_interleave(H // Hk, dim=1)
+        vf = vf.repeat_interleave(H // Hk, dim=1)
+    sc = qf @ kf.transpose(-1, -2) * scale
+    if causal:
+        mask = torch.ones(Tq, Tk, dtype=torch.bool, device=sc.device).tril(Tk - Tq)
+        sc = sc.masked_fill(~mask, float("-inf"))
+    p = torch.softmax(sc, dim=-1)
     return (p @ vf).permute(0, 2, 1, 3).reshape(B * Tq, H * Dv)
 
 
@@ -121,6 +130,25 @@ def test_attention(cuda, B, H, Tq, Tk, Dv, hs, q_shared, qscale):
     y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, head_stride=hs, q_shared=q_shared)
     torch.cuda.synchronize()
     assert relerr(y, _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale)) <= TOL
+
+
+@pytest.mark.parametrize("B,H,Hk,Tq,Tk,Dv", [
+    (1, 28, 4, 662, 662, 128),   # Qwen2-7B prefill (MiniCPM-V 2.6 LLM): 640 MM + 22 text tokens
+    (2, 8, 2, 300, 300, 64),     # two sequences, paired query tiles
+    (1, 4, 4, 129, 200, 64),     # causal with a key prefix (Tk > Tq)
+    (1, 32, 8, 64, 64, 128),     # InternLM2-shaped heads, one short tile
+])
+def test_attention_causal_gqa(cuda, B, H, Hk, Tq, Tk, Dv):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(B + H + Tq + Tk)
+    q = _bf(B * Tq, H * Dv, gen=g)
+    kv = _bf(B * Tk, 2 * Hk * Dv, gen=g)
+    k, v = kv[:, :Hk * Dv], kv[:, Hk * Dv:]
+    scale = 1.0 / math.sqrt(Dv)
+    y = kernels.attention(q, k, v, B, H, Tq, Tk, Dv, scale, kv_heads=Hk, causal=True)
+    torch.cuda.synchronize()
+    ref = _attn_ref(q, k, v, B, H, Tq, Tk, Dv, Dv, False, scale, kv_heads=Hk, causal=True)
+    assert relerr(y, ref) <= TOL
 
 
 def test_attention_rejects_bad_layouts(cuda):
@@ -156,6 +184,64 @@ def test_layernorm_f32_input(cuda, rows, D):
     torch.cuda.synchronize()
     ref = torch.nn.functional.layer_norm(x, (D,), gm.float(), bt.float(), 1e-6)
     assert relerr(y, ref) <= TOL
+
+
+def test_rmsnorm_rope_silu(cuda):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(5)
+    T, D = 662, 3584
+    x = torch.randn(T, D, device=cuda, generator=g) * 3.0
+    gm = _bf(D, gen=g)
+    y = kernels.rmsnorm_f32(x, gm, 1e-6)
+    ref = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-6) * gm.float()
+    assert relerr(y, ref) <= TOL
+    # rope on the Q and K sections of a fused row, positions 5.., rotate-half convention
+    Hq, Hk, hd, theta = 4, 2, 128, 1e6
+    qkv = _bf(T, (Hq + 2 * Hk) * hd, gen=g)
+    ref_q = qkv.float().clone()
+    kernels.rope_(qkv, 0, Hq + Hk, hd, theta, pos0=5)
+    pos = torch.arange(5, 5 + T, device=cuda, dtype=torch.float64)[:, None]
+    inv = theta ** (-torch.arange(0, hd, 2, device=cuda, dtype=torch.float64) / hd)
+    ang = pos * inv[None, :]
+    cos, sin = ang.cos().float(), ang.sin().float()
+    r = ref_q[:, :(Hq + Hk) * hd].reshape(T, Hq + Hk, hd)
+    a, b = r[..., :hd // 2], r[..., hd // 2:]
+    rot = torch.cat([a * cos[:, None] - b * sin[:, None], b * cos[:, None] + a * sin[:, None]], -1)
+    assert relerr(qkv[:, :(Hq + Hk) * hd].reshape(T, Hq + Hk, hd), rot) <= TOL
+    assert torch.equal(qkv[:, (Hq + Hk) * hd:].float(), ref_q[:, (Hq + Hk) * hd:])  # V untouched
+    # swiglu
+    F = 1024
+    gu = _bf(T, 2 * F, scale=2.0, gen=g)
+    y = kernels.silu_mul(gu)
+    ref = torch.nn.functional.silu(gu[:, :F].float()) * gu[:, F:].float()
+    assert relerr(y, ref) <= TOL
+
+
+def test_kv_write_gather_argmax(cuda):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(6)
+    T, Hq, Hk, hd, L, bs = 70, 4, 2, 64, 3, 16
+    qkv = _bf(T, (Hq + 2 * Hk) * hd, gen=g)
+    nblk = -(-T // bs)
+    ids = torch.tensor([7, 2, 9, 0, 5][:nblk], dtype=torch.int32, device=cuda)
+    pool = torch.zeros(2 * L, 12, bs * Hk * hd, dtype=torch.bfloat16, device=cuda)
+    kernels.kv_write_paged(qkv[:, Hq * hd:], Hk * hd, Hk * hd, ids, bs, pool, layer=1)
+    torch.cuda.synchronize()
+    for t in range(T):
+        blk, slot = int(ids[t // bs]), t % bs
+        kk = pool[2, blk, slot * Hk * hd:(slot + 1) * Hk * hd]
+        vv = pool[3, blk, slot * Hk * hd:(slot + 1) * Hk * hd]
+        assert torch.equal(kk, qkv[t, Hq * hd:(Hq + Hk) * hd]) and torch.equal(vv, qkv[t, (Hq + Hk) * hd:])
+    assert pool[0].abs().sum() == 0 and pool[4].abs().sum() == 0
+    src = _bf(50, 256, gen=g)
+    idx = torch.tensor([3, 0, 49, 3], dtype=torch.int32, device=cuda)
+    out = torch.empty(4, 256, device=cuda)
+    kernels.gather_rows_f32(src, idx, out)
+    assert torch.equal(out, src[idx.long()].float())
+    x = _bf(152064, gen=g)
+    x[99999] = 50.0
+    x[123] = 50.0
+    assert int(kernels.argmax(x)) == 123
 
 
 def test_patchify(cuda):
