@@ -116,3 +116,16 @@ def test_product_refuses_cpu_tensors():
     from paper_2501_05460_b200 import kernels
     with pytest.raises(ValueError):
         kernels.linear(torch.zeros(4, 8, dtype=torch.bfloat16), torch.zeros(8, 8, dtype=torch.bfloat16))
+
+
+def test_llm_configs_match_reference_catalog():
+    """The prefill consumer's LLM shapes agree with the reference catalog (models.cfg): layers,
+    KV heads, head dim, hidden -> the same KV bytes per token the P->D handoff moves."""
+    from paper_2501_05460_b200.prefill import INTERNLM25_7B, QWEN2_7B
+    for cfg in (QWEN2_7B, INTERNLM25_7B):
+        g = cfg.geometry
+        assert (cfg.layers, cfg.kv_heads, cfg.head_dim, cfg.hidden) == (g.num_layers, g.kv_heads, g.head_dim,
+                                                                         g.hidden_dim)
+        assert cfg.q_heads * cfg.head_dim == cfg.hidden
+        assert 2 * cfg.layers * cfg.kv_heads * cfg.head_dim * 2 == g.kv_bytes_per_token()
+    assert QWEN2_7B.geometry.kv_bytes_per_token() == 57344 and INTERNLM25_7B.geometry.kv_bytes_per_token() == 131072
