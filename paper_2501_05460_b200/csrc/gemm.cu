@@ -543,7 +543,10 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
   if (N % 8 != 0 || (lda * 2) % 16 != 0 || (ldb * 2) % 16 != 0) return 1002;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return 1003;
   // CTA pairs (256-row tiles, half of B per SM) for large M; single CTAs for small M.
-  int cg = g_cta_group_policy ? g_cta_group_policy : (M >= 2048 ? 2 : 1);
+  // CTA pairs (256-row tiles, each SM streaming half of B) once there are two 128-row M
+  // tiles; single CTAs for M <= 256 (LM head, resampler query precompute). Pairs compute
+  // the same K-ordered sums, so the choice never changes results.
+  int cg = g_cta_group_policy ? g_cta_group_policy : (M > 256 ? 2 : 1);
   int bn = bn_hint;
   if (bn == 0) {
     // Wide tiles amortise the epilogue and B-operand traffic best; step down only
