@@ -83,6 +83,11 @@ class EncodeStage:
         # behind one another).
         self._up = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
         self._down = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
+        # Double-buffered device rings for uploads and packed tokens (no per-request
+        # allocation: caching-allocator churn across three streams can trigger synchronising
+        # frees). A ring slot is reused two requests later, after the event that marks its
+        # last consumer (the encode for inputs, the readback for packed tokens).
+        self._rings: dict = {}
 
     # ------------------------------------------------------------------ helpers
     def _tokens_shape(self, n: int):
@@ -91,8 +96,23 @@ class EncodeStage:
     def _buffer(self, n: int) -> torch.Tensor:
         return torch.empty(self._tokens_shape(n), dtype=torch.bfloat16, device=self.device)
 
-    def _upload(self, tiles_host: torch.Tensor, idx) -> torch.Tensor:
-        """Pinned host tiles -> device on the upload stream; the compute stream waits for it."""
+    def _slot(self, key, shape, dtype):
+        # one ring per (use, shape); rings are never dropped (a dropped buffer may still be
+        # read by queued work), so memory grows only with the number of distinct shapes
+        key = (key, tuple(shape), dtype)
+        r = self._rings.get(key)
+        if r is None:
+            r = {"bufs": [torch.empty(shape, dtype=dtype, device=self.device) for _ in range(2)],
+                 "free": [None, None], "i": 0}
+            self._rings[key] = r
+        k = r["i"]
+        r["i"] ^= 1
+        return r, k
+
+    def _upload(self, tiles_host: torch.Tensor, idx):
+        """Pinned host tiles -> device on the upload stream (into a ring slot); the compute
+        stream waits for it. Returns (tensor, release) -- call release() once the compute
+        stream has queued the last read of the tensor."""
         if isinstance(idx, slice):
             host = tiles_host[idx]
         elif idx is None:
@@ -100,16 +120,33 @@ class EncodeStage:
         else:
             host = tiles_host.index_select(0, torch.as_tensor(idx, dtype=torch.int64))
         if self._up is None:
-            return host.to(self.device, non_blocking=True)
+            return host.to(self.device, non_blocking=True), (lambda: None)
         compute = torch.cuda.current_stream(self.device)
-        self._up.wait_stream(compute)  # the buffer the allocator hands out may still be read there
+        r, k = self._slot("in", host.shape, host.dtype)
+        buf = r["bufs"][k]
+        if r["free"][k] is not None:
+            self._up.wait_event(r["free"][k])
         with torch.cuda.stream(self._up):
-            dev = host.to(self.device, non_blocking=True)
+            buf.copy_(host, non_blocking=True)
         compute.wait_stream(self._up)
-        dev.record_stream(compute)
-        return dev
 
-    def _readback(self, tokens: torch.Tensor, out_host: torch.Tensor) -> torch.cuda.Event:
+        def release():
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            r["free"][k] = ev
+        return buf, release
+
+    def _packed(self, n: int):
+        """Packed-token buffer for n tiles from the ring (waits for its previous readback)."""
+        if self._up is None:
+            return self._buffer(n), None
+        r, k = self._slot("out", self._tokens_shape(n), torch.bfloat16)
+        if r["free"][k] is not None:
+            torch.cuda.current_stream(self.device).wait_event(r["free"][k])
+            r["free"][k] = None
+        return r["bufs"][k], (r, k)
+
+    def _readback(self, tokens: torch.Tensor, out_host: torch.Tensor, slot=None) -> torch.cuda.Event:
         """Packed tokens -> pinned host buffer on the download stream, after the compute
         stream's work so far; returns the event that marks the copy done."""
         compute = torch.cuda.current_stream(self.device)
@@ -118,7 +155,11 @@ class EncodeStage:
             out_host.copy_(tokens, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self._down)
-        tokens.record_stream(self._down)
+        if slot is not None:
+            r, k = slot
+            r["free"][k] = ev  # the slot's next encode waits for this readback
+        else:
+            tokens.record_stream(self._down)
         return ev
 
     def join(self) -> None:
@@ -155,7 +196,8 @@ class EncodeStage:
         ``result.readback`` is the event to wait on."""
         res = self._process(tiles_host, rid, tiles_dev)
         if out_host is not None and res.tokens is not None:
-            res.readback = self._readback(res.tokens, out_host) if self._down is not None else None
+            slot = getattr(res, "_slot", None)
+            res.readback = self._readback(res.tokens, out_host, slot) if self._down is not None else None
             if res.readback is None:
                 out_host.copy_(res.tokens)
         return res
@@ -169,14 +211,20 @@ class EncodeStage:
         if self.cache is None:
             ranges = shard_ranges(n, self.world)
             first, count = ranges[self.rank]
-            packed = self._buffer(n) if is_sink else None
+            packed, slot = self._packed(n) if is_sink else (None, None)
             local = None
             if count > 0:
-                src = (tiles_dev[first:first + count] if tiles_dev is not None
-                       else self._upload(tiles_host, slice(first, first + count)))
+                release = None
+                if tiles_dev is not None:
+                    src = tiles_dev[first:first + count]
+                else:
+                    src, release = self._upload(tiles_host, slice(first, first + count))
                 local = packed[first:first + count] if is_sink else self._buffer(count)
                 self.enc.encode(src.contiguous(), local)
+                if release is not None:
+                    release()
             self._gather(local, packed, ranges)
+            res._slot = slot
             res.encoded_tiles = count
             res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
             res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != self.prefill_rank)
@@ -186,8 +234,12 @@ class EncodeStage:
         # ---- cached path (cache on the prefill rank)
         from .mmcache import hash_tiles
         plan = None
+        release_all = release_mine = None
         if is_sink:
-            all_dev = tiles_dev if tiles_dev is not None else self._upload(tiles_host, None)
+            if tiles_dev is not None:
+                all_dev = tiles_dev
+            else:
+                all_dev, release_all = self._upload(tiles_host, None)
             keys = hash_tiles(all_dev.contiguous())
             plan = self.cache.plan(keys)
             miss = torch.as_tensor(plan.miss_tiles, dtype=torch.int64)
@@ -210,10 +262,15 @@ class EncodeStage:
                 src = all_dev.index_select(0, my.to(self.device))
                 local = staging[first:first + count]
             else:
-                src = (tiles_dev.index_select(0, my.to(self.device)) if tiles_dev is not None
-                       else self._upload(tiles_host, my))
+                if tiles_dev is not None:
+                    src = tiles_dev.index_select(0, my.to(self.device))
+                else:
+                    src, release_mine = self._upload(tiles_host, my)
                 local = self._buffer(count)
             self.enc.encode(src.contiguous(), local)
+        for release in (release_all, release_mine):
+            if release is not None:
+                release()  # the compute stream has queued its last read of the uploaded tiles
         self._gather(local, staging, ranges)
         res.encoded_tiles = count
         res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
