@@ -151,6 +151,43 @@ EPD_DEVICE void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int 
                : "memory");
 }
 
+// Persistent tile schedule. Tiles are (M tile, N offset, width): full BN-wide tiles first
+// (M-major, so consecutive tiles share A rows), then half-width tiles -- the last f_keep..
+// full tiles split in two, so the final round holds only halves, and the ragged last N
+// tile of every M row when its valid width fits in BN/2 (half-width MMAs, no wasted N).
+// Decoded arithmetically by every role (no tile table: graph capture safe).
+struct TileSched {
+  int nf;       // full-width N tiles per M row
+  int ragged;   // 1: one extra half-width N tile per M row at nf * BN
+  int f_keep;   // full tiles kept whole (the rest of the num_m * nf are split)
+  int f_total;  // num_m * nf
+  int total;    // f_keep + 2 (f_total - f_keep) + num_m * ragged
+};
+struct TileAt {
+  int mt, n0, w;
+};
+EPD_DEVICE TileAt tile_at(const TileSched& s, int t, int BN) {
+  TileAt x;
+  if (t < s.f_keep) {
+    x.mt = t / s.nf;
+    x.n0 = (t - x.mt * s.nf) * BN;
+    x.w = BN;
+    return x;
+  }
+  int k = t - s.f_keep;
+  const int nsplit = s.f_total - s.f_keep;
+  if (k < 2 * nsplit) {
+    const int ft = s.f_keep + (k >> 1);
+    x.mt = ft / s.nf;
+    x.n0 = (ft - x.mt * s.nf) * BN + (k & 1) * (BN / 2);
+  } else {
+    x.mt = k - 2 * nsplit;
+    x.n0 = s.nf * BN;
+  }
+  x.w = BN / 2;
+  return x;
+}
+
 // CG = 1: one CTA per 128 x BN tile. CG = 2: a CTA pair (cluster of 2) computes a
 // 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA loads its 128 rows of A
 // and half of B, the leader issues M=256 MMAs, both CTAs drain their own TMEM.
@@ -158,7 +195,8 @@ template <int BN, int KIND, int CG>
 __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
-                     const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep) {
+                     const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep,
+                     const TileSched sched) {
   using Cfg = GemmCfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -201,9 +239,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   pdl_trigger();
   pdl_wait();  // A, the residual stream and the outputs belong to the previous kernels
 
-  const int num_m = (M + kBM * CG - 1) / (kBM * CG);
-  const int num_n = (N + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
+  const int num_tiles = sched.total;
   const int nk = (K + kBK - 1) / kBK;
 
   if (warp == 0) {
@@ -211,8 +247,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = pid; tile < num_tiles; tile += npid) {
-      const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
-      const int n0 = (tile % num_n) * BN + crank * (BN / CG);
+      const TileAt x = tile_at(sched, tile, BN);
+      const int m0 = x.mt * (kBM * CG) + crank * kBM;
+      // each CTA of a pair holds half of the tile's B rows (a half tile uses the first
+      // w/2 rows of each CTA's fixed-size box)
+      const int n0 = x.n0 + crank * (x.w / CG);
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
@@ -234,7 +273,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     if (crank == 0) {
       // MMA issuer: whole warp, elected lane issues (see elect_one)
       constexpr uint32_t idesc_full = make_idesc_bf16(kBM * CG, BN);
-      constexpr uint32_t idesc_half = make_idesc_bf16(kBM, BN / 2);
+      constexpr uint32_t idesc_half = make_idesc_bf16(kBM * CG, BN / 2);
       const uint64_t a0 = make_sdesc(smem_u32(sA), 1024, 2);
       const uint64_t b0 = make_sdesc(smem_u32(sB), 1024, 2);
       int stage = 0;
@@ -243,9 +282,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
-        // ragged last N tile (1-CTA only): issue half-width MMAs when the valid columns fit
-        const uint32_t idesc =
-            (CG == 1 && N - (tile % num_n) * BN <= BN / 2) ? idesc_half : idesc_full;
+        const uint32_t idesc = tile_at(sched, tile, BN).w == BN ? idesc_full : idesc_half;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t dtmem = tmem_base + as * BN;
@@ -284,15 +321,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      const int m0 = (tile / num_n) * (kBM * CG) + crank * kBM;
-      const int n0 = (tile % num_n) * BN;
+      const TileAt x = tile_at(sched, tile, BN);
+      const int m0 = x.mt * (kBM * CG) + crank * kBM;
+      const int n0 = x.n0;
+      const int hw = x.w / 2;  // columns per epilogue half (a multiple of 32)
       const int row = m0 + r;
       // Heads bookkeeping, once per tile-half (no divisions inside the chunk loop):
       // section / head / head-dim of this half's first column, image and token of m0.
       int hsec = 0, hh = 0, hd = 0, img0 = 0, tok0 = 0;
       bool straddle = false;
       if (KIND == EK_HEADS) {
-        const int nn = n0 + half * (BN / 2);
+        const int nn = n0 + half * hw;
         hsec = nn / ep.sec_cols;
         const int within = nn - hsec * ep.sec_cols;
         hh = within / ep.Dp;
@@ -305,7 +344,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
+      for (int c = half * hw; c < (half + 1) * hw; c += 32) {
         const int n = n0 + c;
         if (n >= N) break;  // warp-uniform
         float x[32];
@@ -468,6 +507,37 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   }
 }
 
+// Tile schedule for `units` = SMs / CG persistent units. Half tiles need BN/4 to be a
+// multiple of 32 (the epilogue's chunk width), i.e. BN in {128, 256}.
+TileSched make_sched(int M, int N, int BN, int CG, bool halves_ok) {
+  const int num_m = (M + kBM * CG - 1) / (kBM * CG);
+  const int num_n = (N + BN - 1) / BN;
+  const bool halves = halves_ok && (BN == 256 || BN == 128);
+  TileSched t;
+  t.ragged = (halves && N - (num_n - 1) * BN <= BN / 2) ? 1 : 0;
+  t.nf = num_n - t.ragged;
+  t.f_total = num_m * t.nf;
+  t.f_keep = t.f_total;
+  if (halves) {
+    const int units = num_sms() / CG;
+    const int w2 = 2 * t.f_total + num_m * t.ragged;  // work in half tiles
+    const int r2 = (w2 + units - 1) / units;           // rounds, in half-tile units
+    const int keep = units * (r2 / 2);                 // whole rounds of full tiles
+    if (keep < t.f_keep) t.f_keep = keep;
+  }
+  t.total = t.f_keep + 2 * (t.f_total - t.f_keep) + num_m * t.ragged;
+  return t;
+}
+
+// Rounds (in full-tile time) the schedule takes on the persistent grid.
+double sched_rounds(const TileSched& t, int CG) {
+  const int units = num_sms() / CG;
+  const int halves = t.total - t.f_keep;
+  const int r_full = (t.f_keep + units - 1) / units;
+  const int r_half = (halves + units - 1) / units;
+  return r_full + 0.5 * r_half;
+}
+
 template <int BN, int KIND, int CG>
 int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, const EpiParams& ep,
            cudaStream_t stream) {
@@ -511,11 +581,11 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  const int tiles = ((M + kBM * CG - 1) / (kBM * CG)) * ((N + BN - 1) / BN);
+  const TileSched sched = make_sched(M, N, BN, CG, KIND != EK_HEADS);
   int units = num_sms() / CG;
-  if (tiles < units) units = tiles;
+  if (sched.total < units) units = sched.total;
   const int rc2 = launch_kernel(gemm_bf16_kernel<BN, KIND, CG>, dim3(units * CG), dim3(Cfg::THREADS), Cfg::SMEM,
-                                stream, CG, ta, tb, t0, t1, t2, M, N, K, ep);
+                                stream, CG, ta, tb, t0, t1, t2, M, N, K, ep, sched);
   if (rc2) return rc2;
   return (int)cudaGetLastError();
 }
@@ -554,12 +624,12 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
     const int units = num_sms() / cg;
     double best = 1e30;
     const int cands[3] = {256, 192, 128};
+    (void)units;
     for (int i = 0; i < 3; ++i) {
       const int c = cands[i];
       if (cg == 2 && c == 128) continue;
-      const long tiles = (long)((M + kBM * cg - 1) / (kBM * cg)) * ((N + c - 1) / c);
-      const long waves = (tiles + units - 1) / units;
-      const double cost = (double)waves * c * (c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0));
+      const double rounds = sched_rounds(make_sched(M, N, c, cg, ep.mode != EPI_HEADS), cg);
+      const double cost = rounds * c * (c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0));
       if (cost < best) { best = cost; bn = c; }
     }
   }
