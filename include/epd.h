@@ -180,8 +180,9 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
                              int32_t K, const void* bias, int32_t act, const void* resid, int32_t ldr,
                              int32_t r_mod, const void* lscale, void* out, int32_t ldo, int32_t bn,
                              void* stream);
-/* GEMM tiling policy for subsequent launches in this process: 0 auto (CTA pairs
- * with tcgen05 cta_group::2 for M >= 2048), 1 single-CTA tiles, 2 CTA pairs. */
+/* GEMM tiling policy for subsequent launches in this process: 0 auto, else the cluster
+ * size: 1 single-CTA tiles, 2 CTA pairs (tcgen05 cta_group::2), 4 two CTA pairs sharing
+ * every B tile through TMA multicast. Results do not depend on the policy. */
 epd_status_t epd_set_gemm_cta_group(int32_t policy);
 /* Residual-stream update: h[M,N] (fp32, in place) += lscale * (A W^T + bias); lscale may be NULL.
  * The epilogue is a TMA reduce-add, so h is never read by the SMs. */

@@ -378,7 +378,8 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
 }
 
 epd_status_t epd_set_gemm_cta_group(int32_t policy) {
-  if (policy < 0 || policy > 2) return fail(EPD_ERR_VALUE, "cta group policy must be 0, 1 or 2");
+  if (policy != 0 && policy != 1 && policy != 2 && policy != 4)
+    return fail(EPD_ERR_VALUE, "cta group policy must be 0, 1, 2 or 4");
   epd::set_gemm_cta_group(policy);
   return EPD_OK;
 }

@@ -21,6 +21,12 @@ namespace epd {
 namespace {
 
 constexpr int kBM = 128;
+// Clusters of 4 (two pairs multicasting B) halve B's L2->SM traffic, but only 33 such
+// clusters are co-resident on a B200 (132 of 148 SMs); measured net 2-8 % slower than
+// pairs on the encoder shapes, so the auto policy never picks them (policy 4 forces them).
+#ifndef EPD_CL4_MIN_M
+#define EPD_CL4_MIN_M (1 << 30)
+#endif
 
 constexpr int kBK = 64;
 
@@ -110,6 +116,24 @@ EPD_DEVICE void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// As tma_load_2d_pair, delivered to every CTA in `mask` (same smem offset); each
+// destination's transaction bytes land on its own pair leader's barrier.
+EPD_DEVICE void tma_load_2d_pair_mc(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                    uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu), "h"(mask)
+      : "memory");
+}
+// Arrive on the same barrier offset in every CTA of `mask` once the pair's MMAs complete.
+EPD_DEVICE void tc_commit_pair_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 // Arrive on the same barrier offset in both CTAs of the pair once the pair's MMAs complete.
 EPD_DEVICE void tc_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -191,7 +215,10 @@ EPD_DEVICE TileAt tile_at(const TileSched& s, int t, int BN) {
 // CG = 1: one CTA per 128 x BN tile. CG = 2: a CTA pair (cluster of 2) computes a
 // 256 x BN tile with tcgen05.mma.cta_group::2 -- each CTA loads its 128 rows of A
 // and half of B, the leader issues M=256 MMAs, both CTAs drain their own TMEM.
-template <int BN, int KIND, int CG>
+// CL = cluster size: 1 (single CTA), 2 (one CTA pair) or 4 (two CTA pairs stacked along M
+// that share every B tile: pair 0 multicasts each half of B into both pairs, so the
+// cluster streams B from L2 once for 512 rows -- the big GEMMs are L2-bandwidth bound).
+template <int BN, int KIND, int CG, int CL>
 __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
@@ -211,14 +238,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const uint32_t crank = CG == 2 ? cluster_rank() : 0;
-  const int pid = blockIdx.x / CG;     // CTA pair (or CTA) index
-  const int npid = gridDim.x / CG;
+  static_assert(CL == CG || (CL == 4 && CG == 2), "cluster shape");
+  const uint32_t crank_full = CL > 1 ? cluster_rank() : 0;  // CTA rank in the cluster
+  const uint32_t crank = crank_full & 1;                     // rank within the CTA pair
+  const uint32_t pair = crank_full >> 1;
+  const int pid = blockIdx.x / CL;     // cluster index
+  const int npid = gridDim.x / CL;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL == 4 ? 2 : 1);  // one MMA commit per pair reading the stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -233,7 +263,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     else tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
   }
   tc_fence_before();
-  if (CG == 2) cluster_sync_all(); else __syncthreads();
+  if (CL > 1) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   pdl_trigger();
@@ -248,7 +278,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     uint32_t phase = 0;
     for (int tile = pid; tile < num_tiles; tile += npid) {
       const TileAt x = tile_at(sched, tile, BN);
-      const int m0 = x.mt * (kBM * CG) + crank * kBM;
+      const int m0 = x.mt * (kBM * CL) + crank_full * kBM;
       // each CTA of a pair holds half of the tile's B rows (a half tile uses the first
       // w/2 rows of each CTA's fixed-size box)
       const int n0 = x.n0 + crank * (x.w / CG);
@@ -262,7 +292,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           } else {
             if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
-            tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+            if (CL == 2)
+              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+            else if (pair == 0)  // this half of B, for both pairs
+              tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0,
+                                  (uint16_t)((1u << crank) | (1u << (crank + 2))));
           }
         }
         __syncwarp();
@@ -297,13 +331,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
               if (CG == 2) umma_bf16_pair(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
               else umma_bf16(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
             }
-            if (CG == 2) tc_commit_pair(&empty[stage]); else tc_commit(&empty[stage]);
+            if (CL == 4) tc_commit_pair_mask(&empty[stage], 0xF);  // the stage is free in all 4 CTAs
+            else if (CG == 2) tc_commit_pair(&empty[stage]);
+            else tc_commit(&empty[stage]);
           }
           __syncwarp();
           if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
         }
         if (elect_one()) {
-          if (CG == 2) tc_commit_pair(&tfull[as]); else tc_commit(&tfull[as]);
+          if (CL == 4) tc_commit_pair_mask(&tfull[as], (uint16_t)(3u << (2 * pair)));
+          else if (CG == 2) tc_commit_pair(&tfull[as]);
+          else tc_commit(&tfull[as]);
         }
         __syncwarp();
       }
@@ -316,13 +354,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
     uint8_t* stg = sEpi + half * kEpiStageBytes;
     const int bar_id = 1 + half;
-    const uint32_t tempty_leader = mapa_rank(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader = mapa_rank(smem_u32(&tempty[0]), crank_full & ~1u);  // pair leader
     int local = 0;
     for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const TileAt x = tile_at(sched, tile, BN);
-      const int m0 = x.mt * (kBM * CG) + crank * kBM;
+      const int m0 = x.mt * (kBM * CL) + crank_full * kBM;
       const int n0 = x.n0;
       const int hw = x.w / 2;  // columns per epilogue half (a multiple of 32)
       const int row = m0 + r;
@@ -499,7 +537,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   }
 
   tc_fence_before();
-  if (CG == 2) cluster_sync_all(); else __syncthreads();
+  if (CL > 1) cluster_sync_all(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     if (CG == 2) tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
@@ -507,10 +545,41 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   }
 }
 
-// Tile schedule for `units` = SMs / CG persistent units. Half tiles need BN/4 to be a
-// multiple of 32 (the epilogue's chunk width), i.e. BN in {128, 256}.
-TileSched make_sched(int M, int N, int BN, int CG, bool halves_ok) {
-  const int num_m = (M + kBM * CG - 1) / (kBM * CG);
+// Persistent units that can be co-resident: SMs / CL, capped by how many clusters of CL
+// CTAs (227 KB of smem each) the GPCs can host at once -- a persistent grid larger than
+// that runs its last clusters as a second wave.
+int cluster_units(int CL) {
+  static int cache[5] = {0, 0, 0, 0, 0};
+  if (cache[CL]) return cache[CL];
+  int units = num_sms() / CL;
+  if (CL > 1) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(units * CL);
+    cfg.blockDim = dim3(GemmCfg<256, 2>::THREADS);
+    cfg.dynamicSmemBytes = GemmCfg<256, 2>::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const void* k = CL == 4 ? (const void*)gemm_bf16_kernel<256, EK_ROWS_BF16, 2, 4>
+                            : (const void*)gemm_bf16_kernel<256, EK_ROWS_BF16, 2, 2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<256, 2>::SMEM);
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) == cudaSuccess && n > 0 && n < units) units = n;
+    cudaGetLastError();
+  }
+  cache[CL] = units;
+  return units;
+}
+
+// Tile schedule for `units` = SMs / CL persistent clusters (a tile spans kBM * CL rows).
+// Half tiles need BN/4 to be a multiple of 32 (the epilogue's chunk width), i.e. BN in
+// {128, 256}.
+TileSched make_sched(int M, int N, int BN, int CL, bool halves_ok, int units) {
+  const int num_m = (M + kBM * CL - 1) / (kBM * CL);
   const int num_n = (N + BN - 1) / BN;
   const bool halves = halves_ok && (BN == 256 || BN == 128);
   TileSched t;
@@ -519,7 +588,6 @@ TileSched make_sched(int M, int N, int BN, int CG, bool halves_ok) {
   t.f_total = num_m * t.nf;
   t.f_keep = t.f_total;
   if (halves) {
-    const int units = num_sms() / CG;
     const int w2 = 2 * t.f_total + num_m * t.ragged;  // work in half tiles
     const int r2 = (w2 + units - 1) / units;           // rounds, in half-tile units
     const int keep = units * (r2 / 2);                 // whole rounds of full tiles
@@ -530,17 +598,17 @@ TileSched make_sched(int M, int N, int BN, int CG, bool halves_ok) {
 }
 
 // Rounds (in full-tile time) the schedule takes on the persistent grid.
-double sched_rounds(const TileSched& t, int CG) {
-  const int units = num_sms() / CG;
+double sched_rounds(const TileSched& t, int units) {
   const int halves = t.total - t.f_keep;
   const int r_full = (t.f_keep + units - 1) / units;
   const int r_half = (halves + units - 1) / units;
   return r_full + 0.5 * r_half;
 }
 
-template <int BN, int KIND, int CG>
+template <int BN, int KIND, int CL>
 int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, const EpiParams& ep,
            cudaStream_t stream) {
+  constexpr int CG = CL == 1 ? 1 : 2;
   using Cfg = GemmCfg<BN, CG>;
   CUtensorMap ta, tb, t0, t1, t2;
   int rc = make_tmap_2d(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, kBK, kBM,
@@ -576,32 +644,33 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN, KIND, CG>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_kernel<BN, KIND, CG, CL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return (int)e;
     attr_set = true;
   }
-  const TileSched sched = make_sched(M, N, BN, CG, KIND != EK_HEADS);
-  int units = num_sms() / CG;
+  const int cap = cluster_units(CL);
+  const TileSched sched = make_sched(M, N, BN, CL, KIND != EK_HEADS, cap);
+  int units = cap;
   if (sched.total < units) units = sched.total;
-  const int rc2 = launch_kernel(gemm_bf16_kernel<BN, KIND, CG>, dim3(units * CG), dim3(Cfg::THREADS), Cfg::SMEM,
-                                stream, CG, ta, tb, t0, t1, t2, M, N, K, ep, sched);
+  const int rc2 = launch_kernel(gemm_bf16_kernel<BN, KIND, CG, CL>, dim3(units * CL), dim3(Cfg::THREADS),
+                                Cfg::SMEM, stream, CL, ta, tb, t0, t1, t2, M, N, K, ep, sched);
   if (rc2) return rc2;
   return (int)cudaGetLastError();
 }
 
-template <int BN, int CG>
+template <int BN, int CL>
 int launch_kind(int kind, const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
                 const EpiParams& ep, cudaStream_t stream) {
   switch (kind) {
-    case EK_ROWS_BF16: return launch<BN, EK_ROWS_BF16, CG>(A, lda, B, ldb, M, N, K, ep, stream);
-    case EK_ROWS_F32: return launch<BN, EK_ROWS_F32, CG>(A, lda, B, ldb, M, N, K, ep, stream);
-    case EK_ACC_F32: return launch<BN, EK_ACC_F32, CG>(A, lda, B, ldb, M, N, K, ep, stream);
-    default: return launch<BN, EK_HEADS, CG>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ROWS_BF16: return launch<BN, EK_ROWS_BF16, CL>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ROWS_F32: return launch<BN, EK_ROWS_F32, CL>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_ACC_F32: return launch<BN, EK_ACC_F32, CL>(A, lda, B, ldb, M, N, K, ep, stream);
+    default: return launch<BN, EK_HEADS, CL>(A, lda, B, ldb, M, N, K, ep, stream);
   }
 }
 
-int g_cta_group_policy = 0;  // 0 auto, 1 force single-CTA, 2 force CTA pairs
+int g_cta_group_policy = 0;  // 0 auto; else the cluster size: 1 single CTAs, 2 CTA pairs, 4 pairs sharing B
 
 }  // namespace
 
@@ -612,30 +681,29 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
   if (M <= 0 || N <= 0 || K <= 0) return 1001;
   if (N % 8 != 0 || (lda * 2) % 16 != 0 || (ldb * 2) % 16 != 0) return 1002;
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) return 1003;
-  // CTA pairs (256-row tiles, half of B per SM) for large M; single CTAs for small M.
-  // CTA pairs (256-row tiles, each SM streaming half of B) once there are two 128-row M
-  // tiles; single CTAs for M <= 256 (LM head, resampler query precompute). Pairs compute
-  // the same K-ordered sums, so the choice never changes results.
-  int cg = g_cta_group_policy ? g_cta_group_policy : (M > 256 ? 2 : 1);
+  // Cluster size: CTA pairs (256-row tiles, each SM streaming half of B) once there are two
+  // 128-row M tiles; single CTAs for M <= 256 (LM head, resampler query precompute);
+  // two pairs multicasting B (512-row tiles) when M fills them. All variants compute the
+  // same K-ordered sums, so the choice never changes results.
+  int cl = g_cta_group_policy ? g_cta_group_policy : (M > 256 ? (M >= EPD_CL4_MIN_M ? 4 : 2) : 1);
+  if (cl != 1 && cl != 2 && cl != 4) return 1001;
+  if (ep.mode == EPI_HEADS && cl == 4) cl = 2;
   int bn = bn_hint;
   if (bn == 0) {
-    // Wide tiles amortise the epilogue and B-operand traffic best; step down only
-    // when the last wave of 256-wide tiles would leave most SMs idle.
-    const int units = num_sms() / cg;
+    // Wide tiles amortise the epilogue and operand traffic best; step down only when the
+    // schedule's rounds (half tiles included) favour a narrower tile.
     double best = 1e30;
     const int cands[3] = {256, 192, 128};
-    (void)units;
     for (int i = 0; i < 3; ++i) {
       const int c = cands[i];
-      if (cg == 2 && c == 128) continue;
-      const double rounds = sched_rounds(make_sched(M, N, c, cg, ep.mode != EPI_HEADS), cg);
+      if (cl > 1 && c == 128) continue;
+      const int u = cluster_units(cl);
+      const double rounds = sched_rounds(make_sched(M, N, c, cl, ep.mode != EPI_HEADS, u), u);
       const double cost = rounds * c * (c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0));
       if (cost < best) { best = cost; bn = c; }
     }
   }
-#ifndef EPD_CG2_BN128
-  if (cg == 2 && bn == 128) cg = 1;
-#endif
+  if (cl > 1 && bn == 128) cl = 1;
   int kind;
   if (ep.mode == EPI_HEADS) {
     if (ep.Dp % 16 || ep.sec_cols % ep.Dp || ep.T <= 0) return 1005;
@@ -651,13 +719,17 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
     if (!ep.out || ep.resid_f) return 1005;
     kind = EK_ROWS_BF16;
   }
-  if (cg == 2) {
+  if (cl == 4) {
+    switch (bn) {
+      case 256: return launch_kind<256, 4>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+      case 192: return launch_kind<192, 4>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+      default: return 1004;
+    }
+  }
+  if (cl == 2) {
     switch (bn) {
       case 256: return launch_kind<256, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
       case 192: return launch_kind<192, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-#ifdef EPD_CG2_BN128
-      case 128: return launch_kind<128, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-#endif
       default: return 1004;
     }
   }

@@ -292,7 +292,7 @@ def test_linear_heads(cuda, M, T, H, Dp, dh, trans):
         assert relerr(got, ref) <= TOL, s
 
 
-@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"])
+@pytest.fixture(params=[1, 2, 4], ids=["cta1", "cta2", "cl4"])
 def cta_group(request, cuda):
     from paper_2501_05460_b200._lib import call
     call("epd_set_gemm_cta_group", request.param)

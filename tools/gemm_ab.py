@@ -24,7 +24,11 @@ def timeit(fn, iters=30, warm=5):
 
 tag = Path(os.environ.get("EPD_LIB_PATH", "libepd.so")).stem
 BN = int(os.environ.get("BN", "0"))
-tag += f"/bn{BN}"
+CL = int(os.environ.get("CL", "0"))
+if CL:
+    from paper_2501_05460_b200._lib import call as _call
+    _call("epd_set_gemm_cta_group", CL)
+tag += f"/bn{BN}/cl{CL}"
 dev = torch.device("cuda")
 M = 10240
 line = []
