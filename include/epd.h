@@ -174,7 +174,9 @@ epd_status_t epd_kv_unpack(const void* in, int32_t segments, int64_t segment_str
  * parity tests and profiling. All tensors are device bf16 unless stated.
  *
  * out[M,N] = act(A[M,K] W[N,K]^T + bias) ; if resid: out = resid[row % r_mod] + lscale * out
- * act: 0 none, 1 GELU (tanh approximation), 2 GELU (erf). bias/resid/lscale may be NULL.
+ * act: 0 none, 1 GELU (tanh approximation), 2 GELU (erf), 3 SwiGLU: W's rows alternate
+ * 32-row gate / up groups and out[:, 32g + j] = silu(gate + b) * (up + b) for group g
+ * (out has N/2 columns; no resid / lscale). bias/resid/lscale may be NULL.
  * bn: N tile (0 = auto, else 128/192/256). */
 epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
                              int32_t K, const void* bias, int32_t act, const void* resid, int32_t ldr,
@@ -236,9 +238,12 @@ epd_status_t epd_patchify_u8(const uint8_t* tiles, int32_t n, int32_t S, int32_t
 epd_status_t epd_rmsnorm_f32_bf16(const float* in, int32_t ld_in, void* out, int32_t ld_out, const void* gamma,
                                   int32_t rows, int32_t D, float eps, void* stream);
 /* In-place rotary embedding (rotate-half) on heads [0, nheads) of width hd starting at column
- * col0 of each bf16 row; position of row r = pos0 + r, angle = pos * theta^(-2i/hd). */
+ * col0 of each bf16 row; position of row r = pos0 + r, angle = pos * theta^(-2i/hd).
+ * cos_sin: NULL, or the table epd_rope_table built for the same rows / hd / pos0 / theta. */
 epd_status_t epd_rope_bf16(void* x, int32_t ld, int32_t rows, int32_t col0, int32_t nheads, int32_t hd,
-                           int32_t pos0, float theta, void* stream);
+                           int32_t pos0, float theta, const float* cos_sin, void* stream);
+/* cos_sin[r][i] = (cos, sin)(pos * theta^(-2i/hd)), pos = pos0 + r, i < hd/2: fp32 [rows][hd/2][2]. */
+epd_status_t epd_rope_table(float* cos_sin, int32_t rows, int32_t hd, int32_t pos0, float theta, void* stream);
 /* out[r][c] = silu(gu[r][c]) * gu[r][F + c]. */
 epd_status_t epd_silu_mul_bf16(const void* gu, int32_t ld_in, void* out, int32_t ld_out, int32_t rows, int32_t F,
                                void* stream);

@@ -58,8 +58,10 @@ def prefill(cfg, w: dict, mm_tokens: torch.Tensor | None, text_ids: torch.Tensor
         a = torch.einsum("hqk,khd->qhd", torch.softmax(s, -1), vr).reshape(T, Hq * hd)
         h = h + a @ f[p + "wo"].t()
         x = rms(h, f[p + "mlp_norm"], cfg.rms_eps)
-        gu = x @ f[p + "wgu"].t()
-        h = h + (torch.nn.functional.silu(gu[:, :cfg.ffn]) * gu[:, cfg.ffn:]) @ f[p + "wd"].t()
+        # wgu rows alternate 32-row gate / up groups (prefill.py stores them that way)
+        wg = f[p + "wgu"].view(cfg.ffn // 32, 2, 32, -1)
+        gate, up = x @ wg[:, 0].reshape(cfg.ffn, -1).t(), x @ wg[:, 1].reshape(cfg.ffn, -1).t()
+        h = h + (torch.nn.functional.silu(gate) * up) @ f[p + "wd"].t()
     last = rms(h[-1:], f["final_norm"], cfg.rms_eps)
     logits = (last @ f["lm_head"][:cfg.vocab].t())[0]
     return {"hidden": h, "logits": logits, "token": int(logits.argmax()), "k": ks, "v": vs}

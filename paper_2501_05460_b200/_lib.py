@@ -86,7 +86,8 @@ _SIGS = {
     "epd_layernorm_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _i32, C.c_float, _vp]),
     "epd_layernorm_f32_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _vp, _i32, _i32, C.c_float, _vp]),
     "epd_rmsnorm_f32_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _i32, C.c_float, _vp]),
-    "epd_rope_bf16": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, C.c_float, _vp]),
+    "epd_rope_bf16": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, C.c_float, _vp, _vp]),
+    "epd_rope_table": (_i32, [_vp, _i32, _i32, _i32, C.c_float, _vp]),
     "epd_silu_mul_bf16": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _vp]),
     "epd_kv_write_paged": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i64, _i32, _vp]),
     "epd_gather_rows_f32": (_i32, [_vp, _i32, _vp, _i32, _i32, _vp, _i32, _vp]),

@@ -359,7 +359,7 @@ epd_status_t epd_linear_bf16(const void* A, int32_t lda, const void* W, int32_t 
                              int32_t r_mod, const void* lscale, void* out, int32_t ldo, int32_t bn,
                              void* stream) {
   if (M <= 0 || N <= 0 || K <= 0) return fail(EPD_ERR_VALUE, "linear: empty shape");
-  if (act < 0 || act > 2) return fail(EPD_ERR_VALUE, "linear: unknown activation");
+  if (act < 0 || act > 3) return fail(EPD_ERR_VALUE, "linear: unknown activation");
   if (ldo % 8 || (resid && ldr % 8) || ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(bias) |
                                           reinterpret_cast<uintptr_t>(resid) | reinterpret_cast<uintptr_t>(lscale)) & 15))
     return fail(EPD_ERR_VALUE, "linear: epilogue tensors must be 16-byte aligned");
@@ -481,10 +481,14 @@ epd_status_t epd_rmsnorm_f32_bf16(const float* in, int32_t ld_in, void* out, int
 }
 
 epd_status_t epd_rope_bf16(void* x, int32_t ld, int32_t rows, int32_t col0, int32_t nheads, int32_t hd,
-                           int32_t pos0, float theta, void* stream) {
+                           int32_t pos0, float theta, const float* cos_sin, void* stream) {
   return cuda_status(epd::rope_bf16(reinterpret_cast<epd::bf16*>(x), ld, rows, col0, nheads, hd, pos0, theta,
-                                    S(stream)),
+                                    cos_sin, S(stream)),
                      "rope_bf16");
+}
+
+epd_status_t epd_rope_table(float* cos_sin, int32_t rows, int32_t hd, int32_t pos0, float theta, void* stream) {
+  return cuda_status(epd::rope_table(cos_sin, rows, hd, pos0, theta, S(stream)), "rope_table");
 }
 
 epd_status_t epd_silu_mul_bf16(const void* gu, int32_t ld_in, void* out, int32_t ld_out, int32_t rows, int32_t F,

@@ -67,7 +67,8 @@ EPD_DEVICE float gelu_tanh_fast(float x) {
 //   HEADS     : per-head Q/K/V [bh][T][Dp] (SW32) or keys-major V^T [bh][Dp][Tpad] (no swizzle):
 //               each 32-column chunk leaves as two 16-column 3-D TMA boxes; tiles that
 //               straddle two images store from registers.
-enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS = 3 };
+//   SWIGLU    : 64-column groups (gate 32 | up 32) -> 32 bf16 columns at n/2 (as ROWS_BF16)
+enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS = 3, EK_SWIGLU = 4 };
 
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
 
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * hw; c < (half + 1) * hw; c += 32) {
+      for (int c = half * hw; c < (half + 1) * hw; c += (KIND == EK_SWIGLU ? 64 : 32)) {
         const int n = n0 + c;
         if (n >= N) break;  // warp-uniform
         float x[32];
@@ -393,8 +394,27 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(v[j]);
         }
+        if (KIND == EK_SWIGLU) {
+          // x = gate columns [n, n+32), u = up columns [n+32, n+64) of this 64-column group
+          uint32_t u[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + as * BN + c + 32, u);
+          tmem_ld_wait();
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+          for (int g = 0; g < 4; ++g) {
+            float bg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, bu[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (ep.bias) {
+              load8(ep.bias + n + g * 8, bg);
+              load8(ep.bias + n + 32 + g * 8, bu);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float a = x[g * 8 + j] + bg[j];
+              x[g * 8 + j] = a / (1.f + __expf(-a)) * (__uint_as_float(u[g * 8 + j]) + bu[j]);
+            }
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < 4 && KIND != EK_SWIGLU; ++g) {
           const int col = n + g * 8;
           float* xg = x + g * 8;
           if (col < N) {
@@ -466,7 +486,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         // the previous TMA store(s) must have finished reading the staging buffer
         if (leader) bulk_wait_read0();
         named_bar(bar_id, 128);
-        if (KIND == EK_ROWS_BF16) {
+        if (KIND == EK_ROWS_BF16 || KIND == EK_SWIGLU) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int phys = j ^ ((r >> 1) & 3);
@@ -508,6 +528,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         if (leader) {
           if (KIND == EK_ROWS_BF16 || KIND == EK_ROWS_F32) {
             tma_store_2d(&tmO0, stg, n, m0);
+          } else if (KIND == EK_SWIGLU) {
+            tma_store_2d(&tmO0, stg, n / 2, m0);
           } else if (KIND == EK_ACC_F32) {
             tma_reduce_add_2d(&tmO0, stg, n, m0);
           } else {
@@ -616,9 +638,9 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   if (!rc)
     rc = make_tmap_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  if (KIND == EK_ROWS_BF16) {
-    rc = make_tmap_2d(&t0, ep.out, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 2, 32, kBM,
-                      CU_TENSOR_MAP_SWIZZLE_64B);
+  if (KIND == EK_ROWS_BF16 || KIND == EK_SWIGLU) {
+    rc = make_tmap_2d(&t0, ep.out, (uint64_t)(KIND == EK_SWIGLU ? N / 2 : N), (uint64_t)M, (uint64_t)ep.ldo * 2,
+                      32, kBM, CU_TENSOR_MAP_SWIZZLE_64B);
     t1 = t2 = t0;
   } else if (KIND == EK_ROWS_F32 || KIND == EK_ACC_F32) {
     rc = make_tmap_2d_f32(&t0, ep.out_f, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 4, 32, kBM,
@@ -666,6 +688,7 @@ int launch_kind(int kind, const bf16* A, int lda, const bf16* B, int ldb, int M,
     case EK_ROWS_BF16: return launch<BN, EK_ROWS_BF16, CL>(A, lda, B, ldb, M, N, K, ep, stream);
     case EK_ROWS_F32: return launch<BN, EK_ROWS_F32, CL>(A, lda, B, ldb, M, N, K, ep, stream);
     case EK_ACC_F32: return launch<BN, EK_ACC_F32, CL>(A, lda, B, ldb, M, N, K, ep, stream);
+    case EK_SWIGLU: return launch<BN, EK_SWIGLU, CL>(A, lda, B, ldb, M, N, K, ep, stream);
     default: return launch<BN, EK_HEADS, CL>(A, lda, B, ldb, M, N, K, ep, stream);
   }
 }
@@ -703,6 +726,11 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
       if (cost < best) { best = cost; bn = c; }
     }
   }
+  if (ep.act == ACT_SWIGLU) {
+    // every epilogue half must hold whole 64-column gate|up groups: BN = 256 (halves 128/64)
+    if (bn_hint && bn_hint != 256) return 1004;
+    bn = 256;
+  }
   if (cl > 1 && bn == 128) cl = 1;
   int kind;
   if (ep.mode == EPI_HEADS) {
@@ -715,6 +743,9 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
     if (ep.resid_f && ep.resid) return 1005;
     kind = ep.resid_f ? EK_ACC_F32 : EK_ROWS_F32;
     if (ep.ldo % 4) return 1002;
+  } else if (ep.act == ACT_SWIGLU) {
+    if (!ep.out || ep.resid || ep.resid_f || ep.lscale || N % 64) return 1005;
+    kind = EK_SWIGLU;
   } else {
     if (!ep.out || ep.resid_f) return 1005;
     kind = EK_ROWS_BF16;

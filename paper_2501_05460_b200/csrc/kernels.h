@@ -12,7 +12,10 @@ namespace epd {
 using bf16 = __nv_bfloat16;
 
 enum EpiMode : int { EPI_ROWS = 0, EPI_HEADS = 1 };
-enum Act : int { ACT_NONE = 0, ACT_GELU_TANH = 1, ACT_GELU_ERF = 2 };
+// ACT_SWIGLU: the weight rows come in 32-row groups alternating gate / up (group g of the
+// output = rows [64g, 64g+32) gate, [64g+32, 64g+64) up); the GEMM writes
+// silu(gate + b) * (up + b) to N/2 bf16 output columns (no residual / layer scale).
+enum Act : int { ACT_NONE = 0, ACT_GELU_TANH = 1, ACT_GELU_ERF = 2, ACT_SWIGLU = 3 };
 
 // Epilogue of C = A[M,K] * B[N,K]^T, fused on the TMEM accumulator:
 //   x = act(acc + bias[n]);  if (resid) x = resid[row % r_mod][n] + lscale[n] * x
@@ -100,7 +103,9 @@ int gather_records(const void* src_base, const int32_t* index, int n, size_t byt
 // ---- prefill consumer (llm.cu): the LLM layers around the GEMM / attention kernels.
 int rmsnorm_f32(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma, int rows, int D, float eps,
                 cudaStream_t s);
-int rope_bf16(bf16* x, int ld, int rows, int col0, int nheads, int hd, int pos0, float theta, cudaStream_t s);
+int rope_bf16(bf16* x, int ld, int rows, int col0, int nheads, int hd, int pos0, float theta, const float* cs,
+              cudaStream_t s);
+int rope_table(float* cs, int rows, int hd, int pos0, float theta, cudaStream_t s);
 int silu_mul_bf16(const bf16* gu, int ld_in, bf16* out, int ld_out, int rows, int F, cudaStream_t s);
 int kv_write_paged(const bf16* src, int ld_src, int v_off, int rows, int row_elems, const int32_t* block_ids,
                    int block_size, bf16* pool, size_t seg_elems, int seg0, cudaStream_t s);

@@ -8,47 +8,55 @@ namespace epd {
 
 namespace {
 
-// RMSNorm of fp32 rows into bf16: y = x * rsqrt(mean(x^2) + eps) * gamma. One block per
-// row, two passes over the (L2-resident) row.
+// RMSNorm of fp32 rows into bf16: y = x * rsqrt(mean(x^2) + eps) * gamma. One block of
+// 256 threads per row, the row held in registers (VPT float4 per thread: D <= 4096).
+template <int VPT>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ in, int ld_in,
                                                       bf16* __restrict__ out, int ld_out,
                                                       const bf16* __restrict__ gamma, int D, float eps) {
   __shared__ float red[8];
   const int row = blockIdx.x;
   const float* x = in + (size_t)row * ld_in;
+  float4 v[VPT];
   float ss = 0.f;
-  for (int c = threadIdx.x * 4; c < D; c += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(x + c);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = (threadIdx.x + i * 256) * 4;
+    v[i] = c < D ? *reinterpret_cast<const float4*>(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
   }
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
+  float t = threadIdx.x < 8 ? red[threadIdx.x] : 0.f;
   if (threadIdx.x < 32) {
-    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
     t = warp_sum(t);
     if (threadIdx.x == 0) red[0] = t;
   }
   __syncthreads();
   const float r = rsqrtf(red[0] / (float)D + eps);
   bf16* y = out + (size_t)row * ld_out;
-  for (int c = threadIdx.x * 4; c < D; c += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(x + c);
-    const float2 g01 = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(gamma + c));
-    const float2 g23 = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(gamma + c + 2));
-    uint2 o;
-    o.x = pack_bf16x2(v.x * r * g01.x, v.y * r * g01.y);
-    o.y = pack_bf16x2(v.z * r * g23.x, v.w * r * g23.y);
-    *reinterpret_cast<uint2*>(y + c) = o;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = (threadIdx.x + i * 256) * 4;
+    if (c < D) {
+      const float2 g01 = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(gamma + c));
+      const float2 g23 = unpack_bf16x2(*reinterpret_cast<const uint32_t*>(gamma + c + 2));
+      uint2 o;
+      o.x = pack_bf16x2(v[i].x * r * g01.x, v[i].y * r * g01.y);
+      o.y = pack_bf16x2(v[i].z * r * g23.x, v[i].w * r * g23.y);
+      *reinterpret_cast<uint2*>(y + c) = o;
+    }
   }
 }
 
 // Rotary position embedding, rotate-half convention (Qwen2 / InternLM2): for head dims
 // i < hd/2, (x_i, x_{i+hd/2}) <- (x_i cos - x_{i+hd/2} sin, x_{i+hd/2} cos + x_i sin),
 // angle = pos * theta^(-2i/hd), pos = pos0 + row. In place on heads [0, nheads) starting at
-// column col0 of each row.
+// column col0 of each row. cs (optional): precomputed [rows][hd/2] (cos, sin) pairs for
+// positions pos0.. -- the prefill builds it once per prompt length.
 __global__ void rope_kernel(bf16* __restrict__ x, int ld, int rows, int col0, int nheads, int hd, int pos0,
-                            float log2_theta) {
+                            float log2_theta, const float2* __restrict__ cs) {
   const int half = hd >> 1;
   const size_t total = (size_t)rows * nheads * half;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -56,13 +64,30 @@ __global__ void rope_kernel(bf16* __restrict__ x, int ld, int rows, int col0, in
     const size_t rh = i / half;
     const int h = (int)(rh % nheads);
     const int row = (int)(rh / nheads);
-    const float inv_freq = exp2f(-log2_theta * (2.f * d) / (float)hd);
     float s, c;
-    sincosf((float)(pos0 + row) * inv_freq, &s, &c);
+    if (cs) {
+      const float2 t = cs[(size_t)row * half + d];
+      c = t.x;
+      s = t.y;
+    } else {
+      const float inv_freq = exp2f(-log2_theta * (2.f * d) / (float)hd);
+      sincosf((float)(pos0 + row) * inv_freq, &s, &c);
+    }
     bf16* p = x + (size_t)row * ld + col0 + h * hd + d;
     const float a = __bfloat162float(p[0]), b = __bfloat162float(p[half]);
     p[0] = __float2bfloat16_rn(a * c - b * s);
     p[half] = __float2bfloat16_rn(b * c + a * s);
+  }
+}
+
+__global__ void rope_table_kernel(float2* __restrict__ cs, int rows, int hd, int pos0, float log2_theta) {
+  const int half = hd >> 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * half; i += gridDim.x * blockDim.x) {
+    const int d = i % half, row = i / half;
+    const float inv_freq = exp2f(-log2_theta * (2.f * d) / (float)hd);
+    float s, c;
+    sincosf((float)(pos0 + row) * inv_freq, &s, &c);
+    cs[i] = make_float2(c, s);
   }
 }
 
@@ -162,16 +187,28 @@ int grid_for(size_t work) {
 int rmsnorm_f32(const float* in, int ld_in, bf16* out, int ld_out, const bf16* gamma, int rows, int D, float eps,
                 cudaStream_t s) {
   if (rows <= 0) return 0;
-  if (D % 4 || ld_in % 4 || ld_out % 4) return 1002;
-  rmsnorm_kernel<<<rows, 256, 0, s>>>(in, ld_in, out, ld_out, gamma, D, eps);
+  if (D % 4 || ld_in % 4 || ld_out % 4 || D > 4096) return 1002;
+  if (D <= 2048)
+    rmsnorm_kernel<2><<<rows, 256, 0, s>>>(in, ld_in, out, ld_out, gamma, D, eps);
+  else
+    rmsnorm_kernel<4><<<rows, 256, 0, s>>>(in, ld_in, out, ld_out, gamma, D, eps);
   return (int)cudaGetLastError();
 }
 
-int rope_bf16(bf16* x, int ld, int rows, int col0, int nheads, int hd, int pos0, float theta, cudaStream_t s) {
+int rope_bf16(bf16* x, int ld, int rows, int col0, int nheads, int hd, int pos0, float theta, const float* cs,
+              cudaStream_t s) {
   if (rows <= 0) return 0;
   if (hd % 2 || theta <= 1.f) return 1002;
-  rope_kernel<<<grid_for((size_t)rows * nheads * (hd / 2)), 256, 0, s>>>(x, ld, rows, col0, nheads, hd, pos0,
-                                                                        log2f(theta));
+  rope_kernel<<<grid_for((size_t)rows * nheads * (hd / 2)), 256, 0, s>>>(
+      x, ld, rows, col0, nheads, hd, pos0, log2f(theta), reinterpret_cast<const float2*>(cs));
+  return (int)cudaGetLastError();
+}
+
+int rope_table(float* cs, int rows, int hd, int pos0, float theta, cudaStream_t s) {
+  if (rows <= 0) return 0;
+  if (hd % 2 || theta <= 1.f) return 1002;
+  rope_table_kernel<<<grid_for((size_t)rows * hd / 2), 256, 0, s>>>(reinterpret_cast<float2*>(cs), rows, hd, pos0,
+                                                                    log2f(theta));
   return (int)cudaGetLastError();
 }
 

@@ -10,7 +10,7 @@ import torch
 
 from ._lib import call
 
-ACT = {"none": 0, "gelu_tanh": 1, "gelu_erf": 2}
+ACT = {"none": 0, "gelu_tanh": 1, "gelu_erf": 2, "swiglu": 3}
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -30,12 +30,15 @@ def _need_cuda(*ts: torch.Tensor | None) -> None:
 def linear(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, act: str = "none",
            resid: torch.Tensor | None = None, r_mod: int = 0, lscale: torch.Tensor | None = None,
            out: torch.Tensor | None = None, bn: int = 0) -> torch.Tensor:
-    """out = act(a @ w.T + bias); if resid: out = resid[row % r_mod] + lscale * out (bf16)."""
+    """out = act(a @ w.T + bias); if resid: out = resid[row % r_mod] + lscale * out (bf16).
+
+    act="swiglu": w's rows alternate 32-row gate / up groups (see swiglu_interleave); out has
+    N/2 columns, out[:, 32g + j] = silu(gate) * up of group g."""
     _need_cuda(a, w, bias, resid, lscale, out)
     M, K = a.shape
     N = w.shape[0]
     if out is None:
-        out = torch.empty(M, N, dtype=torch.bfloat16, device=a.device)
+        out = torch.empty(M, N // 2 if act == "swiglu" else N, dtype=torch.bfloat16, device=a.device)
     call("epd_linear_bf16", a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K, _ptr(bias),
          ACT[act], _ptr(resid), resid.stride(0) if resid is not None else 0, r_mod, _ptr(lscale),
          out.data_ptr(), out.stride(0), bn, _stream(a))
@@ -143,6 +146,14 @@ def patchify(tiles: torch.Tensor, patch: int, kpad: int, mean, std, row_offset: 
 
 # ---- prefill consumer (llm.cu)
 
+def swiglu_interleave(gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+    """[F, K] gate and up rows -> [2F, K] in the 32-row alternating layout act="swiglu" reads."""
+    F, K = gate.shape
+    if F % 32 or up.shape != gate.shape:
+        raise ValueError("gate/up must be equal [F, K] with F % 32 == 0")
+    return torch.stack([gate.view(F // 32, 32, K), up.view(F // 32, 32, K)], 1).reshape(2 * F, K)
+
+
 def rmsnorm_f32(x: torch.Tensor, gamma: torch.Tensor, eps: float, out: torch.Tensor | None = None) -> torch.Tensor:
     """fp32 rows -> RMSNorm(gamma) -> bf16 rows."""
     _need_cuda(x, gamma, out)
@@ -154,12 +165,21 @@ def rmsnorm_f32(x: torch.Tensor, gamma: torch.Tensor, eps: float, out: torch.Ten
     return out
 
 
-def rope_(x: torch.Tensor, col0: int, nheads: int, head_dim: int, theta: float, pos0: int = 0) -> torch.Tensor:
-    """In-place rotary embedding (rotate-half) on heads [0, nheads) starting at column col0."""
-    _need_cuda(x)
+def rope_(x: torch.Tensor, col0: int, nheads: int, head_dim: int, theta: float, pos0: int = 0,
+          table: torch.Tensor | None = None) -> torch.Tensor:
+    """In-place rotary embedding (rotate-half) on heads [0, nheads) starting at column col0.
+    ``table``: optional rope_table(...) for the same rows / head_dim / pos0 / theta."""
+    _need_cuda(x, table)
     call("epd_rope_bf16", x.data_ptr(), x.stride(0), x.shape[0], col0, nheads, head_dim, pos0, float(theta),
-         _stream(x))
+         _ptr(table), _stream(x))
     return x
+
+
+def rope_table(rows: int, head_dim: int, theta: float, pos0: int = 0, device=None) -> torch.Tensor:
+    """fp32 [rows, head_dim/2, 2] (cos, sin) table for rope_."""
+    t = torch.empty(rows, head_dim // 2, 2, dtype=torch.float32, device=device)
+    call("epd_rope_table", t.data_ptr(), rows, head_dim, pos0, float(theta), _stream(t))
+    return t
 
 
 def silu_mul(gu: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:

@@ -8,9 +8,9 @@ and produces the first token, so TTFT is measured end to end. Weights are random
 N(0, 0.02) (norm gains 1) of the public LLM geometry; the reference catalog fixes
 layers / KV heads / head dim / hidden (models.cfg), the model cards the rest.
 
-Every op runs on the sm_100a kernels of ``libepd`` (tcgen05 GEMMs with fused bias and
-fp32 residual reduce-add, causal grouped-KV attention, RMSNorm, RoPE, SwiGLU, paged KV
-write, argmax); PyTorch only owns the buffers and captures the launch sequence in one
+Every op runs on the sm_100a kernels of ``libepd`` (tcgen05 GEMMs with fused bias, SwiGLU
+and fp32 residual reduce-add, causal grouped-KV attention, RMSNorm, RoPE, paged KV write,
+argmax); PyTorch only owns the buffers and captures the launch sequence in one
 CUDA graph per prompt shape. K/V land in the paged pool that the P->D handoff
 (handoff.py) moves, so the decode side receives real prefill KV.
 """
@@ -86,7 +86,8 @@ def llm_weights(cfg: LLMConfig, device, seed: int = SEED) -> dict[str, torch.Ten
                                                                           device=device)
         w[p + "wo"] = rnd(H, cfg.q_heads * hd)
         w[p + "mlp_norm"] = torch.ones(H, dtype=torch.bfloat16, device=device)
-        w[p + "wgu"] = rnd(2 * cfg.ffn, H)  # rows [0, F) gate, [F, 2F) up
+        # gate / up rows interleaved in 32-row groups: the GEMM epilogue applies SwiGLU
+        w[p + "wgu"] = kernels.swiglu_interleave(rnd(cfg.ffn, H), rnd(cfg.ffn, H))
         w[p + "wd"] = rnd(H, cfg.ffn)
     return w
 
@@ -112,7 +113,6 @@ class Prefiller:
         self.xn = torch.zeros(T, H, dtype=bf, device=dev)
         self.qkv = torch.zeros(T, cfg.qkv_dim, dtype=bf, device=dev)
         self.attn = torch.zeros(T, cfg.q_heads * cfg.head_dim, dtype=bf, device=dev)
-        self.gu = torch.zeros(T, 2 * cfg.ffn, dtype=bf, device=dev)
         self.act = torch.zeros(T, cfg.ffn, dtype=bf, device=dev)
         self.logits = torch.zeros(1, cfg.vocab_padded, dtype=bf, device=dev)
         self.token = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -120,6 +120,8 @@ class Prefiller:
         self.ids_in = torch.zeros(T, dtype=torch.int32, device=dev)
         self.blocks_in = torch.zeros(T, dtype=torch.int32, device=dev)
         self.iota = torch.arange(T, dtype=torch.int32, device=dev)
+        # RoPE (cos, sin) for positions 0..max_tokens-1, built once
+        self.rope_cs = kernels.rope_table(T, cfg.head_dim, cfg.rope_theta, device=dev)
         self.use_graphs = use_graphs
         self._graphs: dict = {}
 
@@ -132,20 +134,19 @@ class Prefiller:
             kernels.gather_rows_f32(self.mm_in, self.iota[:n_mm], self.h[:n_mm])
         if n_text:
             kernels.gather_rows_f32(w["embed"], self.ids_in[:n_text], self.h[n_mm:T])
-        xn, qkv, attn, gu, act = self.xn[:T], self.qkv[:T], self.attn[:T], self.gu[:T], self.act[:T]
+        xn, qkv, attn, act = self.xn[:T], self.qkv[:T], self.attn[:T], self.act[:T]
         for i in range(cfg.layers):
             p = f"layers.{i}."
             kernels.rmsnorm_f32(h, w[p + "attn_norm"], cfg.rms_eps, out=xn)
             kernels.linear(xn, w[p + "wqkv"], bias=w[p + "bqkv"], out=qkv)
-            kernels.rope_(qkv, 0, Hq + Hk, hd, cfg.rope_theta)
+            kernels.rope_(qkv, 0, Hq + Hk, hd, cfg.rope_theta, table=self.rope_cs)
             if kv is not None:
                 kernels.kv_write_paged(qkv[:, Hq * hd:], Hk * hd, Hk * hd, self.blocks_in, kv.block_size, kv.pool, i)
             kernels.attention(qkv[:, :Hq * hd], qkv[:, Hq * hd:(Hq + Hk) * hd], qkv[:, (Hq + Hk) * hd:], 1, Hq, T, T,
                               hd, hd ** -0.5, out=attn, kv_heads=Hk, causal=True)
             kernels.linear_acc(attn, w[p + "wo"], h)
             kernels.rmsnorm_f32(h, w[p + "mlp_norm"], cfg.rms_eps, out=xn)
-            kernels.linear(xn, w[p + "wgu"], out=gu)
-            kernels.silu_mul(gu, out=act)
+            kernels.linear(xn, w[p + "wgu"], act="swiglu", out=act)  # silu(gate) * up in the epilogue
             kernels.linear_acc(act, w[p + "wd"], h)
         kernels.rmsnorm_f32(h[T - 1:T], w["final_norm"], cfg.rms_eps, out=xn[:1])
         kernels.linear(xn[:1], w["lm_head"], out=self.logits)

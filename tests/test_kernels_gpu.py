@@ -199,7 +199,10 @@ def test_rmsnorm_rope_silu(cuda):
     Hq, Hk, hd, theta = 4, 2, 128, 1e6
     qkv = _bf(T, (Hq + 2 * Hk) * hd, gen=g)
     ref_q = qkv.float().clone()
+    qkv2 = qkv.clone()
     kernels.rope_(qkv, 0, Hq + Hk, hd, theta, pos0=5)
+    kernels.rope_(qkv2, 0, Hq + Hk, hd, theta, pos0=5, table=kernels.rope_table(T, hd, theta, pos0=5, device=cuda))
+    assert torch.equal(qkv, qkv2)  # the table path computes the same angles
     pos = torch.arange(5, 5 + T, device=cuda, dtype=torch.float64)[:, None]
     inv = theta ** (-torch.arange(0, hd, 2, device=cuda, dtype=torch.float64) / hd)
     ang = pos * inv[None, :]
@@ -214,6 +217,22 @@ def test_rmsnorm_rope_silu(cuda):
     gu = _bf(T, 2 * F, scale=2.0, gen=g)
     y = kernels.silu_mul(gu)
     ref = torch.nn.functional.silu(gu[:, :F].float()) * gu[:, F:].float()
+    assert relerr(y, ref) <= TOL
+
+
+@pytest.mark.parametrize("M,F,K", [(662, 18944, 3584), (300, 512, 256), (5000, 1024, 512)])
+def test_linear_swiglu_epilogue(cuda, M, F, K):
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(M + F)
+    a = _bf(M, K, gen=g)
+    gate, up = _bf(F, K, scale=K ** -0.5, gen=g), _bf(F, K, scale=K ** -0.5, gen=g)
+    bg, bu = _bf(F, gen=g), _bf(F, gen=g)
+    w = kernels.swiglu_interleave(gate, up)
+    b = kernels.swiglu_interleave(bg.view(F, 1), bu.view(F, 1)).view(-1)
+    y = kernels.linear(a, w, bias=b, act="swiglu")
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.silu(a.float() @ gate.float().t() + bg.float()) * (a.float() @ up.float().t() + bu.float())
+    assert y.shape == (M, F)
     assert relerr(y, ref) <= TOL
 
 
