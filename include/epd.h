@@ -259,6 +259,15 @@ epd_status_t epd_gather_rows_f32(const void* src, int32_t ld_src, const int32_t*
 /* *out = argmax(x[0:n]) (first index on ties). */
 epd_status_t epd_argmax_bf16(const void* x, int32_t n, int32_t* out, void* stream);
 
+/* ------------------------------------------------------------------ image tiling
+ * SURVEY.md 8(f) item 3 (the step before the path; the reference only looks tile counts up,
+ * models.py:138-143). out[n][S][S][C] uint8 = the cols x rows grid tiles (row-major) of the
+ * image resized to (cols*S, rows*S), plus, when thumb, the whole image resized to S x S --
+ * first when thumb_first (MiniCPM-V order) else last (InternVL order). Antialiased bilinear
+ * (triangle filter widened by the downscale factor). cols*rows may be 0 (thumbnail only). */
+epd_status_t epd_tile_image(const uint8_t* src, int32_t H, int32_t W, int32_t C, int32_t cols, int32_t rows,
+                            int32_t thumb, int32_t thumb_first, int32_t S, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

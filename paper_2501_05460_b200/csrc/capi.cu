@@ -519,4 +519,11 @@ epd_status_t epd_argmax_bf16(const void* x, int32_t n, int32_t* out, void* strea
 }
 
 
+epd_status_t epd_tile_image(const uint8_t* src, int32_t H, int32_t W, int32_t C, int32_t cols, int32_t rows,
+                            int32_t thumb, int32_t thumb_first, int32_t tile, uint8_t* out, void* stream) {
+  if (!src || !out) return fail(EPD_ERR_VALUE, "tile_image: null buffer");
+  return cuda_status(epd::tile_image_u8(src, H, W, C, cols, rows, thumb, thumb_first, tile, out, S(stream)),
+                     "tile_image");
+}
+
 }  // extern "C"

@@ -113,6 +113,11 @@ int gather_rows_f32(const bf16* src, int ld_src, const int32_t* index, int rows,
                     cudaStream_t s);
 int argmax_bf16(const bf16* x, int n, int32_t* out, cudaStream_t s);
 
+// ---- image tiling (tiler.cu): grid tiles of the image resized to (cols*S, rows*S) plus an
+// optional S x S thumbnail (first or last), antialiased bilinear, uint8 HWC.
+int tile_image_u8(const uint8_t* src, int H, int W, int C, int cols, int rows, int thumb, int thumb_first, int S,
+                  uint8_t* out, cudaStream_t s);
+
 // ---- fp32 check mode (check_f32.cu): CUDA-core fp32 twins of the kernels above.
 // Epilogue: x = act(acc + bias[n]) * lscale[n] + resid[row % r_mod][n]; ROWS writes
 // (or, with accumulate, adds to) out[row*ldo + n]; HEADS scatters like EpiParams
