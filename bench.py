@@ -54,6 +54,10 @@ def workload(name: str):
     if name == "c2":
         return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b",
                     desc="C2: MiniCPM-V 2.6-shaped SigLIP-400M + resampler, 10 tiles (448x448) per request")
+    if name == "c2i":
+        return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b", image=(4032, 3024),
+                    desc="C2 from pixels: one 4032x3024 photo per request, MiniCPM-V slicing on the GPU -> "
+                         "10 tiles (448x448) -> SigLIP-400M + resampler")
     if name == "c4":
         return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True,
                     desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
@@ -227,6 +231,12 @@ def run_ours(args, wl, world, rank, local):
     stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache)
 
     tiles_host = tiles_for_request(n, cfg, seed=20260808, repeat_period=wl["repeat"]).pin_memory()
+    image_host = None
+    if wl.get("image"):
+        # one synthetic photo per request; the stage tiles it on the GPU (tiler.py)
+        iw, ih = wl["image"]
+        g = torch.Generator().manual_seed(20260808)
+        image_host = torch.randint(0, 256, (ih, iw, cfg.channels), dtype=torch.uint8, generator=g).pin_memory()
     tiles_dev = tiles_host.to(dev)
     out_host = torch.empty(n, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16).pin_memory()
 
@@ -246,6 +256,8 @@ def run_ours(args, wl, world, rank, local):
         # pinned H2D of the request's tiles -> encode -> D2H of the packed tokens; the stage
         # pipelines its host I/O streams across consecutive requests
         reset_cache()
+        if image_host is not None:
+            return stage.process_image(image_host, cfg.geometry.name, out_host=out_host if rank == 0 else None)
         return stage.process(tiles_host, out_host=out_host if rank == 0 else None)
 
     def max_over_ranks(x: float) -> float:
@@ -315,7 +327,8 @@ def run_ours(args, wl, world, rank, local):
         tok_host = torch.empty(1, dtype=torch.int32).pin_memory()
 
         def step_ttft():
-            res = stage.process(tiles_host)
+            res = (stage.process_image(image_host, cfg.geometry.name) if image_host is not None
+                   else stage.process(tiles_host))
             if pf is not None:
                 tok = pf.prefill(res.tokens.view(-1, cfg.out_dim), prompt)
                 tok_host.copy_(tok, non_blocking=True)
@@ -408,7 +421,8 @@ def run_ours(args, wl, world, rank, local):
                      "the packed MM tokens (+ their D2H). The 'modeled prefill' variant adds the reference's "
                      "costs.prefill_latency with SYNTHETIC_COSTS (presets.py:53-61) instead.",
         "e2e": {"value": e2e_value, "unit": "tiles/s",
-                "h2d_bytes_per_step": int(n * cfg.tile_bytes),  # summed over ranks (each uploads its shard)
+                "h2d_bytes_per_step": int(image_host.numel() * world if image_host is not None
+                                          else n * cfg.tile_bytes),  # summed over ranks
                 "d2h_bytes_per_step": int(out_host.numel() * 2)},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all encoder GEMM launches, profiled pass)",

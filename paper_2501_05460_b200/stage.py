@@ -202,6 +202,25 @@ class EncodeStage:
                 out_host.copy_(res.tokens)
         return res
 
+    def process_image(self, image_host: torch.Tensor, model: str, rid: int = 0,
+                      out_host: torch.Tensor | None = None) -> RequestResult:
+        """One request = one photo (uint8 HWC, pinned): upload it, cut the model's tiles on the
+        GPU (tiler.py), then encode as :meth:`process`. Single-rank
+        (the tiles are then sharded by process() when world > 1 via tiles_dev on each rank)."""
+        from .tiler import plan, tile_image
+        H, W, Cc = image_host.shape
+        cols, rows, thumb, _ = plan(model, W, H)
+        n = cols * rows + (1 if thumb else 0)
+        img, release = self._upload(image_host[None], None)
+        r, k = self._slot("tiles", (n, self.cfg.image_size, self.cfg.image_size, Cc), torch.uint8)
+        tiles = tile_image(img[0], model, tile=self.cfg.image_size, out=r["bufs"][k])
+        release()
+        res = self.process(None, rid, tiles_dev=tiles, out_host=out_host)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        r["free"][k] = ev  # the tiles slot is reusable once this request's encode is queued
+        return res
+
     def _process(self, tiles_host, rid, tiles_dev) -> RequestResult:
         n = tiles_host.shape[0] if tiles_host is not None else tiles_dev.shape[0]
         is_sink = self.rank == self.prefill_rank

@@ -43,3 +43,21 @@ def test_tile_image_matches_reference(cuda, model, w, h):
     diff = (tiles.float() - ref).abs()
     assert float(diff.max()) <= 1.0
     assert float((diff > 0).float().mean()) < 1e-3  # only rounding ties may differ
+
+
+def test_stage_process_image_equals_tiles_path(cuda):
+    """process_image (upload photo -> GPU tiles -> encode) packs exactly the tokens that
+    encoding the same GPU-cut tiles directly gives."""
+    from paper_2501_05460_b200.configs import TINY_VIT
+    from paper_2501_05460_b200.encoder import VisionEncoder
+    from paper_2501_05460_b200.stage import EncodeStage
+    from paper_2501_05460_b200.tiler import tile_image
+    enc = VisionEncoder(TINY_VIT, cuda, max_tiles=16)
+    stage = EncodeStage(enc, cuda)
+    g = torch.Generator().manual_seed(3)
+    img = torch.randint(0, 256, (1100, 1500, 3), dtype=torch.uint8, generator=g).pin_memory()
+    res = stage.process_image(img, "minicpm-v-2.6")
+    tiles = tile_image(img.to(cuda), "minicpm-v-2.6", tile=TINY_VIT.image_size)
+    ref = enc.encode(tiles)
+    torch.cuda.synchronize()
+    assert res.tokens.shape[0] == tiles.shape[0] and torch.equal(res.tokens, ref)
