@@ -268,6 +268,16 @@ epd_status_t epd_argmax_bf16(const void* x, int32_t n, int32_t* out, void* strea
 epd_status_t epd_tile_image(const uint8_t* src, int32_t H, int32_t W, int32_t C, int32_t cols, int32_t rows,
                             int32_t thumb, int32_t thumb_first, int32_t S, uint8_t* out, void* stream);
 
+/* ------------------------------------------------------------------ device block free list
+ * blocks.BlockManager's free stack (blocks.py:29, 52, 61) in device
+ * memory (int32 stack[total], int32 *top), stream-ordered. init: stack = total-1 .. 0, top =
+ * total (ids 0, 1, 2, ... come out first). alloc: out[i] = stack[top-1-i], top -= need. free:
+ * ids pushed in reverse, top += n (so they are handed out again in their original order).
+ * Capacity / double-free checks are the caller's: the counts are host-known. */
+epd_status_t epd_blocks_init(int32_t* stack, int32_t* top, int32_t total, void* stream);
+epd_status_t epd_blocks_alloc(int32_t* stack, int32_t* top, int32_t need, int32_t* out_ids, void* stream);
+epd_status_t epd_blocks_free(int32_t* stack, int32_t* top, const int32_t* ids, int32_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

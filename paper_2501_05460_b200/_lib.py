@@ -92,6 +92,9 @@ _SIGS = {
     "epd_kv_write_paged": (_i32, [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i64, _i32, _vp]),
     "epd_gather_rows_f32": (_i32, [_vp, _i32, _vp, _i32, _i32, _vp, _i32, _vp]),
     "epd_argmax_bf16": (_i32, [_vp, _i32, _vp, _vp]),
+    "epd_blocks_init": (_i32, [_vp, _vp, _i32, _vp]),
+    "epd_blocks_alloc": (_i32, [_vp, _vp, _i32, _vp, _vp]),
+    "epd_blocks_free": (_i32, [_vp, _vp, _vp, _i32, _vp]),
     "epd_tile_image": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "epd_patchify_u8": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
 }

@@ -526,4 +526,16 @@ epd_status_t epd_tile_image(const uint8_t* src, int32_t H, int32_t W, int32_t C,
                      "tile_image");
 }
 
+epd_status_t epd_blocks_init(int32_t* stack, int32_t* top, int32_t total, void* stream) {
+  return cuda_status(epd::blocks_init(stack, top, total, S(stream)), "blocks_init");
+}
+
+epd_status_t epd_blocks_alloc(int32_t* stack, int32_t* top, int32_t need, int32_t* out_ids, void* stream) {
+  return cuda_status(epd::blocks_alloc(stack, top, need, out_ids, S(stream)), "blocks_alloc");
+}
+
+epd_status_t epd_blocks_free(int32_t* stack, int32_t* top, const int32_t* ids, int32_t n, void* stream) {
+  return cuda_status(epd::blocks_free(stack, top, ids, n, S(stream)), "blocks_free");
+}
+
 }  // extern "C"

@@ -113,6 +113,11 @@ int gather_rows_f32(const bf16* src, int ld_src, const int32_t* index, int rows,
                     cudaStream_t s);
 int argmax_bf16(const bf16* x, int n, int32_t* out, cudaStream_t s);
 
+// ---- device block free list (blocks.cu): LIFO ids as blocks.py hands them out.
+int blocks_init(int32_t* stack, int32_t* top, int total, cudaStream_t s);
+int blocks_alloc(int32_t* stack, int32_t* top, int need, int32_t* out, cudaStream_t s);
+int blocks_free(int32_t* stack, int32_t* top, const int32_t* ids, int n, cudaStream_t s);
+
 // ---- image tiling (tiler.cu): grid tiles of the image resized to (cols*S, rows*S) plus an
 // optional S x S thumbnail (first or last), antialiased bilinear, uint8 HWC.
 int tile_image_u8(const uint8_t* src, int H, int W, int C, int cols, int rows, int thumb, int thumb_first, int S,
