@@ -153,9 +153,30 @@ __global__ void __launch_bounds__(1024) argmax_kernel(const bf16* __restrict__ x
   __shared__ int si[32];
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+  // 16-byte loads (8 values) while the pointer is 16-byte aligned; each thread walks its
+  // chunks in increasing index order, so within a thread the first index wins ties
+  const int head = (int)(((16 - (reinterpret_cast<uintptr_t>(x) & 15)) & 15) / 2);
+  const int h = head < n ? head : n;
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
     const float v = __bfloat162float(x[i]);
-    if (v > best) { best = v; bi = i; }  // increasing i: first index wins ties within a thread
+    if (v > best) { best = v; bi = i; }
+  }
+  const int nv = (n - h) / 8;
+  const uint4* xv = reinterpret_cast<const uint4*>(x + h);
+  for (int k = threadIdx.x; k < nv; k += blockDim.x) {
+    const uint4 u = xv[k];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = unpack_bf16x2(w[j]);
+      const int i = h + k * 8 + 2 * j;
+      if (f.x > best) { best = f.x; bi = i; }
+      if (f.y > best) { best = f.y; bi = i + 1; }
+    }
+  }
+  for (int i = h + nv * 8 + threadIdx.x; i < n; i += blockDim.x) {
+    const float v = __bfloat162float(x[i]);
+    if (v > best) { best = v; bi = i; }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const float ov = __shfl_xor_sync(0xffffffffu, best, o);
