@@ -59,7 +59,7 @@ def workload(name: str):
                     desc="C2 from pixels: one 4032x3024 photo per request, MiniCPM-V slicing on the GPU -> "
                          "10 tiles (448x448) -> SigLIP-400M + resampler")
     if name == "c4":
-        return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True,
+        return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True, llm="qwen2-7b",
                     desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
     if name == "c5":
         return dict(cfg=INTERNVIT_300M, tiles=12, repeat=None, cache=False, kv_handoff=True, llm="internlm2.5-7b",
@@ -327,6 +327,7 @@ def run_ours(args, wl, world, rank, local):
         tok_host = torch.empty(1, dtype=torch.int32).pin_memory()
 
         def step_ttft():
+            reset_cache()  # every TTFT request starts cold, like the e2e loop
             res = (stage.process_image(image_host, cfg.geometry.name) if image_host is not None
                    else stage.process(tiles_host))
             if pf is not None:
