@@ -50,6 +50,37 @@ EPD_DEVICE float ex2_poly(float x) {
   const float p = fmaf(fmaf(fmaf(0.05517133f, f, 0.2426105f), f, 0.693261f), f, 0.9999281f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): two lanes of softmax arithmetic per instruction.
+EPD_DEVICE float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\nmov.b64 rc, {%6,%7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0,%1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+EPD_DEVICE float2 add2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
+      "add.rn.f32x2 rd, ra, rb;\nmov.b64 {%0,%1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// ex2_poly on a pair, the arithmetic packed
+EPD_DEVICE float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 K = make_float2(12582912.f, 12582912.f), nK = make_float2(-12582912.f, -12582912.f);
+  const float2 t = add2(x, K);
+  const float2 r = add2(t, nK);
+  const float2 f = add2(x, make_float2(-r.x, -r.y));
+  float2 q = fma2(make_float2(0.05517133f, 0.05517133f), f, make_float2(0.2426105f, 0.2426105f));
+  q = fma2(q, f, make_float2(0.693261f, 0.693261f));
+  q = fma2(q, f, make_float2(0.9999281f, 0.9999281f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
 #ifndef EPD_POLY_EIGHTHS
 #define EPD_POLY_EIGHTHS 2  // pairs (of every 8) whose exponentials run on the FMA pipe
 #endif
@@ -468,22 +499,24 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
             }
           }
           const float nm = -m_used;
-          float rs0 = 0.f, rs1 = 0.f;
+          float2 rs0 = make_float2(0.f, 0.f), rs1 = rs0;
           uint32_t pk[32];
+          const float2 c2 = make_float2(c, c), nm2 = make_float2(nm, nm);
 #pragma unroll
           for (int i = 0; i < 64; i += 2) {
-            // The softmax is MUFU-bound (16 ex2/clk/SM): a share of the pairs goes to the FMA pipe.
+            // The softmax is MUFU-bound (16 ex2/clk/SM): a share of the pairs goes to the FMA
+            // pipe; the pair arithmetic runs as packed FFMA2 / FADD2.
             const bool poly = ((i >> 1) & 7) < EPD_POLY_EIGHTHS;
-            const float a0 = fmaf(__uint_as_float(sv[i]), c, nm), a1 = fmaf(__uint_as_float(sv[i + 1]), c, nm);
-            const float e0 = poly ? ex2_poly(a0) : ex2(a0);
-            const float e1 = poly ? ex2_poly(a1) : ex2(a1);
-            rs0 += e0;
-            rs1 += e1;
-            pk[i >> 1] = pack_bf16x2(e0, e1);
+            const float2 a = fma2(make_float2(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), c2, nm2);
+            const float2 e = poly ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
+            if ((i >> 1) & 1) rs1 = add2(rs1, e);
+            else rs0 = add2(rs0, e);
+            pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
           tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
           tmem_st_wait();
-          l += rs0 + rs1;
+          const float2 rs = add2(rs0, rs1);
+          l += rs.x + rs.y;
           tc_fence_before();
           mbar_arrive(&p_ready[2 * g + (j & 1)]);
           ++pv_count;
