@@ -81,6 +81,23 @@ EPD_DEVICE float2 ex2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
+#ifndef EPD_ATTN_TRACE
+#define EPD_ATTN_TRACE 0
+#endif
+#if EPD_ATTN_TRACE
+// Timeline of CTA 0's first 3 items, experiment builds only (tools/attn_trace.py):
+// [event][softmax warp or MMA tile][item * 16 + block] = SM clock.
+__device__ uint32_t g_attn_trace[8][8][48];
+#define ATR(what, unit, it, j)                                                   \
+  do {                                                                         \
+    if (blockIdx.x == 0 && (it) < 3 && (j) < 16 && lane == 0)                  \
+      g_attn_trace[what][unit][(it) * 16 + (j)] = (uint32_t)clock64();         \
+  } while (0)
+#else
+#define ATR(what, unit, it, j) \
+  do {                         \
+  } while (0)
+#endif
 #ifndef EPD_POLY_EIGHTHS
 #define EPD_POLY_EIGHTHS 2  // pairs (of every 8) whose exponentials run on the FMA pipe
 #endif
@@ -342,7 +359,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         }
         tc_commit_warp(&s_full[2 * g + (j & 1)]);
       };
-      for (int w = blockIdx.x; w < nitems; w += gridDim.x) {
+      for (int w = blockIdx.x, mit = 0; w < nitems; w += gridDim.x, ++mit) {
         const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
         if (x.nq == 0) continue;
         for (int g = 0; g < x.nq; ++g) {
@@ -364,6 +381,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
           for (int g = 0; g < x.nq; ++g) {
             const int pb = 2 * g + (j & 1);
             mbar_wait(&p_ready[pb], (pr_ph >> pb) & 1);
+            ATR(2, g, mit, j);
             pr_ph ^= 1u << pb;
             if (g == 0) mbar_wait(&v_full[sv], ((vc + j) / C::KVS) & 1);
             tc_fence_after();
@@ -383,6 +401,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
               if (g == 0) mbar_wait(&k_full[ks], ((kc + j + 2) / C::KS) & 1);
               tc_fence_after();
               issue_s(g, j + 2, ks);
+              ATR(3, g, mit, j);
             }
           }
           tc_commit_warp(&v_empty[sv]);
@@ -448,6 +467,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         for (int j = 0; j < nkb; ++j) {
           const int kvalid = klim - j * C::KB;
           mbar_wait(&s_full[2 * g + (j & 1)], (sf_ph >> (j & 1)) & 1);
+          ATR(0, wi, it, j);
           sf_ph ^= 1u << (j & 1);
           tc_fence_after();
           const uint32_t s_tm = tmem + lane_off + C::s_col(g, j & 1);
@@ -455,6 +475,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
           tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
           tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
           tmem_ld_wait();
+          ATR(4, wi, it, j);
           if (kvalid < 64) {
 #pragma unroll
             for (int i = 0; i < 64; ++i)
@@ -477,6 +498,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
             // Lazy rescale: only when a row max grows by more than 2^8. PV_g(j-1) may still
             // be accumulating into O_g, so wait for it first (rare path).
             const bool need = m_new > m_used + 8.f;
+            ATR(5, wi, it, j);
             if (__any_sync(0xffffffffu, need)) {
               mbar_wait(&pv_done[g], (pv_count - 1) & 1);
               tc_fence_after();
@@ -513,11 +535,14 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
             else rs0 = add2(rs0, e);
             pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
+          ATR(6, wi, it, j);
           tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
           tmem_st_wait();
+          ATR(7, wi, it, j);
           const float2 rs = add2(rs0, rs1);
           l += rs.x + rs.y;
           tc_fence_before();
+          ATR(1, wi, it, j);
           mbar_arrive(&p_ready[2 * g + (j & 1)]);
           ++pv_count;
         }
@@ -600,6 +625,12 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
 }
 
 }  // namespace
+
+#if EPD_ATTN_TRACE
+extern "C" int epd_debug_attn_trace(void* dst) {
+  return (int)cudaMemcpyFromSymbol(dst, g_attn_trace, sizeof(g_attn_trace));
+}
+#endif
 
 int attention_bf16(const AttnParams& p, cudaStream_t stream) {
   if (p.B <= 0 || p.H <= 0 || p.Tq <= 0 || p.Tk <= 0 || p.Dv <= 0 || p.Dv > p.Dp) return 1001;
