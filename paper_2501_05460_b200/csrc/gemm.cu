@@ -187,6 +187,9 @@ struct TileSched {
   int f_keep;   // full tiles kept whole (the rest of the num_m * nf are split)
   int f_total;  // num_m * nf
   int total;    // f_keep + 2 (f_total - f_keep) + num_m * ragged
+  int num_m;    // M tiles
+  int mfast;    // 1: consecutive full tiles walk down M (B, the larger operand, is read
+                // from HBM once and reused from L2 by every M tile); 0: along N
 };
 struct TileAt {
   int mt, n0, w;
@@ -194,8 +197,15 @@ struct TileAt {
 EPD_DEVICE TileAt tile_at(const TileSched& s, int t, int BN) {
   TileAt x;
   if (t < s.f_keep) {
-    x.mt = t / s.nf;
-    x.n0 = (t - x.mt * s.nf) * BN;
+    int nt;
+    if (s.mfast) {
+      nt = t / s.num_m;
+      x.mt = t - nt * s.num_m;
+    } else {
+      x.mt = t / s.nf;
+      nt = t - x.mt * s.nf;
+    }
+    x.n0 = nt * BN;
     x.w = BN;
     return x;
   }
@@ -203,8 +213,15 @@ EPD_DEVICE TileAt tile_at(const TileSched& s, int t, int BN) {
   const int nsplit = s.f_total - s.f_keep;
   if (k < 2 * nsplit) {
     const int ft = s.f_keep + (k >> 1);
-    x.mt = ft / s.nf;
-    x.n0 = (ft - x.mt * s.nf) * BN + (k & 1) * (BN / 2);
+    int nt;
+    if (s.mfast) {
+      nt = ft / s.num_m;
+      x.mt = ft - nt * s.num_m;
+    } else {
+      x.mt = ft / s.nf;
+      nt = ft - x.mt * s.nf;
+    }
+    x.n0 = nt * BN + (k & 1) * (BN / 2);
   } else {
     x.mt = k - 2 * nsplit;
     x.n0 = s.nf * BN;
@@ -616,6 +633,16 @@ TileSched make_sched(int M, int N, int BN, int CL, bool halves_ok, int units) {
     if (keep < t.f_keep) t.f_keep = keep;
   }
   t.total = t.f_keep + 2 * (t.f_total - t.f_keep) + num_m * t.ragged;
+  t.num_m = num_m;
+  // Walk down M when B (N x K) outweighs A (M x K): one pass over the weights from HBM,
+  // shared through L2 by the few M tiles. (Walking N, a prefill's 662-row activations
+  // against the 271 MB gate/up weight re-read the weights from HBM once per M tile.)
+  t.mfast = (N > M && num_m > 1) ? 1 : 0;
+  static const int force = [] {
+    const char* e = getenv("EPD_GEMM_MFAST");  // A/B override: 0 / 1
+    return e ? atoi(e) : -1;
+  }();
+  if (force >= 0) t.mfast = force;
   return t;
 }
 
