@@ -368,6 +368,7 @@ def run_ours(args, wl, world, rank, local):
     _lib.call("epd_encoder_profile", enc._h, 0)
 
     kv = kv_handoff_bench(wl, cfg, n, world, rank, dev, args) if wl.get("kv_handoff") else None
+    gather = gather_bench(stage, cfg, n, world, rank, dev, args) if not wl["cache"] else None
 
     encoded_tiles = n  # tiles that complete the request per step (cache hits count as served)
     value = encoded_tiles * args.steps / (total_ms / 1e3)
@@ -439,6 +440,8 @@ def run_ours(args, wl, world, rank, local):
     }
     if wl.get("kv_handoff"):
         line["kv_handoff"] = kv
+    if gather is not None:
+        line["gather"] = gather
     if cache is not None and last is not None and last.kinds is not None:
         line["cache"] = {"hits": last.kinds.count("hit"), "misses": last.kinds.count("miss"),
                          "dups": last.kinds.count("dup")}
@@ -487,6 +490,47 @@ def kv_handoff_bench(wl, cfg, n, world, rank, dev, args):
             "ms_per_request": ms, "GBps": moved / (ms / 1e3) / 1e9,
             "path": "pack -> self-copy -> unpack (same GPU)" if world == 1 else "pack -> NCCL P2P -> unpack",
             "note": "whole 16-token blocks move; pd_bytes is the reference's token-exact count (engine.py:553-554)"}
+
+
+NVLINK_GBPS = 900.0  # NVLink 5 per GPU per direction (nominal; MEASURED_PEAKS.json has no NVLink figure)
+
+
+def gather_bench(stage, cfg, n, world, rank, dev, args):
+    """The EP exchange alone (engine.py:521-526 bytes): every encode rank's shard of
+    post-projector MM tokens -> the prefill rank at its tile offset (EncodeStage._gather,
+    NCCL grouped P2P over NVLink), timed on the device over K requests, max over ranks.
+    Roofline: bytes into the prefill GPU / time against the NVLink ingress bandwidth."""
+    import torch.distributed as dist
+
+    from paper_2501_05460_b200.routing import ep_bytes, shard_ranges
+    ranges = shard_ranges(n, world)
+    tpp, bpt = cfg.out_tokens, cfg.out_dim * 2
+    into_sink = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != 0)
+    if world == 1:
+        return {"bytes_per_request": 0, "note": "single GPU: the shard is written in place into the packed buffer"}
+    first, count = ranges[rank]
+    local = torch.randn(max(count, 1), cfg.out_tokens, cfg.out_dim, device=dev).to(torch.bfloat16)[:count]
+    dest = torch.empty(n, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16, device=dev) if rank == 0 else None
+    for _ in range(args.warmup):
+        stage._gather(local if count else None, dest, ranges)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(max(args.steps, 20)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        stage._gather(local if count else None, dest, ranges)
+        b.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ts.append(float(t.item()))
+    ms = _percentile(ts, 0.5)
+    gbs = into_sink / (ms / 1e3) / 1e9
+    return {"bytes_per_request": into_sink, "p50_ms": ms, "GBps": gbs, "peak_GBps": NVLINK_GBPS,
+            "frac": gbs / NVLINK_GBPS, "peak_source": "nominal NVLink 5 ingress per GPU",
+            "path": "NCCL grouped P2P (batch_isend_irecv) into the prefill rank at tile offsets"}
 
 
 def stage_tiles_per_rank(n: int, world: int, rank: int) -> int:

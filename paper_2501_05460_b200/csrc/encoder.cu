@@ -16,9 +16,13 @@
 
 #include "encoder.h"
 #include "kernels.h"
+#include "launch.h"
 #include "tmap.h"
 
 namespace epd {
+
+// Largest chunk whose forward is launched with PDL in auto mode (launch.h).
+constexpr int kPdlMaxTiles = 3;
 
 namespace {
 
@@ -649,6 +653,8 @@ int Encoder::prof_read(double* ms, double* flops, double* bytes, int64_t* count,
 }
 
 int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s) {
+  // PDL (auto mode) for small IRP shards only; scheduling only, results are identical
+  PdlScope pdl(nt <= kPdlMaxTiles);
   const int M = nt * T;
   const float eps = d.ln_eps;
   const bool internvl = d.family == EPD_FAMILY_INTERNVIT_MLP;

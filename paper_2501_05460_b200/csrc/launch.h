@@ -4,8 +4,10 @@
 // (barrier init, TMEM allocation, tensor-map prefetch, weight staging) early; each
 // kernel executes griddepcontrol.wait (pdl_wait) before it touches memory the previous
 // kernel produced or consumes. Because every kernel waits before completing, the
-// ordering is transitive along the stream. Opt-in (EPD_PDL=1): it measured neutral on the
-// power-capped C2 step and made the InternViT (C5) step erratic (671-900 vs 1135 tiles/s).
+// ordering is transitive along the stream. EPD_PDL=1 forces it on, EPD_PDL=0 off; by default
+// (auto) the encoder turns it on only for small chunks (PdlScope), where launch ramps are a
+// large share of every kernel: a 1-3 tile IRP shard runs 4-6 % faster, while on 10-tile
+// chunks it cost 6 % on the power-capped C2 step and made C5 erratic (671-900 vs 1135 tiles/s).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -15,14 +17,30 @@
 
 namespace epd {
 
-inline bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
+// -1 auto, 0 off, 1 on
+inline int pdl_mode() {
+  static int v = -2;
+  if (v == -2) {
     const char* e = std::getenv("EPD_PDL");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = (e && e[0]) ? (e[0] == '1' ? 1 : 0) : -1;
   }
-  return v != 0;
+  return v;
 }
+
+// auto-mode decision for the launches this thread is issuing (set by PdlScope)
+inline thread_local bool g_pdl_auto = false;
+
+inline bool pdl_enabled() {
+  const int m = pdl_mode();
+  return m < 0 ? g_pdl_auto : m == 1;
+}
+
+// Scoped auto-mode choice (restores the previous one on exit).
+struct PdlScope {
+  bool prev;
+  explicit PdlScope(bool on) : prev(g_pdl_auto) { g_pdl_auto = on; }
+  ~PdlScope() { g_pdl_auto = prev; }
+};
 
 template <typename... KArgs, typename... Args>
 int launch_kernel(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, int cluster,
