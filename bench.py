@@ -229,6 +229,8 @@ def run_ours(args, wl, world, rank, local):
     if wl["cache"] and rank == 0:
         cache = MMTokenCache(capacity=max(n, 750), tokens_per_tile=cfg.out_tokens, hidden=cfg.out_dim, device=dev)
     stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache)
+    if world > 1 and os.environ.get("EPD_GATHER", "peer") != "nccl":
+        stage.enable_peer_gather(max(n, 16))  # shards stored into the prefill GPU over NVLink
 
     tiles_host = tiles_for_request(n, cfg, seed=20260808, repeat_period=wl["repeat"]).pin_memory()
     image_host = None
@@ -408,6 +410,7 @@ def run_ours(args, wl, world, rank, local):
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": wl["desc"], "encoder": cfg.name, "tiles_per_request": n,
                    "irp_width": world, "prefill_rank": 0, "parallelism": f"irp{world}",
+                   "ep_transport": stage.transport,
                    "l2": "working set > L2 (0.97 GB bf16 weights + ~0.5 GB activations streamed per step)",
                    "weights": "random-init N(0,0.02), seed 20260808"},
         "p50_ttft_ms": prefill["p50_ttft_ms"] if prefill else p50_ttft,
@@ -497,9 +500,9 @@ NVLINK_GBPS = 900.0  # NVLink 5 per GPU per direction (nominal; MEASURED_PEAKS.j
 
 def gather_bench(stage, cfg, n, world, rank, dev, args):
     """The EP exchange alone (engine.py:521-526 bytes): every encode rank's shard of
-    post-projector MM tokens -> the prefill rank at its tile offset (EncodeStage._gather,
-    NCCL grouped P2P over NVLink), timed on the device over K requests, max over ranks.
-    Roofline: bytes into the prefill GPU / time against the NVLink ingress bandwidth."""
+    post-projector MM tokens -> the prefill rank at its tile offset (EncodeStage.gather_only:
+    NVLink peer-memory stores, or NCCL grouped P2P with EPD_GATHER=nccl), timed on the
+    device over K requests, max over ranks. Roofline: bytes into the prefill GPU / time against the NVLink ingress bandwidth."""
     import torch.distributed as dist
 
     from paper_2501_05460_b200.routing import ep_bytes, shard_ranges
@@ -510,9 +513,8 @@ def gather_bench(stage, cfg, n, world, rank, dev, args):
         return {"bytes_per_request": 0, "note": "single GPU: the shard is written in place into the packed buffer"}
     first, count = ranges[rank]
     local = torch.randn(max(count, 1), cfg.out_tokens, cfg.out_dim, device=dev).to(torch.bfloat16)[:count]
-    dest = torch.empty(n, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16, device=dev) if rank == 0 else None
     for _ in range(args.warmup):
-        stage._gather(local if count else None, dest, ranges)
+        stage.gather_only(local if count else None, n)
     torch.cuda.synchronize()
     ts = []
     for _ in range(max(args.steps, 20)):
@@ -520,7 +522,7 @@ def gather_bench(stage, cfg, n, world, rank, dev, args):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        stage._gather(local if count else None, dest, ranges)
+        stage.gather_only(local if count else None, n)
         b.record()
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
@@ -530,7 +532,10 @@ def gather_bench(stage, cfg, n, world, rank, dev, args):
     gbs = into_sink / (ms / 1e3) / 1e9
     return {"bytes_per_request": into_sink, "p50_ms": ms, "GBps": gbs, "peak_GBps": NVLINK_GBPS,
             "frac": gbs / NVLINK_GBPS, "peak_source": "nominal NVLink 5 ingress per GPU",
-            "path": "NCCL grouped P2P (batch_isend_irecv) into the prefill rank at tile offsets"}
+            "path": ("16 B stores into the prefill GPU's packed slot over NVLink peer memory (CUDA IPC) + "
+                     "per-rank sequence flags, stream-memop waits (peer.py)") if stage.transport == "nvlink-peer"
+            else "NCCL grouped P2P (batch_isend_irecv) into the prefill rank at tile offsets",
+            "transport": stage.transport}
 
 
 def stage_tiles_per_rank(n: int, world: int, rank: int) -> int:

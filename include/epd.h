@@ -169,6 +169,30 @@ epd_status_t epd_kv_unpack(const void* in, int32_t segments, int64_t segment_str
                            int64_t block_bytes, const int32_t* block_ids, int32_t nblocks, void* cache,
                            void* stream);
 
+/* ------------------------------------------------------------------ EP gather over peer memory
+ * The B200-native transport for the encode -> prefill MM-token transfer
+ * (engine._send_ready_shards / _schedule_transfer, engine.py:511-526; arrival accounting
+ * _on_transfer_end("ep"), engine.py:424-435). The prefill rank exports its packed-token
+ * slots and per-rank flags with CUDA IPC; each encode rank maps them, stores its shard at
+ * the shard's tile offset over NVLink (epd_peer_put) and raises its flag; the prefill
+ * rank's stream waits on its local flags (epd_stream_wait_geq). Buffers shared this way
+ * come from epd_peer_alloc (zero-filled, allocation base = the pointer). */
+epd_status_t epd_peer_alloc(int64_t bytes, void** ptr);
+epd_status_t epd_peer_free(void* ptr);
+/* handle: 64 bytes (cudaIpcMemHandle_t) for a pointer returned by epd_peer_alloc. */
+epd_status_t epd_peer_export(void* ptr, void* handle);
+/* Map another process's exported allocation into this device's address space. */
+epd_status_t epd_peer_open(const void* handle, void** ptr);
+epd_status_t epd_peer_close(void* ptr);
+/* dst[0:bytes] = src[0:bytes] (16-byte aligned; dst may be a peer mapping), then, when
+ * flag is non-null, *flag = value once the bytes are visible system-wide. */
+epd_status_t epd_peer_put(const void* src, void* dst, int64_t bytes, uint32_t* flag, uint32_t value,
+                          void* stream);
+/* *flag = value (release, system scope) after the stream's earlier work. */
+epd_status_t epd_peer_signal(uint32_t* flag, uint32_t value, void* stream);
+/* The stream's later work waits until *flag >= value (flag in this device's memory). */
+epd_status_t epd_stream_wait_geq(const uint32_t* flag, uint32_t value, void* stream);
+
 /* ------------------------------------------------------------------ kernel-level ops
  * The building blocks epd_encode_tiles is made of, exported for per-kernel
  * parity tests and profiling. All tensors are device bf16 unless stated.

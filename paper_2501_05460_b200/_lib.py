@@ -73,6 +73,14 @@ _SIGS = {
     "epd_mmcache_check": (_i32, [_vp, _vp]),
     "epd_gather_records": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
     "epd_scatter_records": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
+    "epd_peer_alloc": (_i32, [_i64, C.POINTER(_vp)]),
+    "epd_peer_free": (_i32, [_vp]),
+    "epd_peer_export": (_i32, [_vp, _vp]),
+    "epd_peer_open": (_i32, [_vp, C.POINTER(_vp)]),
+    "epd_peer_close": (_i32, [_vp]),
+    "epd_peer_put": (_i32, [_vp, _vp, _i64, _vp, C.c_uint32, _vp]),
+    "epd_peer_signal": (_i32, [_vp, C.c_uint32, _vp]),
+    "epd_stream_wait_geq": (_i32, [_vp, C.c_uint32, _vp]),
     "epd_kv_pack": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp]),
     "epd_kv_unpack": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp]),
     "epd_linear_bf16": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _i32, _vp,

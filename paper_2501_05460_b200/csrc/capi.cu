@@ -342,6 +342,57 @@ epd_status_t epd_scatter_records(const void* src, const int32_t* index, int32_t 
   return cuda_status((int)cudaGetLastError(), "scatter_records");
 }
 
+epd_status_t epd_peer_alloc(int64_t bytes, void** ptr) {
+  if (bytes <= 0 || !ptr) return fail(EPD_ERR_VALUE, "peer_alloc: bytes must be > 0");
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, (size_t)bytes);
+  if (e != cudaSuccess) {
+    if (p) cudaFree(p);
+    return cuda_status((int)e, "peer_alloc");
+  }
+  *ptr = p;
+  return EPD_OK;
+}
+
+epd_status_t epd_peer_free(void* ptr) { return cuda_status((int)cudaFree(ptr), "peer_free"); }
+
+epd_status_t epd_peer_export(void* ptr, void* handle) {
+  if (!ptr || !handle) return fail(EPD_ERR_VALUE, "peer_export: null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e != cudaSuccess) return cuda_status((int)e, "peer_export (cudaIpcGetMemHandle)");
+  std::memcpy(handle, &h, sizeof(h));
+  return EPD_OK;
+}
+
+epd_status_t epd_peer_open(const void* handle, void** ptr) {
+  if (!handle || !ptr) return fail(EPD_ERR_VALUE, "peer_open: null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  const cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return cuda_status((int)e, "peer_open (cudaIpcOpenMemHandle)");
+}
+
+epd_status_t epd_peer_close(void* ptr) { return cuda_status((int)cudaIpcCloseMemHandle(ptr), "peer_close"); }
+
+epd_status_t epd_peer_put(const void* src, void* dst, int64_t bytes, uint32_t* flag, uint32_t value,
+                          void* stream) {
+  if (bytes < 0) return fail(EPD_ERR_VALUE, "peer_put: negative size");
+  return cuda_status(epd::peer_put(src, dst, (size_t)bytes, flag, value, S(stream)), "peer_put");
+}
+
+epd_status_t epd_peer_signal(uint32_t* flag, uint32_t value, void* stream) {
+  if (!flag) return fail(EPD_ERR_VALUE, "peer_signal: null flag");
+  return cuda_status(epd::peer_signal(flag, value, S(stream)), "peer_signal");
+}
+
+epd_status_t epd_stream_wait_geq(const uint32_t* flag, uint32_t value, void* stream) {
+  if (!flag) return fail(EPD_ERR_VALUE, "stream_wait_geq: null flag");
+  return cuda_status(epd::stream_wait_geq(flag, value, S(stream)), "stream_wait_geq (cuStreamWaitValue32)");
+}
+
 epd_status_t epd_kv_pack(const void* cache, int32_t segments, int64_t segment_stride, int64_t block_bytes,
                          const int32_t* block_ids, int32_t nblocks, void* out, void* stream) {
   return kv_copy(cache, out, segments, segment_stride, block_bytes, block_ids, nblocks, 1, stream);

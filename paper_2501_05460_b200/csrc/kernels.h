@@ -97,6 +97,13 @@ int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int 
                 cudaStream_t stream);
 
 // Gather equal-sized byte records: dst[i] = src_base[index[i]] (record = bytes).
+// EP gather over NVLink peer memory (peer.cu): 16 B copy into a (possibly peer-mapped)
+// destination + system fence, then *flag = value (release, system scope) when flag != 0.
+int peer_put(const void* src, void* dst, size_t bytes, uint32_t* flag, uint32_t value, cudaStream_t s);
+int peer_signal(uint32_t* flag, uint32_t value, cudaStream_t s);
+// The stream waits until *flag >= value (cuStreamWaitValue32, GEQ; flag in local memory).
+int stream_wait_geq(const uint32_t* flag, uint32_t value, cudaStream_t s);
+
 int gather_records(const void* src_base, const int32_t* index, int n, size_t bytes, void* dst,
                    cudaStream_t stream);
 

@@ -88,6 +88,75 @@ class EncodeStage:
         # frees). A ring slot is reused two requests later, after the event that marks its
         # last consumer (the encode for inputs, the readback for packed tokens).
         self._rings: dict = {}
+        # EP gather transport: NCCL grouped P2P by default; enable_peer_gather() switches the
+        # no-cache path to stores over NVLink peer memory (peer.py)
+        self._peer = None
+
+    def enable_peer_gather(self, max_tiles: int, exchange=None) -> bool:
+        """Collective over the stage's ranks: map the prefill rank's packed-token slots
+        (room for ``max_tiles`` tiles) into every encode rank over CUDA IPC so shards are
+        stored straight into them over NVLink (peer.py). Returns False, on every rank, if
+        any rank could not set it up (the NCCL transport then stays in use)."""
+        if self.world == 1 or self.device.type != "cuda":
+            return False
+        from .peer import PeerGather
+        if exchange is None:
+            def exchange(rec):
+                out = [None] * self.world
+                dist.all_gather_object(out, rec, group=self.group)
+                return out
+        slot_bytes = max_tiles * self.cfg.out_tokens * self.cfg.out_dim * 2
+        err = None
+        try:
+            peer = PeerGather(self.device, self.rank, self.world, self.prefill_rank, slot_bytes, exchange)
+        except Exception as e:  # reported on every rank below
+            peer, err = None, f"{type(e).__name__}: {e}"
+        ok = torch.tensor([0 if peer is None else 1], dtype=torch.int32, device=self.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if int(ok.item()) == 1:
+            self._peer = peer
+            self._peer_tiles = max_tiles
+            return True
+        if peer is not None:
+            peer.close()
+        if err:
+            import sys
+            print(f"[rank {self.rank}] peer-memory gather unavailable ({err}); using NCCL P2P", file=sys.stderr)
+        return False
+
+    @property
+    def transport(self) -> str:
+        return "nvlink-peer" if self._peer is not None else ("nccl-p2p" if self.world > 1 else "local")
+
+    def close(self) -> None:
+        if self._peer is not None:
+            self._peer.close()
+            self._peer = None
+
+    def gather_only(self, local: torch.Tensor | None, n: int) -> torch.Tensor | None:
+        """The EP exchange of one n-tile request on its own (bench: the gather's NVLink
+        roofline): ``local`` is this rank's already-encoded shard; returns the packed
+        buffer on the prefill rank."""
+        ranges = shard_ranges(n, self.world)
+        first, count = ranges[self.rank]
+        is_sink = self.rank == self.prefill_rank
+        if self._peer is not None and n <= self._peer_tiles:
+            stream = torch.cuda.current_stream(self.device)
+            seq = self._peer.begin()
+            if is_sink:
+                packed, _ = self._peer.packed(seq, n, self.cfg.out_tokens, self.cfg.out_dim, stream)
+                if count > 0:
+                    packed[first:first + count].copy_(local)
+                self._peer.wait(seq, ranges, stream)
+                return packed
+            if count > 0:
+                self._peer.put(seq, local, first, stream)
+            return None
+        dest = self._buffer(n) if is_sink else None
+        if is_sink and count > 0:
+            dest[first:first + count].copy_(local)
+        self._gather(local if count > 0 else None, dest, ranges)
+        return dest
 
     # ------------------------------------------------------------------ helpers
     def _tokens_shape(self, n: int):
@@ -144,7 +213,7 @@ class EncodeStage:
         if r["free"][k] is not None:
             torch.cuda.current_stream(self.device).wait_event(r["free"][k])
             r["free"][k] = None
-        return r["bufs"][k], (r, k)
+        return r["bufs"][k], (lambda ev: r["free"].__setitem__(k, ev))
 
     def _readback(self, tokens: torch.Tensor, out_host: torch.Tensor, slot=None) -> torch.cuda.Event:
         """Packed tokens -> pinned host buffer on the download stream, after the compute
@@ -156,8 +225,7 @@ class EncodeStage:
             ev = torch.cuda.Event()
             ev.record(self._down)
         if slot is not None:
-            r, k = slot
-            r["free"][k] = ev  # the slot's next encode waits for this readback
+            slot(ev)  # the slot's next use waits for this readback
         else:
             tokens.record_stream(self._down)
         return ev
@@ -230,7 +298,16 @@ class EncodeStage:
         if self.cache is None:
             ranges = shard_ranges(n, self.world)
             first, count = ranges[self.rank]
-            packed, slot = self._packed(n) if is_sink else (None, None)
+            peer = self._peer if (self._peer is not None and n <= self._peer_tiles) else None
+            if peer is not None:
+                compute = torch.cuda.current_stream(self.device)
+                seq = peer.begin()
+                packed, slot = None, None
+                if is_sink:
+                    packed, ps = peer.packed(seq, n, tpp, self.cfg.out_dim, compute)
+                    slot = (lambda ev, ps=ps: peer.set_free_event(ps, ev))
+            else:
+                packed, slot = self._packed(n) if is_sink else (None, None)
             local = None
             if count > 0:
                 release = None
@@ -242,7 +319,12 @@ class EncodeStage:
                 self.enc.encode(src.contiguous(), local)
                 if release is not None:
                     release()
-            self._gather(local, packed, ranges)
+            if peer is None:
+                self._gather(local, packed, ranges)
+            elif is_sink:
+                peer.wait(seq, ranges, compute)  # every other shard has landed in the slot
+            elif count > 0:
+                peer.put(seq, local, first, compute)  # stores over NVLink + this rank's flag
             res._slot = slot
             res.encoded_tiles = count
             res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]

@@ -63,13 +63,19 @@ def _worker(rank, world, port, n, q):
         tiles = torch.randint(0, 256, (n, 8, 8, 3), dtype=torch.uint8, generator=g)
         enc = _StandInEncoder()
         st = EncodeStage(enc, torch.device("cpu"), rank=rank, world=world, prefill_rank=0)
+        # the peer-memory transport needs CUDA IPC: a CPU stage keeps the collective path
+        assert not st.enable_peer_gather(16) and st.transport == "nccl-p2p"
         res = st.process(tiles, rid=7)
         first, count = shard_ranges(n, world)[rank]
-        out = {"rank": rank, "encoded": res.encoded_tiles, "calls": enc.calls,
+        out = {"rank": rank, "encoded": res.encoded_tiles, "calls": enc.calls[:],
                "shards": [(s.worker, s.patches) for s in res.shards], "ep_bytes": res.ep_bytes}
+        # the exchange on its own (bench.py gather_bench): a pre-encoded shard -> packed buffer
+        local = _expected(tiles[first:first + count]) if count else None
+        gathered = st.gather_only(local, n)
         if rank == 0:
             out["tokens"] = res.tokens.float()
             out["expected"] = _expected(tiles).float()
+            out["gathered"] = gathered.float()
         q.put(out)
     finally:
         dist.destroy_process_group()
@@ -96,3 +102,4 @@ def test_irp_gather_request_order(world, n):
     # EP bytes: every non-prefill shard, tokens_per_tile * hidden * 2 bytes per tile (engine.py:524)
     assert outs[0]["ep_bytes"] == sum(c for k, (_, c) in enumerate(ranges) if k != 0) * 4 * 8 * 2
     assert torch.equal(outs[0]["tokens"], outs[0]["expected"])
+    assert torch.equal(outs[0]["gathered"], outs[0]["expected"])
