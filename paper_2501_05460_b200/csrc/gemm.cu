@@ -239,6 +239,7 @@ EPD_DEVICE TileAt tile_at(const TileSched& s, int t, int BN) {
 template <int BN, int KIND, int CG, int CL>
 __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmBh,
                      const __grid_constant__ CUtensorMap tmO0, const __grid_constant__ CUtensorMap tmO1,
                      const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep,
                      const TileSched sched) {
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmBh);
   }
   if (warp == 1) {
     if (CG == 2) tmem_alloc_pair(tmem_holder, Cfg::TMEM_COLS);
@@ -297,23 +299,26 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     for (int tile = pid; tile < num_tiles; tile += npid) {
       const TileAt x = tile_at(sched, tile, BN);
       const int m0 = x.mt * (kBM * CL) + crank_full * kBM;
-      // each CTA of a pair holds half of the tile's B rows (a half tile uses the first
-      // w/2 rows of each CTA's fixed-size box)
+      // each CTA of a pair holds half of the tile's B rows; a half-width tile loads only
+      // the first half of each CTA's box (tmBh), which is all its MMAs read
       const int n0 = x.n0 + crank * (x.w / CG);
+      const bool hw = x.w != BN;
+      const CUtensorMap* tb = hw ? &tmBh : &tmB;
+      const uint32_t stage_bytes = Cfg::A_BYTES + (hw ? Cfg::B_BYTES / 2 : Cfg::B_BYTES);
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
           if (CG == 1) {
-            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], stage_bytes);
             tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
-            tma_load_2d(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+            tma_load_2d(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0);
           } else {
-            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
             if (CL == 2)
-              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0);
+              tma_load_2d_pair(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0);
             else if (pair == 0)  // this half of B, for both pairs
-              tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * kBK, n0,
+              tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0,
                                   (uint16_t)((1u << crank) | (1u << (crank + 2))));
           }
         }
@@ -659,11 +664,14 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
            cudaStream_t stream) {
   constexpr int CG = CL == 1 ? 1 : 2;
   using Cfg = GemmCfg<BN, CG>;
-  CUtensorMap ta, tb, t0, t1, t2;
+  CUtensorMap ta, tb, tbh, t0, t1, t2;
   int rc = make_tmap_2d(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * 2, kBK, kBM,
                         CU_TENSOR_MAP_SWIZZLE_128B);
   if (!rc)
     rc = make_tmap_2d(&tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN / CG, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (!rc)  // half-width tiles (BN in {128, 256}; otherwise never used)
+    rc = make_tmap_2d(&tbh, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb * 2, kBK, BN / CG / 2,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   if (KIND == EK_ROWS_BF16 || KIND == EK_SWIGLU) {
     rc = make_tmap_2d(&t0, ep.out, (uint64_t)(KIND == EK_SWIGLU ? N / 2 : N), (uint64_t)M, (uint64_t)ep.ldo * 2,
@@ -703,7 +711,7 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   int units = cap;
   if (sched.total < units) units = sched.total;
   const int rc2 = launch_kernel(gemm_bf16_kernel<BN, KIND, CG, CL>, dim3(units * CL), dim3(Cfg::THREADS),
-                                Cfg::SMEM, stream, CL, ta, tb, t0, t1, t2, M, N, K, ep, sched);
+                                Cfg::SMEM, stream, CL, ta, tb, tbh, t0, t1, t2, M, N, K, ep, sched);
   if (rc2) return rc2;
   return (int)cudaGetLastError();
 }
