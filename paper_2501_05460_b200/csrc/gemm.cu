@@ -70,6 +70,10 @@ EPD_DEVICE float gelu_tanh_fast(float x) {
 //   SWIGLU    : 64-column groups (gate 32 | up 32) -> 32 bf16 columns at n/2 (as ROWS_BF16)
 enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS = 3, EK_SWIGLU = 4 };
 
+#ifndef EPD_GEMM_EXP
+#define EPD_GEMM_EXP 0  // A/B experiments only (tools/build_variant.sh -DEPD_GEMM_EXP=n)
+#endif
+
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
 
 template <int BN, int CG>
@@ -307,7 +311,12 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       const uint32_t stage_bytes = Cfg::A_BYTES + (hw ? Cfg::B_BYTES / 2 : Cfg::B_BYTES);
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
+#if EPD_GEMM_EXP == 1  // experiment: no operand loads (MMA + epilogue alone)
+        if (elect_one() && crank == 0) mbar_arrive(&full[stage]);
+        if (false) {
+#else
         if (elect_one()) {
+#endif
           if (CG == 1) {
             mbar_arrive_expect_tx(&full[stage], stage_bytes);
             tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           const uint64_t bo = b0 + (uint64_t)((stage * Cfg::B_BYTES) >> 4);
           if (elect_one()) {
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
+            for (int k = 0; k < (EPD_GEMM_EXP == 2 ? 0 : kBK / 16); ++k) {  // EXP 2: no MMAs
               if (CG == 2) umma_bf16_pair(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
               else umma_bf16(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
             }
@@ -405,7 +414,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * hw; c < (half + 1) * hw; c += (KIND == EK_SWIGLU ? 64 : 32)) {
+      for (int c = half * hw; c < (EPD_GEMM_EXP == 3 ? 0 : (half + 1) * hw);  // EXP 3: no epilogue
+           c += (KIND == EK_SWIGLU ? 64 : 32)) {
         const int n = n0 + c;
         if (n >= N) break;  // warp-uniform
         float x[32];
@@ -506,13 +516,15 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           if (!(pon[0] && !pdirect[0]) && !(pon[1] && !pdirect[1])) continue;  // nothing staged
         }
         // the previous TMA store(s) must have finished reading the staging buffer
+        // (double-buffering the bf16 chunks measured neutral)
+        uint8_t* sbuf = stg;
         if (leader) bulk_wait_read0();
         named_bar(bar_id, 128);
         if (KIND == EK_ROWS_BF16 || KIND == EK_SWIGLU) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int phys = j ^ ((r >> 1) & 3);
-            *reinterpret_cast<uint4*>(stg + r * 64 + phys * 16) =
+            *reinterpret_cast<uint4*>(sbuf + r * 64 + phys * 16) =
                 make_uint4(pack_bf16x2(x[8 * j + 0], x[8 * j + 1]), pack_bf16x2(x[8 * j + 2], x[8 * j + 3]),
                            pack_bf16x2(x[8 * j + 4], x[8 * j + 5]), pack_bf16x2(x[8 * j + 6], x[8 * j + 7]));
           }
@@ -549,9 +561,9 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         named_bar(bar_id, 128);
         if (leader) {
           if (KIND == EK_ROWS_BF16 || KIND == EK_ROWS_F32) {
-            tma_store_2d(&tmO0, stg, n, m0);
+            tma_store_2d(&tmO0, sbuf, n, m0);
           } else if (KIND == EK_SWIGLU) {
-            tma_store_2d(&tmO0, stg, n / 2, m0);
+            tma_store_2d(&tmO0, sbuf, n / 2, m0);
           } else if (KIND == EK_ACC_F32) {
             tma_reduce_add_2d(&tmO0, stg, n, m0);
           } else {
