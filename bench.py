@@ -399,6 +399,8 @@ def run_ours(args, wl, world, rank, local):
         traffic = json.loads(tj.read_text()).get(wl["cfg"].name, {}).get("gemm_dram_bytes_per_launch")
 
     launches_per_step = enc.launches(stage_tiles_per_rank(n, world, rank)) + (2 if cache is not None else 0)
+    if stage.transport == "nvlink-peer":
+        launches_per_step += world - 1  # the prefill rank's release-flag stores (peer.py)
     model = cfg.geometry.name
     total_tokens = n * cfg.out_tokens + PROMPT_TOKENS
     prefill_ms = modeled_prefill_s(model, total_tokens) * 1e3 if model in PREFILL_COST else None

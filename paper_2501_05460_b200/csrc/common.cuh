@@ -70,6 +70,12 @@ EPD_DEVICE void fence_proxy_async_smem() {
 }
 
 // ---------------------------------------------------------------- TMA
+// L2 prefetch of one 2-D box (no shared-memory destination, no barrier)
+EPD_DEVICE void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
 EPD_DEVICE void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

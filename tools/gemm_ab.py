@@ -28,9 +28,9 @@ CL = int(os.environ.get("CL", "0"))
 if CL:
     from paper_2501_05460_b200._lib import call as _call
     _call("epd_set_gemm_cta_group", CL)
-tag += f"/bn{BN}/cl{CL}"
+tag += f"/bn{BN}/cl{CL}/M{os.environ.get('M', '10240')}"
 dev = torch.device("cuda")
-M = 10240
+M = int(os.environ.get("M", "10240"))
 line = []
 for (N, K, act, name, acc) in [(3840, 1152, "none", "qkv", False), (1152, 1152, "none", "o+acc", True),
                                (4304, 1152, "gelu_tanh", "fc1", False), (1152, 4304, "none", "fc2+acc", True),
