@@ -214,9 +214,15 @@ EPD_DEVICE AttnItem attn_item(const AttnParams& p, int w, int nqp, int npairs_ma
   it.nkb = (kend + 63) / 64;
   return it;
 }
-// Number of items and pairs kept whole for a persistent grid of G CTAs.
+// Number of items and pairs kept whole for a persistent grid of G CTAs. The r pairs of a
+// last, partial round are split only when their 2r single tiles still fit in one round: a
+// single-tile item takes ~0.6 of a pair's time (its softmax is latency-bound), so two
+// rounds of singles would be slower than the one round of pairs (a 2-tile IRP shard:
+// 128 pairs on 148 SMs). The rule is stable under G -> min(items, G), so the kernel
+// recomputes the host's schedule from gridDim.x.
 __host__ __device__ inline void attn_sched(int npairs, int G, int nq_max, int* main_pairs, int* nitems) {
-  const int m = nq_max > 1 ? (npairs / G) * G : npairs;
+  int m = nq_max > 1 ? (npairs / G) * G : npairs;
+  if (2 * (npairs - m) > G) m = npairs;
   *main_pairs = m;
   *nitems = m + 2 * (npairs - m);
 }
