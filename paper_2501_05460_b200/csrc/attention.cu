@@ -23,6 +23,7 @@
 // Q/K are K-major smem operands (64-wide SW128 atoms + a 16-wide SW32 tail when
 // Dp % 64 != 0); V is the MN-major B operand from 16-wide SW32 atoms (LBO = 2 KB
 // between atoms, SBO = 256 B between 8-key groups).
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -230,11 +231,15 @@ EPD_DEVICE AttnItem attn_item(const AttnParams& p, int w, int nqp, int npairs_ma
 // last, partial round are split only when their 2r single tiles still fit in one round: a
 // single-tile item takes ~0.6 of a pair's time (its softmax is latency-bound), so two
 // rounds of singles would be slower than the one round of pairs (a 2-tile IRP shard:
-// 128 pairs on 148 SMs). The rule is stable under G -> min(items, G), so the kernel
-// recomputes the host's schedule from gridDim.x.
-__host__ __device__ inline void attn_sched(int npairs, int G, int nq_max, int* main_pairs, int* nitems) {
+// 128 pairs on 148 SMs). The host passes the schedule (pairs kept whole) to the kernel.
+// EPD_ATTN_SPLIT=0 keeps every pair whole, =1 always splits the partial round (A/B runs).
+inline void attn_sched(int npairs, int G, int nq_max, int* main_pairs, int* nitems) {
+  static const int mode = [] {
+    const char* e = std::getenv("EPD_ATTN_SPLIT");
+    return e && e[0] ? atoi(e) : -1;
+  }();
   int m = nq_max > 1 ? (npairs / G) * G : npairs;
-  if (2 * (npairs - m) > G) m = npairs;
+  if (mode == 0 || (mode < 0 && 2 * (npairs - m) > G)) m = npairs;
   *main_pairs = m;
   *nitems = m + 2 * (npairs - m);
 }
@@ -246,7 +251,7 @@ template <int DP, int NQ>
 __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     attention_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmQt,
                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmKt,
-                     const __grid_constant__ CUtensorMap tmV, const AttnParams p) {
+                     const __grid_constant__ CUtensorMap tmV, const AttnParams p, const int pmain) {
   using C = Cfg<DP, NQ>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -270,8 +275,7 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
   const int warp = warp_id();
   const int lane = lane_id();
   const int nqp = (p.Tq + NQ * 128 - 1) / (NQ * 128);
-  int pmain, nitems;
-  attn_sched(nqp * p.H * p.B, gridDim.x, NQ, &pmain, &nitems);
+  const int nitems = pmain + 2 * (nqp * p.H * p.B - pmain);
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -694,13 +698,11 @@ int launch_attn(const AttnParams& p, cudaStream_t stream) {
     attr_set = true;
   }
   const int npairs = ((p.Tq + NQ * 128 - 1) / (NQ * 128)) * p.H * p.B;
-  // (the kernel recomputes the same schedule from gridDim.x: with fewer items than SMs,
-  // every pair is split and the grid is the item count)
   int pmain = 0, nitems = 0;
   attn_sched(npairs, num_sms(), NQ, &pmain, &nitems);
   const int grid = nitems < num_sms() ? nitems : num_sms();
   return launch_kernel(attention_kernel<DP, NQ>, dim3(grid), dim3(C::THREADS), C::SMEM, stream, 1, mq, mqt, mk, mkt,
-                       mv, p);
+                       mv, p, pmain);
 }
 
 }  // namespace
