@@ -1,4 +1,5 @@
-"""Repeated pipelined e2e loops (C2) to characterise run-to-run variance."""
+"""Repeated pipelined e2e loops (C2) to characterise run-to-run variance and attribute the
+e2e cost (h2d: uploads only, d2h: readbacks only)."""
 import sys
 from pathlib import Path
 
@@ -21,13 +22,17 @@ for _ in range(5):
     stage.process(None, tiles_dev=td)
 torch.cuda.synchronize()
 for rep in range(6):
-    for mode in ("resident", "e2e"):
+    for mode in ("resident", "e2e", "h2d", "d2h"):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         for _ in range(20):
             if mode == "e2e":
                 stage.process(th, out_host=oh)
+            elif mode == "h2d":
+                stage.process(th)
+            elif mode == "d2h":
+                stage.process(None, tiles_dev=td, out_host=oh)
             else:
                 stage.process(None, tiles_dev=td)
         stage.join()
