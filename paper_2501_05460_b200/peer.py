@@ -76,26 +76,44 @@ class PeerGather:
         self._owned: list[int] = []
         self._opened: list[int] = []
         with torch.cuda.device(self.device):
-            rel = self._own(4 * SLOTS)
-            rec = {"pid": os.getpid(), "rank": rank, "rel": (rel, _export(rel))}
-            if rank == sink:
-                slots = self._own(SLOTS * self.slot_bytes)
-                flags = self._own(4 * world)
-                rec["slots"] = (slots, _export(slots))
-                rec["data"] = (flags, _export(flags))
+            # every rank takes part in exactly one exchange, even if its own setup failed, so
+            # a local failure surfaces on all ranks instead of leaving peers in the collective
+            rec = {"pid": os.getpid(), "rank": rank}
+            try:
+                rel = self._own(4 * SLOTS)
+                rec["rel"] = (rel, _export(rel))
+                if rank == sink:
+                    slots = self._own(SLOTS * self.slot_bytes)
+                    flags = self._own(4 * world)
+                    rec["slots"] = (slots, _export(slots))
+                    rec["data"] = (flags, _export(flags))
+            except Exception as e:
+                rec["error"] = f"{type(e).__name__}: {e}"
             recs = exchange(rec)
             if [r["rank"] for r in recs] != list(range(world)):
+                self.close()
                 raise RuntimeError("peer gather: exchange must return one record per rank in rank order")
+            bad = [f"rank {r['rank']}: {r['error']}" for r in recs if "error" in r]
+            if bad:
+                self.close()
+                raise RuntimeError("peer gather setup failed: " + "; ".join(bad))
             self.rel_local = rel
-            if rank == sink:
-                self.slots = slots
-                self.data_local = flags
-                self.rel_remote = {k: self._map(recs[k]["rel"], recs[k]["pid"]) for k in range(world) if k != sink}
-                self._slot_u8 = torch.as_tensor(_Cai(slots, SLOTS * self.slot_bytes), device=self.device)
-                self._free = [None] * SLOTS  # per-slot event of its last readback
-            else:
-                self.slots_remote = self._map(recs[sink]["slots"], recs[sink]["pid"])
-                self.data_remote = self._map(recs[sink]["data"], recs[sink]["pid"])
+            # a failure to map a peer's buffer is local; EncodeStage.enable_peer_gather agrees
+            # on the outcome with one all_reduce
+            try:
+                if rank == sink:
+                    self.slots = slots
+                    self.data_local = flags
+                    self.rel_remote = {k: self._map(recs[k]["rel"], recs[k]["pid"])
+                                       for k in range(world) if k != sink}
+                    self._slot_u8 = torch.as_tensor(_Cai(slots, SLOTS * self.slot_bytes), device=self.device)
+                    self._free = [None] * SLOTS  # per-slot event of its last readback
+                else:
+                    self.slots_remote = self._map(recs[sink]["slots"], recs[sink]["pid"])
+                    self.data_remote = self._map(recs[sink]["data"], recs[sink]["pid"])
+            except Exception:
+                self.close()
+                raise
 
     # ------------------------------------------------------------------ setup helpers
     def _own(self, nbytes: int) -> int:
@@ -112,6 +130,8 @@ class PeerGather:
         return p
 
     def close(self) -> None:
+        if not (self._opened or self._owned):
+            return
         torch.cuda.synchronize(self.device)
         for p in self._opened:
             call("epd_peer_close", C.c_void_p(p))

@@ -107,7 +107,7 @@ class EncodeStage:
                 return out
         slot_bytes = max_tiles * self.cfg.out_tokens * self.cfg.out_dim * 2
         err = None
-        try:
+        try:  # PeerGather runs exactly one exchange on every rank, failed or not
             peer = PeerGather(self.device, self.rank, self.world, self.prefill_rank, slot_bytes, exchange)
         except Exception as e:  # reported on every rank below
             peer, err = None, f"{type(e).__name__}: {e}"

@@ -217,3 +217,31 @@ def test_peer_ipc_two_processes(cuda):
     for p in procs:
         p.join(timeout=30)
     assert all(o == ("ok", True) for o in outs), outs
+
+
+def test_peer_setup_failure_is_reported_on_every_rank(cuda):
+    """A rank whose allocation fails still takes part in the one exchange, so every rank
+    raises the same error instead of a peer waiting forever in the collective."""
+    from paper_2501_05460_b200.peer import PeerGather
+    world = 2
+    recs = [None] * world
+    bar = threading.Barrier(world)
+    errs = [None] * world
+
+    def make(rank):
+        def exchange(rec):
+            recs[rank] = rec
+            bar.wait()
+            return list(recs)
+        try:
+            # the prefill rank (0) asks for an impossible slot; rank 1's setup succeeds
+            PeerGather(cuda, rank, world, 0, (1 << 50) if rank == 0 else 1024, exchange)
+        except Exception as e:
+            errs[rank] = e
+
+    ts = [threading.Thread(target=make, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(isinstance(e, RuntimeError) and "rank 0" in str(e) for e in errs), errs
