@@ -192,7 +192,8 @@ struct Cfg {
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
-// Work items: (query-tile pair, head, image), consecutive pairs sharing (image, head).
+// Work items: (query-tile pair, head, image), consecutive pairs sharing (image, head)
+// (causal: the last query tiles of every head first).
 // Pairs that would form a last, partial round over the persistent CTAs are split into
 // single 128-row tiles, so that round takes about half as long; a single tile past Tq
 // is an empty item (nq = 0) that every role skips without touching a barrier.
@@ -207,8 +208,15 @@ EPD_DEVICE AttnItem attn_item(const AttnParams& p, int w, int nqp, int npairs_ma
     half = (w - npairs_main) & 1;
   }
   AttnItem it;
-  const int qp = pair % nqp;
-  const int bh = pair / nqp;
+  int qp = pair % nqp;
+  int bh = pair / nqp;
+  if (p.causal) {
+    // causal items differ in work (query tile i reads ~i + 1 key blocks): hand them out
+    // longest first, so a CTA's second item is one of the short ones
+    const int nbh = p.H * p.B;
+    qp = nqp - 1 - pair / nbh;
+    bh = pair % nbh;
+  }
   it.h = bh % p.H;
   it.b = bh / p.H;
   it.q0 = qp * (NQ * 128);

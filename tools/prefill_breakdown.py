@@ -29,6 +29,7 @@ for name in ("rmsnorm_f32", "linear", "rope_", "attention", "linear_acc", "silu_
 
     def wrap(*a, _fn=fn, _name=name, **k):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200_000)  # the op's launch queues behind it: the events time the GPU only
         s.record()
         r = _fn(*a, **k)
         e.record()
