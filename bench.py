@@ -501,7 +501,7 @@ def kv_handoff_bench(wl, cfg, n, world, rank, dev, args):
     moved = info["moved_bytes"]
     return {"tokens": total, "pd_bytes": total * geo.kv_bytes_per_token(), "moved_bytes_per_request": moved,
             "ms_per_request": ms, "GBps": moved / (ms / 1e3) / 1e9,
-            "path": "pack -> self-copy -> unpack (same GPU)" if world == 1 else "pack -> NCCL P2P -> unpack",
+            "path": "epd_kv_move: one block-to-block kernel (same GPU)" if world == 1 else "pack -> NCCL P2P -> unpack",
             "note": "whole 16-token blocks move; pd_bytes is the reference's token-exact count (engine.py:553-554)"}
 
 

@@ -169,6 +169,13 @@ epd_status_t epd_kv_unpack(const void* in, int32_t segments, int64_t segment_str
                            int64_t block_bytes, const int32_t* block_ids, int32_t nblocks, void* cache,
                            void* stream);
 
+/* The same handoff without a staging buffer: dst[s][dst_ids[i]] = src[s][src_ids[i]] for
+ * every segment s. dst_cache may be another GPU's pool mapped with epd_peer_open, in which
+ * case this one kernel is the NVLink transfer (prefill pushes into the decode pool). */
+epd_status_t epd_kv_move(const void* src_cache, int64_t src_segment_stride, void* dst_cache,
+                         int64_t dst_segment_stride, int32_t segments, int64_t block_bytes, const int32_t* src_ids,
+                         const int32_t* dst_ids, int32_t nblocks, void* stream);
+
 /* ------------------------------------------------------------------ EP gather over peer memory
  * The B200-native transport for the encode -> prefill MM-token transfer
  * (engine._send_ready_shards / _schedule_transfer, engine.py:511-526; arrival accounting

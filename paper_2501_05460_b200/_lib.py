@@ -81,6 +81,7 @@ _SIGS = {
     "epd_peer_put": (_i32, [_vp, _vp, _i64, _vp, C.c_uint32, _vp]),
     "epd_peer_signal": (_i32, [_vp, C.c_uint32, _vp]),
     "epd_stream_wait_geq": (_i32, [_vp, C.c_uint32, _vp]),
+    "epd_kv_move": (_i32, [_vp, _i64, _vp, _i64, _i32, _i64, _vp, _vp, _i32, _vp]),
     "epd_kv_pack": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp]),
     "epd_kv_unpack": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _vp, _vp]),
     "epd_linear_bf16": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _i32, _vp,

@@ -47,6 +47,22 @@ __global__ void kv_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __restr
     b[v] = a[v];
 }
 
+// Block-to-block KV move (handoff without a staging buffer): for block pair i and segment
+// s, dst[s][dst_ids[i]] = src[s][src_ids[i]]. dst may be a peer mapping of another GPU's
+// pool, so the copy is the NVLink transfer itself.
+__global__ void kv_move_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, long long src_stride,
+                               long long dst_stride, long long block_bytes, const int32_t* __restrict__ src_ids,
+                               const int32_t* __restrict__ dst_ids) {
+  const int i = blockIdx.z;
+  const int s = blockIdx.y;
+  const uint4* a = reinterpret_cast<const uint4*>(src + (long long)s * src_stride + (long long)src_ids[i] * block_bytes);
+  uint4* b = reinterpret_cast<uint4*>(dst + (long long)s * dst_stride + (long long)dst_ids[i] * block_bytes);
+  const long long vecs = block_bytes / 16;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < vecs;
+       v += (long long)gridDim.x * blockDim.x)
+    b[v] = a[v];
+}
+
 __global__ void scatter_records_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ index,
                                        size_t vecs, uint4* __restrict__ dst) {
   const int rec = blockIdx.y;
@@ -391,6 +407,26 @@ epd_status_t epd_peer_signal(uint32_t* flag, uint32_t value, void* stream) {
 epd_status_t epd_stream_wait_geq(const uint32_t* flag, uint32_t value, void* stream) {
   if (!flag) return fail(EPD_ERR_VALUE, "stream_wait_geq: null flag");
   return cuda_status(epd::stream_wait_geq(flag, value, S(stream)), "stream_wait_geq (cuStreamWaitValue32)");
+}
+
+epd_status_t epd_kv_move(const void* src_cache, int64_t src_segment_stride, void* dst_cache,
+                         int64_t dst_segment_stride, int32_t segments, int64_t block_bytes, const int32_t* src_ids,
+                         const int32_t* dst_ids, int32_t nblocks, void* stream) {
+  if (segments < 1 || block_bytes <= 0 || nblocks < 0 || src_segment_stride < block_bytes ||
+      dst_segment_stride < block_bytes)
+    return fail(EPD_ERR_VALUE, "kv move: bad geometry");
+  if (block_bytes % 16 || src_segment_stride % 16 || dst_segment_stride % 16 ||
+      ((reinterpret_cast<uintptr_t>(src_cache) | reinterpret_cast<uintptr_t>(dst_cache)) & 15))
+    return fail(EPD_ERR_VALUE, "kv move: blocks must be 16-byte aligned");
+  if (nblocks == 0) return EPD_OK;
+  if (segments > 65535 || nblocks > 65535) return fail(EPD_ERR_VALUE, "kv move: too many blocks");
+  const long long vecs = block_bytes / 16;
+  int bx = (int)((vecs + 255) / 256);
+  if (bx > 8) bx = 8;
+  kv_move_kernel<<<dim3(bx, segments, nblocks), 256, 0, S(stream)>>>(
+      reinterpret_cast<const uint8_t*>(src_cache), reinterpret_cast<uint8_t*>(dst_cache), src_segment_stride,
+      dst_segment_stride, block_bytes, src_ids, dst_ids);
+  return cuda_status((int)cudaGetLastError(), "kv move");
 }
 
 epd_status_t epd_kv_pack(const void* cache, int32_t segments, int64_t segment_stride, int64_t block_bytes,

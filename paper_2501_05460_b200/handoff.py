@@ -1,4 +1,4 @@
-"""Prefill -> decode KV-block handoff (PD migration) over NCCL.
+"""Prefill -> decode KV-block handoff (PD migration): one block-to-block kernel on a shared GPU, NCCL P2P across GPUs.
 
 Reference seam (relative to /root/reference/pkg/src/disaggsim/):
 ``_try_reserve_decode`` reserves ``total_tokens + output_tokens`` KV tokens on
@@ -9,10 +9,12 @@ the decode instance (engine.py:542-552), schedules a transfer of
 
 Here the KV cache is a real paged pool: ``2 * num_layers`` segments (K and V
 per layer) of ``num_blocks`` blocks, each block = ``block_size`` tokens x
-``kv_heads`` x ``head_dim`` bf16. The prefill rank packs the request's blocks
+``kv_heads`` x ``head_dim`` bf16. Across GPUs the prefill rank packs the request's blocks
 into one contiguous buffer (``epd_kv_pack``), sends it with NCCL P2P, and the
 decode rank unpacks into the block ids its BlockManager reserved
-(``epd_kv_unpack``). Whole blocks move; the reference's byte count is the
+(``epd_kv_unpack``). When prefill and decode share a GPU, one kernel moves every
+block straight from the prefill pool into the decode pool (``epd_kv_move``: half the
+HBM traffic of pack + unpack). Whole blocks move; the reference's byte count is the
 token-exact figure and is reported alongside (``pd_bytes``).
 """
 from __future__ import annotations
@@ -59,6 +61,18 @@ class PagedKVCache:
              self.block_bytes, C.c_void_p(ids.data_ptr()), n, C.c_void_p(out.data_ptr()), self._stream())
         return out
 
+    def move_to(self, dst: "PagedKVCache", src_ids: list[int], dst_ids: list[int]) -> None:
+        """dst.pool[s][dst_ids[i]] = self.pool[s][src_ids[i]] for every segment (one kernel)."""
+        if len(src_ids) != len(dst_ids):
+            raise ValueError("move_to: src and dst block lists differ in length")
+        if (dst.segments, dst.block_elems) != (self.segments, self.block_elems):
+            raise ValueError("move_to: pools of different geometry")
+        n = len(src_ids)
+        ids = torch.tensor(list(src_ids) + list(dst_ids), dtype=torch.int32, device=self.device)
+        call("epd_kv_move", C.c_void_p(self.pool.data_ptr()), self.num_blocks * self.block_bytes,
+             C.c_void_p(dst.pool.data_ptr()), dst.num_blocks * dst.block_bytes, self.segments, self.block_bytes,
+             C.c_void_p(ids.data_ptr()), C.c_void_p(ids.data_ptr() + 4 * n), n, self._stream())
+
     def unpack(self, packed: torch.Tensor, block_ids: list[int]) -> None:
         n = len(block_ids)
         ids = torch.tensor(block_ids, dtype=torch.int32, device=self.device)
@@ -79,14 +93,13 @@ def kv_handoff(rid: int, total_tokens: int, output_tokens: int, src: PagedKVCach
     if rank == src_rank:
         src_ids = src.manager.allocated[rid]
         info["pd_bytes"] = pd_bytes(total_tokens, src.kv_bytes_per_token)
-        packed = src.pack(src_ids)
-        info["moved_bytes"] = packed.numel() * 2
+        info["moved_bytes"] = len(src_ids) * src.segments * src.block_bytes
         if dst_rank == src_rank:
             dst_ids = dst.manager.allocate(rid, total_tokens + output_tokens)
-            dst.unpack(packed, dst_ids[:len(src_ids)])
+            src.move_to(dst, src_ids, dst_ids[:len(src_ids)])
             info["dst_blocks"] = dst_ids
         else:
-            dist.send(packed, dst_rank, group=group)
+            dist.send(src.pack(src_ids), dst_rank, group=group)
         src.manager.free(rid)
     elif rank == dst_rank:
         dst_ids = dst.manager.allocate(rid, total_tokens + output_tokens)
