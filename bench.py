@@ -512,7 +512,8 @@ def gather_bench(stage, cfg, n, world, rank, dev, args):
     """The EP exchange alone (engine.py:521-526 bytes): every encode rank's shard of
     post-projector MM tokens -> the prefill rank at its tile offset (EncodeStage.gather_only:
     NVLink peer-memory stores, or NCCL grouped P2P with EPD_GATHER=nccl), timed on the
-    device over K requests, max over ranks. Roofline: bytes into the prefill GPU / time against the NVLink ingress bandwidth."""
+    device over K requests, max over ranks. Roofline: bytes into the prefill GPU / time
+    against the NVLink ingress bandwidth."""
     import torch.distributed as dist
 
     from paper_2501_05460_b200.routing import ep_bytes, shard_ranges
