@@ -179,8 +179,11 @@ struct Cfg {
   static constexpr int OFF_K = OFF_Q + 2 * NQ * Q_AL;
   static constexpr int OFF_V = OFF_K + KS * K_AL;
   static constexpr int OFF_BAR = OFF_V + KVS * V_AL;
-  static constexpr int OFF_X = OFF_BAR + 256;           // split-item row max / sum exchange
-  static constexpr int SMEM = OFF_X + 1024 + 1024;       // 31 mbarriers + TMEM holder in the 256 B
+  static constexpr int BAR_BYTES = 34 * 8 + 8;          // 34 mbarriers + the TMEM holder
+  static constexpr int OFF_X = OFF_BAR + 512;           // split-item row max / sum exchange
+  static constexpr int X_BYTES = 2 * 128 * 4;           // [2 key halves][128 rows]
+  static constexpr int SMEM = OFF_X + X_BYTES + 1024;   // + slack for the 1024 B base alignment
+  static_assert(BAR_BYTES <= OFF_X - OFF_BAR, "barrier region overlaps the exchange buffer");
   static constexpr int THREADS = 64 + NQ * 128;
   // TMEM columns: S_{g,b} (fp32, 64 wide) at (2g + b) * 64, P_{g,b} = bf16 pairs in its first
   // 32 columns; O_g at 256 + 128 g (DP wide); Q_g (bf16 pairs, DP/2 wide) right after O_g.
