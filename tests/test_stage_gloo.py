@@ -73,9 +73,11 @@ def _worker(rank, world, port, n, q):
         local = _expected(tiles[first:first + count]) if count else None
         gathered = st.gather_only(local, n)
         if rank == 0:
-            out["tokens"] = res.tokens.float()
-            out["expected"] = _expected(tiles).float()
-            out["gathered"] = gathered.float()
+            # numpy arrays pickle by value (torch tensors would travel as shared-memory fds
+            # that the parent can only open while this process is still alive)
+            out["tokens"] = res.tokens.float().numpy()
+            out["expected"] = _expected(tiles).float().numpy()
+            out["gathered"] = gathered.float().numpy()
         q.put(out)
     finally:
         dist.destroy_process_group()
@@ -101,5 +103,5 @@ def test_irp_gather_request_order(world, n):
         assert o["shards"] == [(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
     # EP bytes: every non-prefill shard, tokens_per_tile * hidden * 2 bytes per tile (engine.py:524)
     assert outs[0]["ep_bytes"] == sum(c for k, (_, c) in enumerate(ranges) if k != 0) * 4 * 8 * 2
-    assert torch.equal(outs[0]["tokens"], outs[0]["expected"])
-    assert torch.equal(outs[0]["gathered"], outs[0]["expected"])
+    assert (outs[0]["tokens"] == outs[0]["expected"]).all()
+    assert (outs[0]["gathered"] == outs[0]["expected"]).all()
