@@ -24,7 +24,6 @@
 // Dp % 64 != 0); V is the MN-major B operand from 16-wide SW32 atoms (LBO = 2 KB
 // between atoms, SBO = 256 B between 8-key groups).
 #include <cstdlib>
-#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -127,16 +126,7 @@ EPD_DEVICE void tmem_st32(uint32_t taddr, const uint32_t* r) {
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
-EPD_DEVICE void tmem_st16(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
 EPD_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-EPD_DEVICE void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // Warp-wide issue helpers: every lane executes the call with identical (warp-uniform)
 // operands, so the compiler keeps them in uniform registers; elect.sync picks the one
@@ -179,11 +169,9 @@ struct Cfg {
   static constexpr int OFF_K = OFF_Q + 2 * NQ * Q_AL;
   static constexpr int OFF_V = OFF_K + KS * K_AL;
   static constexpr int OFF_BAR = OFF_V + KVS * V_AL;
-  static constexpr int BAR_BYTES = 34 * 8 + 8;          // 34 mbarriers + the TMEM holder
-  static constexpr int OFF_X = OFF_BAR + 512;           // split-item row max / sum exchange
-  static constexpr int X_BYTES = 2 * 128 * 4;           // [2 key halves][128 rows]
-  static constexpr int SMEM = OFF_X + X_BYTES + 1024;   // + slack for the 1024 B base alignment
-  static_assert(BAR_BYTES <= OFF_X - OFF_BAR, "barrier region overlaps the exchange buffer");
+  static constexpr int BAR_BYTES = 34 * 8 + 8;         // 34 mbarriers + the TMEM holder
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;     // + slack for the 1024 B base alignment
+  static_assert(BAR_BYTES <= 512, "barrier region");
   static constexpr int THREADS = 64 + NQ * 128;
   // TMEM columns: S_{g,b} (fp32, 64 wide) at (2g + b) * 64, P_{g,b} = bf16 pairs in its first
   // 32 columns; O_g at 256 + 128 g (DP wide); Q_g (bf16 pairs, DP/2 wide) right after O_g.
@@ -451,14 +439,10 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     const int qq = warp & 3;  // TMEM lane quarter this warp may access
     const int r = qq * 32 + lane;
     const uint32_t lane_off = (uint32_t)(qq * 32) << 16;
+    const uint32_t o_tm = tmem + lane_off + C::o_col(g);
     const float c = p.scale * 1.4426950408889634f;
-    // Phase bits per (tile, S buffer) and per tile: group 1 works on tile 1 in pair items
-    // and, together with group 0, on tile 0 in single-tile items, so it follows both tiles.
-    uint32_t sf_ph = 0, od_ph = 0;
-    int pv_count = 0;  // PV commits of tile g so far (only this group rescales O_g)
-    // [2 groups][128 rows]: partial row maxima / sums of a split single-tile item
-    float* xch = reinterpret_cast<float*>(smem + C::OFF_X);
-    const int pair_bar = 1 + qq;  // named barrier of warps w and w + 4 (same TMEM lane quarter)
+    uint32_t sf_ph = 0, od_ph = 0;  // s_full phase bit per buffer
+    int pv_count = 0;  // PV_g commits so far (pv_done phase bookkeeping)
     // Wait for item `it`'s Q buffer; tiles of this warp's group copy their Q rows into TMEM
     // as bf16 pairs (column c = head dims 2c, 2c+1: the TS-MMA A layout), zeroing dims >= Dv.
     // Every thread releases the buffer. Called only once all S MMAs of the previous item
@@ -495,163 +479,108 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
     if ((int)blockIdx.x < nitems) take_q(0, attn_item<NQ>(p, blockIdx.x, nqp, pmain).nq);
     for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
       const AttnItem x = attn_item<NQ>(p, w, nqp, pmain);
-      // A single-tile item is shared by both groups (NQ == 2): group 0 takes keys 0-31 of
-      // every block and group 1 keys 32-63 of the same rows, halving each thread's
-      // latency-bound exp chain; partial row maxima / sums meet in shared memory. The
-      // arithmetic is the same as a whole-row thread's (max is exact; sums are kept per key
-      // half and added at the end), so a tile's output does not depend on its item kind.
-      const bool split = NQ == 2 && x.nq == 1;
-      const int t = split ? 0 : g;  // query tile of this thread
+      float l = 0.f;
       const int nkb = x.nkb;
       // keys this thread's query row may see (causal: up to its own position)
-      const int klim = p.causal ? min(p.Tk, x.q0 + t * 128 + r + 1 + (p.Tk - p.Tq)) : p.Tk;
-      const uint32_t o_tm = tmem + lane_off + C::o_col(t);
-      float lh0 = 0.f, lh1 = 0.f;  // running row sums over key halves 0-31 / 32-63 of each block
-      if (t < x.nq) {
+      const int klim = p.causal ? min(p.Tk, x.q0 + g * 128 + r + 1 + (p.Tk - p.Tq)) : p.Tk;
+      if (g < x.nq) {
         float m_used = -INFINITY;
-        // one block of S for NK keys starting at koff (NK = 64: whole row; 32: split half)
-        auto block = [&](auto nk_c, int j) {
-          constexpr int NK = decltype(nk_c)::value;
-          const int koff = NK == 64 ? 0 : g * 32;
-          const int bf = j & 1;
-          const int kvalid = klim - j * C::KB - koff;
-          mbar_wait(&s_full[2 * t + bf], (sf_ph >> (2 * t + bf)) & 1);
+        for (int j = 0; j < nkb; ++j) {
+          const int kvalid = klim - j * C::KB;
+          mbar_wait(&s_full[2 * g + (j & 1)], (sf_ph >> (j & 1)) & 1);
           ATR(0, wi, it, j);
-          sf_ph ^= 1u << (2 * t + bf);
+          sf_ph ^= 1u << (j & 1);
           tc_fence_after();
-          const uint32_t s_tm = tmem + lane_off + C::s_col(t, bf);
-          uint32_t sv[NK];
-          tmem_ld32(s_tm + koff, *reinterpret_cast<uint32_t(*)[32]>(sv));
-          if (NK == 64) tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 % NK));
+          const uint32_t s_tm = tmem + lane_off + C::s_col(g, j & 1);
+          uint32_t sv[64];
+          tmem_ld32(s_tm, *reinterpret_cast<uint32_t(*)[32]>(sv));
+          tmem_ld32(s_tm + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
           tmem_ld_wait();
           ATR(4, wi, it, j);
-          if (kvalid < NK) {
+          if (kvalid < 64) {
 #pragma unroll
-            for (int i = 0; i < NK; ++i)
+            for (int i = 0; i < 64; ++i)
               if (i >= kvalid) sv[i] = __float_as_uint(-INFINITY);
           }
           float mx;
           {
             float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-            for (int i = 0; i < NK; i += 8)
+            for (int i = 0; i < 64; i += 8)
 #pragma unroll
               for (int u = 0; u < 4; ++u)
                 m4[u] = fmax3(m4[u], __uint_as_float(sv[i + 2 * u]), __uint_as_float(sv[i + 2 * u + 1]));
             mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
           }
-          if (NK == 32) {  // the partner's half (its slot was read before the last P barrier)
-            xch[g * 128 + r] = mx;
-            named_bar_sync(pair_bar, 64);
-            mx = fmaxf(mx, xch[(g ^ 1) * 128 + r]);
-          }
           const float m_new = fmaxf(m_used, mx * c);
           if (j == 0) {
             m_used = m_new;
           } else {
-            // Lazy rescale: only when a row max grows by more than 2^8. PV(j-1) may still
-            // be accumulating into O, so wait for it first (rare path). In a split item
-            // group 0 rescales O; both groups rescale their own partial sum.
+            // Lazy rescale: only when a row max grows by more than 2^8. PV_g(j-1) may still
+            // be accumulating into O_g, so wait for it first (rare path).
             const bool need = m_new > m_used + 8.f;
             ATR(5, wi, it, j);
             if (__any_sync(0xffffffffu, need)) {
+              mbar_wait(&pv_done[g], (pv_count - 1) & 1);
+              tc_fence_after();
               const float alpha = need ? ex2(m_used - m_new) : 1.f;
-              if (g == t) {
-                mbar_wait(&pv_done[t], (pv_count - 1) & 1);
-                tc_fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < DP; c0 += 16) {
-                  uint32_t o[16];
-                  tmem_ld16(o_tm + c0, o);
-                  tmem_ld_wait();
+              for (int c0 = 0; c0 < DP; c0 += 16) {
+                uint32_t o[16];
+                tmem_ld16(o_tm + c0, o);
+                tmem_ld_wait();
 #pragma unroll
-                  for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                  tmem_st8(o_tm + c0, o);
-                  tmem_st8(o_tm + c0 + 8, o + 8);
-                }
-                tmem_st_wait();
+                for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                tmem_st8(o_tm + c0, o);
+                tmem_st8(o_tm + c0 + 8, o + 8);
               }
+              tmem_st_wait();
               if (need) {
-                lh0 *= alpha;
-                lh1 *= alpha;
+                l *= alpha;
                 m_used = m_new;
               }
             }
           }
           const float nm = -m_used;
-          // per key half: two alternating accumulators over its 16 pairs
-          float2 ra[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-          float2 rb[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-          uint32_t pk[NK / 2];
+          float2 rs0 = make_float2(0.f, 0.f), rs1 = rs0;
+          uint32_t pk[32];
           const float2 c2 = make_float2(c, c), nm2 = make_float2(nm, nm);
 #pragma unroll
-          for (int i = 0; i < NK; i += 2) {
+          for (int i = 0; i < 64; i += 2) {
             // The softmax is MUFU-bound (16 ex2/clk/SM): a share of the pairs goes to the FMA
-            // pipe (chosen by key index, the same keys in either item kind); the pair
-            // arithmetic runs as packed FFMA2 / FADD2.
+            // pipe; the pair arithmetic runs as packed FFMA2 / FADD2.
             const bool poly = ((i >> 1) & 7) < EPD_POLY_EIGHTHS;
             const float2 a = fma2(make_float2(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])), c2, nm2);
             const float2 e = poly ? ex2_poly2(a) : make_float2(ex2(a.x), ex2(a.y));
-            const int hh = (i >> 5) & 1;  // key half within this thread's keys
-            if ((i >> 1) & 1) rb[hh] = add2(rb[hh], e);
-            else ra[hh] = add2(ra[hh], e);
+            if ((i >> 1) & 1) rs1 = add2(rs1, e);
+            else rs0 = add2(rs0, e);
             pk[i >> 1] = pack_bf16x2(e.x, e.y);
           }
           ATR(6, wi, it, j);
-          if (NK == 64) tmem_st32(s_tm, pk);  // P(j) over the first 32 columns of S(j)
-          else tmem_st16(s_tm + g * 16, pk);  // this half's 16 columns of P(j)
+          tmem_st32(s_tm, pk);  // P_g(j) over the first 32 columns of S_g(j)
           tmem_st_wait();
           ATR(7, wi, it, j);
-          {
-            const float2 rs = add2(ra[0], rb[0]);
-            if (NK == 64 || g == 0) lh0 += rs.x + rs.y;
-            else lh1 += rs.x + rs.y;
-          }
-          if (NK == 64) {
-            const float2 rs = add2(ra[1], rb[1]);
-            lh1 += rs.x + rs.y;
-          }
+          const float2 rs = add2(rs0, rs1);
+          l += rs.x + rs.y;
           tc_fence_before();
-          if (NK == 32) named_bar_sync(pair_bar, 64);  // both halves of P(j) are in TMEM
           ATR(1, wi, it, j);
-          if (g == t) {
-            mbar_arrive(&p_ready[2 * t + bf]);
-            ++pv_count;
-          }
-        };
-        for (int j = 0; j < nkb; ++j) {
-          if (split) block(std::integral_constant<int, 32>{}, j);
-          else block(std::integral_constant<int, 64>{}, j);
+          mbar_arrive(&p_ready[2 * g + (j & 1)]);
+          ++pv_count;
         }
-      }
-      if (NQ == 2 && g == 1 && !split && x.nq == 2) {
-        // tile 0's barriers moved on without this group: nkb S blocks and one o_done
-        sf_ph ^= (uint32_t)(((nkb + 1) >> 1) & 1) | ((uint32_t)((nkb >> 1) & 1) << 1);
-        od_ph ^= 1u;
       }
       // All S MMAs of this item are complete: hand the next item's Q to the tensor core
       // before the O epilogue, so its first S blocks overlap the epilogue.
       const int wn = w + gridDim.x;
       if (wn < nitems) take_q(it + 1, attn_item<NQ>(p, wn, nqp, pmain).nq);
-      if (t < x.nq) {
-        mbar_wait(&o_done[t], (od_ph >> t) & 1);
-        od_ph ^= 1u << t;
+      if (g < x.nq) {
+        mbar_wait(&o_done[g], od_ph);
+        od_ph ^= 1;
         tc_fence_after();
-        float l;
-        if (split) {
-          xch[g * 128 + r] = g ? lh1 : lh0;
-          named_bar_sync(pair_bar, 64);
-          l = xch[r] + xch[128 + r];
-        } else {
-          l = lh0 + lh1;
-        }
-        const int qrow = x.q0 + t * 128 + r;
+        const int qrow = x.q0 + g * 128 + r;
         const float inv = 1.f / l;
         bf16* dst = p.out + ((size_t)x.b * p.Tq + qrow) * p.ldo + (size_t)x.h * p.Dv;
-        // a split item's two groups write alternate 16-column chunks of O
 #pragma unroll
         for (int c0 = 0; c0 < DP; c0 += 16) {
-          if (split && ((c0 >> 4) & 1) != g) continue;
           uint32_t o[16];
           tmem_ld16(o_tm + c0, o);
           tmem_ld_wait();
@@ -668,11 +597,9 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
             }
           }
         }
-        // O is read: the next item's PV(0) (issued after its P(0), i.e. after group 0's
-        // next p_ready arrival) may overwrite it -- in a split item only once group 1 is
-        // done reading too.
+        // O_g is read: the next item's PV_g(0) (issued after its P_g(0), i.e. after this
+        // thread's next p_ready arrival) may overwrite it.
         tc_fence_before();
-        if (split) named_bar_sync(pair_bar, 64);
       }
     }
   }
