@@ -146,7 +146,15 @@ def init_dist(gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != gpus and world != 1:
         raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
-    if world > 1:
+    if world > 1 and os.environ.get("EPD_BENCH_ONE_GPU") == "1":
+        # functional check of the N > 1 path on one GPU (every rank on cuda:0, gloo control
+        # plane, the peer-memory gather between processes); its timings mean nothing
+        import torch.distributed as dist
+        local = 0
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+        dist.barrier()
+    elif world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
