@@ -236,7 +236,7 @@ def run_ours(args, wl, world, rank, local):
     cache = None
     if wl["cache"] and rank == 0:
         cache = MMTokenCache(capacity=max(n, 750), tokens_per_tile=cfg.out_tokens, hidden=cfg.out_dim, device=dev)
-    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache)
+    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache, cached=wl["cache"])
     if world > 1 and os.environ.get("EPD_GATHER", "peer") != "nccl":
         stage.enable_peer_gather(max(n, 16))  # shards stored into the prefill GPU over NVLink
 

@@ -61,11 +61,12 @@ class EncodeStage:
     ``encoder`` must expose ``cfg`` (an EncoderConfig) and
     ``encode(tiles_dev, out)``; in production it is
     :class:`~.encoder.VisionEncoder` (sm_100a kernels). ``cache`` is an
-    optional :class:`~.mmcache.MMTokenCache` living on the prefill rank.
+    optional :class:`~.mmcache.MMTokenCache` living on the prefill rank; with
+    world > 1 the encode ranks pass ``cached=True`` so they join its miss broadcast.
     """
 
     def __init__(self, encoder, device: torch.device, rank: int = 0, world: int = 1, prefill_rank: int = 0,
-                 cache=None, group=None):
+                 cache=None, group=None, cached: bool | None = None):
         self.enc = encoder
         self.cfg = encoder.cfg
         self.device = torch.device(device)
@@ -76,6 +77,11 @@ class EncodeStage:
         self.group = group
         if cache is not None and rank != prefill_rank:
             raise ValueError("the MM-token cache lives on the prefill rank")
+        # Whether the prefill rank runs the MM-token cache: every rank must take the same
+        # path (the cached one broadcasts the miss list first), so encode ranks are told.
+        self.cached = (cache is not None) if cached is None else bool(cached)
+        if self.cached and rank == prefill_rank and cache is None:
+            raise ValueError("cached=True needs the cache object on the prefill rank")
         self._staging = None
         # Host I/O runs on its own streams so consecutive requests pipeline: request i+1's
         # H2D upload overlaps request i's encode, and request i's D2H readback overlaps
@@ -295,7 +301,7 @@ class EncodeStage:
         res = RequestResult(rid=rid, n_tiles=n, encoded_tiles=0)
         tpp, bpt = self.cfg.out_tokens, self.cfg.out_dim * 2
 
-        if self.cache is None:
+        if not self.cached:
             ranges = shard_ranges(n, self.world)
             first, count = ranges[self.rank]
             peer = self._peer if (self._peer is not None and n <= self._peer_tiles) else None
@@ -355,7 +361,14 @@ class EncodeStage:
         m = miss.numel()
         ranges = shard_ranges(m, self.world)
         first, count = ranges[self.rank]
-        staging = self._buffer(m) if is_sink and m else None
+        # every rank knows m, so every rank picks the same transport for this request
+        peer = self._peer if (self._peer is not None and 0 < m <= self._peer_tiles) else None
+        compute = torch.cuda.current_stream(self.device)
+        if peer is not None:
+            seq = peer.begin()
+            staging = peer.packed(seq, m, tpp, self.cfg.out_dim, compute)[0] if is_sink else None
+        else:
+            staging = self._buffer(m) if is_sink and m else None
         local = None
         if count > 0:
             my = miss[first:first + count]
@@ -372,7 +385,12 @@ class EncodeStage:
         for release in (release_all, release_mine):
             if release is not None:
                 release()  # the compute stream has queued its last read of the uploaded tiles
-        self._gather(local, staging, ranges)
+        if peer is None:
+            self._gather(local, staging, ranges)
+        elif is_sink:
+            peer.wait(seq, ranges, compute)  # every other shard of misses has landed
+        elif count > 0:
+            peer.put(seq, local, first, compute)
         res.encoded_tiles = count
         res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
         res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != self.prefill_rank)

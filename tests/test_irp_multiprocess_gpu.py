@@ -21,12 +21,15 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,tiles", [(2, 10), (3, 13)])
-def test_irp_peer_gather_multiprocess(cuda, world, tiles):
+@pytest.mark.parametrize("world,tiles,mode", [(2, 10, ""), (3, 13, ""), (3, 12, "cache")])
+def test_irp_peer_gather_multiprocess(cuda, world, tiles, mode):
+    """mode "cache": the prefill rank's MM-token cache plans the misses, which are sharded
+    and land in the peer slot as staging before being scattered into the cache store."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(world),
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), str(ROOT / "tools" / "irp_check.py"),
-           "12", str(tiles)]
+           "12", str(tiles)] + ([mode] if mode else [])
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=240)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
-    assert f"irp_check world={world} tiles={tiles}" in out and "OK (transport nvlink-peer)" in out, out[-3000:]
+    tag = f"irp_check world={world} tiles={tiles}" + (" cache" if mode else "")
+    assert tag in out and "OK (transport nvlink-peer)" in out, out[-3000:]

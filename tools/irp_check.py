@@ -8,7 +8,9 @@ No kernel waits on another rank: the only cross-process waits are stream memory 
 (the mechanism CUDA IPC events use between processes on one GPU).
 
 usage: torchrun --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 \
-           tools/irp_check.py [requests] [tiles]"""
+           tools/irp_check.py [requests] [tiles] [cache]
+With "cache" the prefill rank holds the MM-token cache (cleared per request, tile i + n/2
+repeats tile i): misses are sharded over the ranks and land in the peer slot as staging."""
 import os
 import sys
 from pathlib import Path
@@ -23,18 +25,26 @@ from paper_2501_05460_b200.stage import EncodeStage, tiles_for_request  # noqa: 
 
 
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("IRP_CHECK_TIMEOUT", "150")), exit=True)
     reqs = int(sys.argv[1]) if len(sys.argv) > 1 else 20
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    use_cache = len(sys.argv) > 3 and sys.argv[3] == "cache"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     cfg = SIGLIP_MINICPM.with_layers(4)
     enc = VisionEncoder(cfg, dev, max_tiles=n)
-    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0)
+    cache = None
+    if use_cache and rank == 0:
+        from paper_2501_05460_b200.mmcache import MMTokenCache
+        cache = MMTokenCache(capacity=4 * n, tokens_per_tile=cfg.out_tokens, hidden=cfg.out_dim, device=dev)
+    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache, cached=use_cache)
     ok = stage.enable_peer_gather(max(n, 16))
     assert ok and stage.transport == "nvlink-peer", "peer gather did not come up"
-    requests = [tiles_for_request(n, cfg, seed=100 + i).pin_memory() for i in range(4)]
+    requests = [tiles_for_request(n, cfg, seed=100 + i, repeat_period=(n // 2 if use_cache else None)).pin_memory()
+                for i in range(4)]
     expected = None
     if rank == 0:
         expected = [enc.encode(t.to(dev)).clone() for t in requests]
@@ -44,6 +54,8 @@ def main():
     outs = []
     # pipelined: requests are issued back to back, slots reused every other request
     for i in range(reqs):
+        if cache is not None:
+            cache.clear()  # every request misses (and repeats within itself)
         res = stage.process(requests[i % 4])
         if rank == 0:
             outs.append((i, res.tokens.clone()))  # clone on the compute stream, before reuse
@@ -57,6 +69,8 @@ def main():
     # and one request at a time, with host readback through the prefill rank's slot
     out_host = torch.empty(n, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16).pin_memory()
     for i in range(4):
+        if cache is not None:
+            cache.clear()
         res = stage.process(requests[i], out_host=out_host if rank == 0 else None)
         stage.join()
         torch.cuda.synchronize()
@@ -69,7 +83,7 @@ def main():
     transport = stage.transport
     stage.close()
     if rank == 0:
-        print(f"irp_check world={world} tiles={n} requests={reqs + 4}: "
+        print(f"irp_check world={world} tiles={n}{' cache' if use_cache else ''} requests={reqs + 4}: "
               f"{'OK' if int(flag) == 0 else f'{int(flag)} BAD'} (transport {transport})", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if int(flag) == 0 else 1)
