@@ -145,24 +145,11 @@ class EncodeStage:
         buffer on the prefill rank."""
         ranges = shard_ranges(n, self.world)
         first, count = ranges[self.rank]
-        is_sink = self.rank == self.prefill_rank
-        if self._peer is not None and n <= self._peer_tiles:
-            stream = torch.cuda.current_stream(self.device)
-            seq = self._peer.begin()
-            if is_sink:
-                packed, _ = self._peer.packed(seq, n, self.cfg.out_tokens, self.cfg.out_dim, stream)
-                if count > 0:
-                    packed[first:first + count].copy_(local)
-                self._peer.wait(seq, ranges, stream)
-                return packed
-            if count > 0:
-                self._peer.put(seq, local, first, stream)
-            return None
-        dest = self._buffer(n) if is_sink else None
-        if is_sink and count > 0:
-            dest[first:first + count].copy_(local)
-        self._gather(local if count > 0 else None, dest, ranges)
-        return dest
+        ex = self._open_exchange(n, ring=False)
+        if self.rank == self.prefill_rank and count > 0:
+            ex["dest"][first:first + count].copy_(local)
+        self._close_exchange(ex, local if count > 0 else None, ranges)
+        return ex["dest"]
 
     # ------------------------------------------------------------------ helpers
     def _tokens_shape(self, n: int):
@@ -295,6 +282,38 @@ class EncodeStage:
         r["free"][k] = ev  # the tiles slot is reusable once this request's encode is queued
         return res
 
+    def _open_exchange(self, m: int, ring: bool) -> dict:
+        """Start the EP exchange of an m-tile request on every rank: picks the transport
+        (the peer slots when they are up and hold m tiles, else the collective) and, on the
+        prefill rank, the buffer the shards land in -- a peer slot, a ring slot (``ring``,
+        read back by process()) or a fresh buffer."""
+        is_sink = self.rank == self.prefill_rank
+        peer = self._peer if (self._peer is not None and 0 < m <= self._peer_tiles) else None
+        ex = {"peer": peer, "seq": None, "dest": None, "slot": None}
+        if peer is not None:
+            ex["seq"] = peer.begin()
+            if is_sink:
+                ex["dest"], ps = peer.packed(ex["seq"], m, self.cfg.out_tokens, self.cfg.out_dim,
+                                             torch.cuda.current_stream(self.device))
+                ex["slot"] = lambda ev, ps=ps: peer.set_free_event(ps, ev)
+        elif is_sink and ring:
+            ex["dest"], ex["slot"] = self._packed(m)
+        elif is_sink and m:
+            ex["dest"] = self._buffer(m)
+        return ex
+
+    def _close_exchange(self, ex: dict, local: torch.Tensor | None, ranges) -> None:
+        """Finish the exchange: this rank's shard (already encoded into ``local``, which on the
+        prefill rank is a view of the destination) reaches the prefill rank at its tile offset."""
+        peer, is_sink = ex["peer"], self.rank == self.prefill_rank
+        first, count = ranges[self.rank]
+        if peer is None:
+            self._gather(local, ex["dest"], ranges)
+        elif is_sink:
+            peer.wait(ex["seq"], ranges, torch.cuda.current_stream(self.device))  # every shard landed
+        elif count > 0:
+            peer.put(ex["seq"], local, first, torch.cuda.current_stream(self.device))  # NVLink stores + flag
+
     def _process(self, tiles_host, rid, tiles_dev) -> RequestResult:
         n = tiles_host.shape[0] if tiles_host is not None else tiles_dev.shape[0]
         is_sink = self.rank == self.prefill_rank
@@ -304,16 +323,8 @@ class EncodeStage:
         if not self.cached:
             ranges = shard_ranges(n, self.world)
             first, count = ranges[self.rank]
-            peer = self._peer if (self._peer is not None and n <= self._peer_tiles) else None
-            if peer is not None:
-                compute = torch.cuda.current_stream(self.device)
-                seq = peer.begin()
-                packed, slot = None, None
-                if is_sink:
-                    packed, ps = peer.packed(seq, n, tpp, self.cfg.out_dim, compute)
-                    slot = (lambda ev, ps=ps: peer.set_free_event(ps, ev))
-            else:
-                packed, slot = self._packed(n) if is_sink else (None, None)
+            ex = self._open_exchange(n, ring=True)
+            packed = ex["dest"]
             local = None
             if count > 0:
                 release = None
@@ -325,13 +336,8 @@ class EncodeStage:
                 self.enc.encode(src.contiguous(), local)
                 if release is not None:
                     release()
-            if peer is None:
-                self._gather(local, packed, ranges)
-            elif is_sink:
-                peer.wait(seq, ranges, compute)  # every other shard has landed in the slot
-            elif count > 0:
-                peer.put(seq, local, first, compute)  # stores over NVLink + this rank's flag
-            res._slot = slot
+            self._close_exchange(ex, local, ranges)
+            res._slot = ex["slot"]
             res.encoded_tiles = count
             res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
             res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != self.prefill_rank)
@@ -362,13 +368,8 @@ class EncodeStage:
         ranges = shard_ranges(m, self.world)
         first, count = ranges[self.rank]
         # every rank knows m, so every rank picks the same transport for this request
-        peer = self._peer if (self._peer is not None and 0 < m <= self._peer_tiles) else None
-        compute = torch.cuda.current_stream(self.device)
-        if peer is not None:
-            seq = peer.begin()
-            staging = peer.packed(seq, m, tpp, self.cfg.out_dim, compute)[0] if is_sink else None
-        else:
-            staging = self._buffer(m) if is_sink and m else None
+        ex = self._open_exchange(m, ring=False)
+        staging = ex["dest"]
         local = None
         if count > 0:
             my = miss[first:first + count]
@@ -385,12 +386,7 @@ class EncodeStage:
         for release in (release_all, release_mine):
             if release is not None:
                 release()  # the compute stream has queued its last read of the uploaded tiles
-        if peer is None:
-            self._gather(local, staging, ranges)
-        elif is_sink:
-            peer.wait(seq, ranges, compute)  # every other shard of misses has landed
-        elif count > 0:
-            peer.put(seq, local, first, compute)
+        self._close_exchange(ex, local, ranges)
         res.encoded_tiles = count
         res.shards = [ShardRecord(k, c) for k, (_, c) in enumerate(ranges) if c > 0]
         res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for k, (_, c) in enumerate(ranges) if k != self.prefill_rank)
