@@ -16,6 +16,7 @@ import torch
 from . import _lib
 from ._lib import EncoderDesc, call, lib
 from .configs import SEED, EncoderConfig
+from .weights import canonical_weights as _canonical
 from .weights import init_weights
 
 
@@ -79,12 +80,9 @@ class EncoderSchema:
 
 
 def canonical_weights(cfg: EncoderConfig, seed: int = SEED) -> dict[str, torch.Tensor]:
-    """The fp32 canonical weights both the GPU path and the CPU oracle use."""
-    sch = EncoderSchema(cfg)
-    try:
-        return init_weights(sch.schema(), cfg, seed)
-    finally:
-        sch.close()
+    """The fp32 canonical weights both the GPU path and the CPU oracle use (schema from
+    weights.weight_schema, which tests/test_abi_cpu.py pins to the C library's)."""
+    return _canonical(cfg, seed)
 
 
 class VisionEncoder(EncoderSchema):

@@ -39,6 +39,61 @@ def _is_ln(name: str) -> bool:
     return len(parts) >= 2 and (parts[-2].startswith("ln") or parts[-2] == "post_ln")
 
 
+def weight_schema(cfg) -> list[tuple[str, tuple[int, ...]]]:
+    """The canonical weight list (names, shapes, order) in pure Python.
+
+    Mirrors ``Encoder::validate_and_build_schema`` (csrc/encoder.cu) so host-only
+    callers -- the CPU reference arm of bench.py, fixture scripts -- never open
+    libepd.so; ``tests/test_abi_cpu.py`` checks the two agree for every config.
+    """
+    from ._lib import FAMILY_INTERNVIT_MLP, FAMILY_SIGLIP_RESAMPLER
+    D, F, E, P, Ch = cfg.hidden, cfg.mlp, cfg.out_dim, cfg.patch_size, cfg.channels
+    grid = cfg.image_size // cfg.patch_size
+    siglip = cfg.family == FAMILY_SIGLIP_RESAMPLER
+    if not siglip and cfg.family != FAMILY_INTERNVIT_MLP:
+        raise ValueError("unknown encoder family")
+    T = grid * grid + (0 if siglip else 1)
+    s: list[tuple[str, tuple[int, ...]]] = [("patch_embed.weight", (D, Ch, P, P)), ("patch_embed.bias", (D,))]
+    if not siglip:
+        s.append(("cls_token", (D,)))
+    s.append(("pos_embed", (T, D)))
+    for l in range(cfg.layers):
+        p = f"layers.{l}."
+        s += [(p + "ln1.weight", (D,)), (p + "ln1.bias", (D,))]
+        if siglip:
+            for m in "qkv":
+                s += [(p + f"attn.{m}.weight", (D, D)), (p + f"attn.{m}.bias", (D,))]
+        else:
+            s += [(p + "attn.qkv.weight", (3 * D, D)), (p + "attn.qkv.bias", (3 * D,))]
+        s += [(p + "attn.o.weight", (D, D)), (p + "attn.o.bias", (D,))]
+        if not siglip:
+            s.append((p + "ls1", (D,)))
+        s += [(p + "ln2.weight", (D,)), (p + "ln2.bias", (D,)),
+              (p + "mlp.fc1.weight", (F, D)), (p + "mlp.fc1.bias", (F,)),
+              (p + "mlp.fc2.weight", (D, F)), (p + "mlp.fc2.bias", (D,))]
+        if not siglip:
+            s.append((p + "ls2", (D,)))
+    if siglip:
+        Q = cfg.out_tokens
+        s += [("post_ln.weight", (D,)), ("post_ln.bias", (D,)), ("rs.query", (Q, E)),
+              ("rs.kv_proj.weight", (E, D)), ("rs.ln_q.weight", (E,)), ("rs.ln_q.bias", (E,)),
+              ("rs.ln_kv.weight", (E,)), ("rs.ln_kv.bias", (E,))]
+        for m in "qkvo":
+            s += [(f"rs.attn.{m}.weight", (E, E)), (f"rs.attn.{m}.bias", (E,))]
+        s += [("rs.ln_post.weight", (E,)), ("rs.ln_post.bias", (E,)), ("rs.proj", (E, E)),
+              ("rs.pos_embed", (T, E))]
+    else:
+        C4 = 4 * D
+        s += [("mlp1.ln.weight", (C4,)), ("mlp1.ln.bias", (C4,)), ("mlp1.fc1.weight", (E, C4)),
+              ("mlp1.fc1.bias", (E,)), ("mlp1.fc2.weight", (E, E)), ("mlp1.fc2.bias", (E,))]
+    return s
+
+
+def canonical_weights(cfg, seed: int) -> dict[str, torch.Tensor]:
+    """The fp32 canonical weights of ``cfg`` without loading the C library."""
+    return init_weights(weight_schema(cfg), cfg, seed)
+
+
 def init_weights(schema: list[tuple[str, tuple[int, ...]]], cfg, seed: int) -> dict[str, torch.Tensor]:
     """Canonical fp32 CPU tensors for every schema entry, drawn in schema order."""
     g = torch.Generator().manual_seed(seed)

@@ -57,6 +57,8 @@ def test_encoder_schema_host_only(cfg, params, flops):
         # SURVEY.md 8(d) algorithmic work per tile
         assert s.flops_per_tile() == pytest.approx(flops, rel=1e-9)
     assert s.launches(10) > 0
+    from paper_2501_05460_b200.weights import weight_schema
+    assert weight_schema(cfg) == sch  # the pure-Python schema the CPU reference arm uses
     s.close()
 
 

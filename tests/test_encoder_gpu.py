@@ -128,3 +128,61 @@ def test_fp32_check_mode_requires_opt_in(cuda):
     _, enc = _setup(TINY_VIT, cuda)
     with pytest.raises(RuntimeError):
         enc.encode_f32(torch.zeros(1, TINY_VIT.image_size, TINY_VIT.image_size, 3, dtype=torch.uint8, device=cuda))
+
+
+# ---- parity at the benched request sizes (C2 = 10 SigLIP tiles, C5 = 13 InternViT tiles)
+@pytest.mark.parametrize("cfg,n", [(SIGLIP_MINICPM, 10), (INTERNVIT_300M, 13)])
+def test_encoder_matches_oracle_at_bench_size(cuda, cfg, n):
+    """The whole benched request in one encoder call (max_tiles = n, the bench's GEMM tile
+    schedules and attention item mix) against the fp32 oracle on the bf16-valued weights."""
+    import oracle.encoders as oe
+    from paper_2501_05460_b200.stage import tiles_for_request
+    w, enc = _setup(cfg, cuda, max_tiles=n)
+    tiles = tiles_for_request(n, cfg, seed=SEED)
+    y = enc.encode(tiles.to(cuda))
+    torch.cuda.synchronize()
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    err = oe.relerr(y, oe.encode(cfg, oe.bf16_weights(w), tiles))
+    print(f"{cfg.name}: n={n} relerr={err:.3e}")
+    assert err <= TOL_BF16
+
+
+@pytest.mark.parametrize("cfg,n", [(SIGLIP_MINICPM, 10), (INTERNVIT_300M, 13)])
+def test_irp_shards_equal_slices_of_the_whole_request(cuda, cfg, n):
+    """IRP at any width returns the single-GPU tokens bit for bit: every shard encode of
+    irp_shard(n, w), w = 2/4/8, equals its slice of the n-tile encode (batch invariance
+    across the 1/2/3/5/7-tile GEMM and attention schedules)."""
+    from paper_2501_05460_b200.routing import shard_ranges
+    from paper_2501_05460_b200.stage import tiles_for_request
+    _, enc = _setup(cfg, cuda, max_tiles=n)
+    tiles = tiles_for_request(n, cfg, seed=SEED + 1).to(cuda)
+    whole = enc.encode(tiles)
+    for w_ in (2, 4, 8):
+        for first, count in shard_ranges(n, w_):
+            if count:
+                part = enc.encode(tiles[first:first + count].contiguous())
+                assert torch.equal(part, whole[first:first + count]), (w_, first, count)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("key", ["siglip", "internvit"])
+def test_encoder_matches_public_implementation(cuda, key):
+    """Direct pin against the public model code: the B200 tokens vs the outputs of
+    transformers' Idefics2VisionTransformer + vLLM Resampler2_5 / transformers' InternVL
+    vision tower + projector recorded in tests/golden/encoder_golden.json (fp32-valued
+    weights; bf16 compute budget 1e-2)."""
+    import json
+    from pathlib import Path
+
+    from paper_2501_05460_b200.configs import CONFIGS
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "encoder_golden.json").read_text())["models"][key]
+    cfg = CONFIGS[g["config"]]
+    _, enc = _setup(cfg, cuda, max_tiles=4)
+    gen = torch.Generator().manual_seed(g["tile_seed"])
+    tiles = torch.randint(0, 256, (g["n_tiles"], cfg.image_size, cfg.image_size, cfg.channels), dtype=torch.uint8,
+                          generator=gen)
+    y = enc.encode(tiles.to(cuda)).float().cpu().reshape(-1)
+    idx = torch.arange(0, y.numel(), g["sample_stride"])[:len(g["samples"])]
+    err = float((y[idx] - torch.tensor(g["samples"])).abs().max()) / g["max_abs"]
+    print(f"{key}: B200 vs public implementation (sampled) relerr {err:.3e}")
+    assert err <= TOL_BF16
