@@ -50,10 +50,14 @@ def modeled_prefill_s(model: str, total_tokens: int) -> float:
 
 
 def workload(name: str):
-    from paper_2501_05460_b200.configs import INTERNVIT_300M, SIGLIP_MINICPM
+    from paper_2501_05460_b200.configs import INTERNVIT_300M, SIGLIP_MINICPM, TINY_VIT
+    if name == "c1":
+        return dict(cfg=TINY_VIT, tiles=4, repeat=None, cache=False,
+                    desc="C1: PR1 oracle config, tiny ViT (4 tokens x 8 dims per tile), 1 request x 4 tiles")
     if name == "c2":
-        return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b",
-                    desc="C2: MiniCPM-V 2.6-shaped SigLIP-400M + resampler, 10 tiles (448x448) per request")
+        return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b", kv_handoff=True,
+                    desc="C2: MiniCPM-V 2.6-shaped SigLIP-400M + resampler, 10 tiles (448x448) per request "
+                         "(+ Qwen2-7B prefill, prefill->decode KV-block handoff of 662 tokens)")
     if name == "c2i":
         return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b", image=(4032, 3024),
                     desc="C2 from pixels: one 4032x3024 photo per request, MiniCPM-V slicing on the GPU -> "
@@ -61,10 +65,16 @@ def workload(name: str):
     if name == "c4":
         return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True, llm="qwen2-7b",
                     desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
+    if name == "c4w":
+        return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=None, cache=True, llm="qwen2-7b", rotate=(100, 20),
+                    desc="C4 warm: 40 images x 10 tiles per request; each request repeats the previous request's "
+                         "last 20 images (cross-request MM-token cache hits) and brings 20 new ones (misses)")
     if name == "c5":
-        return dict(cfg=INTERNVIT_300M, tiles=12, repeat=None, cache=False, kv_handoff=True, llm="internlm2.5-7b",
-                    desc="C5: InternVL2-8B-shaped InternViT-300M + pixel shuffle + mlp1, 12 tiles per request, "
-                         "+ prefill->decode KV-block handoff (3094 tokens)")
+        # the catalog maps a 4032x3024 image to 13 InternVL2-8B tiles (models.cfg:28):
+        # 12 dynamic tiles + the thumbnail
+        return dict(cfg=INTERNVIT_300M, tiles=13, repeat=None, cache=False, kv_handoff=True, llm="internlm2.5-7b",
+                    desc="C5: InternVL2-8B-shaped InternViT-300M + pixel shuffle + mlp1, 13 tiles per request "
+                         "(12 dynamic + thumbnail, models.cfg:28), + prefill->decode KV-block handoff (3350 tokens)")
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -140,6 +150,33 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(gpus: int) -> None:
+    """`python bench.py --gpus N` with N > 1 outside torchrun: re-exec under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1). Under torchrun
+    (WORLD_SIZE set) this is a no-op. NCCL's INIT log is kept on stderr so the rank count
+    of every communicator can be checked."""
+    if gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if os.environ.get("EPD_BENCH_ONE_GPU") != "1" and torch.cuda.device_count() < gpus:
+        raise SystemExit(f"--gpus {gpus} but only {torch.cuda.device_count()} CUDA device(s) are visible "
+                         "(EPD_BENCH_ONE_GPU=1 runs every rank on cuda:0 as a functional check)")
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "4")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py")] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execvpe(sys.executable, cmd, env)
+
+
 def init_dist(gpus: int):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -164,18 +201,29 @@ def init_dist(gpus: int):
     return world, rank, local
 
 
+def bench_config(wl, world: int) -> dict:
+    """The workload description both arms print (identical for --impl ours / reference)."""
+    cfg = wl["cfg"]
+    return {"workload": wl["desc"], "encoder": cfg.name, "tiles_per_request": wl["tiles"],
+            "irp_width": world, "prefill_rank": 0, "parallelism": f"irp{world}",
+            "l2": "working set > L2 (0.97 GB bf16 weights + ~0.5 GB activations streamed per step)",
+            "weights": "random-init N(0,0.02), seed 20260808"}
+
+
 def reference_arm(args, wl, world, rank):
     """--impl reference: the reference's CPU path for the encode stage = the fp32 CPU
     oracle (the reference ships no encoder), on all host cores."""
     if rank != 0:
         return
+    # host only: the weight schema comes from weights.weight_schema, so this arm never
+    # loads libepd.so (tests/test_bench_cpu.py checks it)
     import oracle.encoders as oe
-    from paper_2501_05460_b200.encoder import canonical_weights
     from paper_2501_05460_b200.stage import tiles_for_request
+    from paper_2501_05460_b200.weights import canonical_weights
     cfg = wl["cfg"]
     torch.set_num_threads(os.cpu_count())
-    w = canonical_weights(cfg)
-    tiles = tiles_for_request(wl["tiles"], cfg, seed=20260808)
+    w = canonical_weights(cfg, 20260808)
+    tiles = tiles_for_request(min(wl["tiles"], 16), cfg, seed=20260808)
     per_step = 1  # bounded sample: one tile of the request per step
     for i in range(args.warmup):
         oe.encode(cfg, w, tiles[i % tiles.shape[0]:i % tiles.shape[0] + per_step])
@@ -188,10 +236,10 @@ def reference_arm(args, wl, world, rank):
     line = {"metric": METRIC, "value": v, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": wl["desc"], "tiles_per_request": wl["tiles"], "sample_tiles_per_step": per_step},
+            "impl": "reference", "config": bench_config(wl, world), "sample_tiles_per_step": per_step,
             "cpu_baseline": {"value": v, "unit": "tiles/s", "cores": torch.get_num_threads(), "kind": "port",
-                             "sample": f"{per_step} tile per step, fp32 PyTorch CPU oracle (oracle/encoders.py)"},
+                             "sample": f"{per_step} tile of the {wl['tiles']}-tile request per step (bounded "
+                                       "sample), fp32 PyTorch CPU oracle (oracle/encoders.py)"},
             "e2e": {"value": v, "unit": "tiles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,6 +258,7 @@ def main():
         print("note: warm-up raised to the minimum of 3", file=sys.stderr)
         args.warmup = 3
     wl = workload(args.workload)
+    spawn_ranks(args.gpus)
     world, rank, local = init_dist(args.gpus) if args.impl == "ours" else (
         int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0)
     if args.impl == "reference":
@@ -236,11 +285,34 @@ def run_ours(args, wl, world, rank, local):
     cache = None
     if wl["cache"] and rank == 0:
         cache = MMTokenCache(capacity=max(n, 750), tokens_per_tile=cfg.out_tokens, hidden=cfg.out_dim, device=dev)
-    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache, cached=wl["cache"])
+    comm = None
+    if world > 1 and os.environ.get("EPD_GATHER", "peer") == "nccl":
+        from paper_2501_05460_b200.comm import NcclComm
+        comm = NcclComm(dev)  # the EP gather's NCCL leg through the C ABI (epd_gather_tokens)
+    stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache, cached=wl["cache"],
+                        comm=comm)
     if world > 1 and os.environ.get("EPD_GATHER", "peer") != "nccl":
         stage.enable_peer_gather(max(n, 16))  # shards stored into the prefill GPU over NVLink
 
-    tiles_host = tiles_for_request(n, cfg, seed=20260808, repeat_period=wl["repeat"]).pin_memory()
+    rot = wl.get("rotate")
+    if rot:
+        # a pool of P images (+ the first 2 rq-image windows again, same content) so request k is the
+        # contiguous window [rq*k mod P, rq*k mod P + 2 rq) of images: half of it is the previous
+        # request's second half (cache hits), half is new (last seen P/rq requests ago: evicted)
+        P, rq = rot
+        per = n // (2 * rq)  # tiles per image
+        pool = tiles_for_request(P * per, cfg, seed=20260808)
+        tiles_pool = torch.cat([pool, pool[:2 * rq * per]]).pin_memory()
+        pool_dev = tiles_pool.to(dev)
+        step_no = [0]
+
+        def window():
+            o = (step_no[0] * rq % P) * per
+            step_no[0] += 1
+            return slice(o, o + n)
+        tiles_host = tiles_pool[:n]
+    else:
+        tiles_host = tiles_for_request(n, cfg, seed=20260808, repeat_period=wl["repeat"]).pin_memory()
     image_host = None
     if wl.get("image"):
         # one synthetic photo per request; the stage tiles it on the GPU (tiler.py)
@@ -255,11 +327,15 @@ def run_ours(args, wl, world, rank, local):
             dist.barrier()
 
     def reset_cache():
-        if cache is not None:
+        # C4: every request starts cold (its hits are in-request duplicates); C4 warm keeps the
+        # cache across requests, so the previous request's images hit
+        if cache is not None and not rot:
             cache.clear()
 
     def step_resident():
         reset_cache()
+        if rot:
+            return stage.process(None, tiles_dev=pool_dev[window()])
         return stage.process(None, tiles_dev=tiles_dev)
 
     def step_e2e():
@@ -268,6 +344,8 @@ def run_ours(args, wl, world, rank, local):
         reset_cache()
         if image_host is not None:
             return stage.process_image(image_host, cfg.geometry.name, out_host=out_host if rank == 0 else None)
+        if rot:
+            return stage.process(tiles_pool[window()], out_host=out_host if rank == 0 else None)
         return stage.process(tiles_host, out_host=out_host if rank == 0 else None)
 
     def max_over_ranks(x: float) -> float:
@@ -327,6 +405,7 @@ def run_ours(args, wl, world, rank, local):
     # [MM tokens | prompt] and reads back the first token, so TTFT = tile upload -> encode ->
     # gather -> prefill -> first token on the host.
     prefill = None
+    pf = prompt_ids = mm_last = None
     if wl.get("llm") and not args.no_prefill:
         from paper_2501_05460_b200.prefill import INTERNLM25_7B, QWEN2_7B, Prefiller
         lcfg = {"qwen2-7b": QWEN2_7B, "internlm2.5-7b": INTERNLM25_7B}[wl["llm"]]
@@ -335,11 +414,12 @@ def run_ours(args, wl, world, rank, local):
         prompt = torch.randint(0, lcfg.vocab, (PROMPT_TOKENS,), dtype=torch.int32,
                                generator=torch.Generator().manual_seed(20260808)).to(dev)
         tok_host = torch.empty(1, dtype=torch.int32).pin_memory()
+        prompt_ids = prompt
 
         def step_ttft():
-            reset_cache()  # every TTFT request starts cold, like the e2e loop
+            reset_cache()  # every TTFT request starts cold, like the e2e loop (C4 warm: steady state)
             res = (stage.process_image(image_host, cfg.geometry.name) if image_host is not None
-                   else stage.process(tiles_host))
+                   else stage.process(tiles_pool[window()] if rot else tiles_host))
             if pf is not None:
                 tok = pf.prefill(res.tokens.view(-1, cfg.out_dim), prompt)
                 tok_host.copy_(tok, non_blocking=True)
@@ -350,7 +430,9 @@ def run_ours(args, wl, world, rank, local):
                 pf.prefill(last.tokens.view(-1, cfg.out_dim), prompt)
 
         for _ in range(3):
-            step_ttft()
+            mm_last = step_ttft().tokens
+        if mm_last is not None:
+            mm_last = mm_last.view(-1, cfg.out_dim).clone()
         torch.cuda.synchronize()
         ttft_full = latencies(step_ttft, max(50, args.steps))
         pre_only = latencies(step_prefill_only, 20)
@@ -380,7 +462,8 @@ def run_ours(args, wl, world, rank, local):
     _lib.call("epd_encoder_profile_read", enc._h, ms, fl, by, cnt, nc)
     _lib.call("epd_encoder_profile", enc._h, 0)
 
-    kv = kv_handoff_bench(wl, cfg, n, world, rank, dev, args) if wl.get("kv_handoff") else None
+    kv = (kv_handoff_bench(wl, cfg, n, world, rank, dev, args, pf=pf, mm=mm_last, prompt=prompt_ids)
+          if wl.get("kv_handoff") else None)
     gather = gather_bench(stage, cfg, n, world, rank, dev, args) if not wl["cache"] else None
 
     encoded_tiles = n  # tiles that complete the request per step (cache hits count as served)
@@ -424,11 +507,7 @@ def run_ours(args, wl, world, rank, local):
         "metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": wl["desc"], "encoder": cfg.name, "tiles_per_request": n,
-                   "irp_width": world, "prefill_rank": 0, "parallelism": f"irp{world}",
-                   "ep_transport": stage.transport,
-                   "l2": "working set > L2 (0.97 GB bf16 weights + ~0.5 GB activations streamed per step)",
-                   "weights": "random-init N(0,0.02), seed 20260808"},
+        "config": bench_config(wl, world), "ep_transport": stage.transport,
         "p50_ttft_ms": prefill["p50_ttft_ms"] if prefill else p50_ttft,
         "p50_ttft_ms_encode_side": p50_ttft,
         "p50_ttft_ms_resident": p50_resident,
@@ -469,27 +548,49 @@ def run_ours(args, wl, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
-def kv_handoff_bench(wl, cfg, n, world, rank, dev, args):
-    """Prefill -> decode KV-block handoff of one request (engine.py:542-555, 436-439):
-    pack the prefill rank's paged blocks, NCCL P2P to the decode rank (the last rank;
-    the same GPU at N = 1), unpack into the decode-side block ids."""
-    import torch.distributed as dist
-
-    from paper_2501_05460_b200.handoff import PagedKVCache, kv_handoff
+def kv_handoff_bench(wl, cfg, n, world, rank, dev, args, pf=None, mm=None, prompt=None):
+    """Prefill -> decode KV-block handoff of one request (engine.py:542-555, 436-439) through
+    handoff.KVHandoff: the prefill rank (0) holds the request's paged KV, written by the real
+    LLM prefill of the request when it ran (``pf``), and the decode rank (the last rank; the
+    same GPU at N = 1) reserves total + output tokens and receives it: one block-move kernel
+    on a shared GPU, the same kernel pushing into the decode pool over NVLink across GPUs
+    (EPD_KV=nccl: pack -> ncclSend/Recv -> unpack through the C ABI)."""
+    from paper_2501_05460_b200.handoff import KVHandoff, PagedKVCache
     geo = cfg.geometry
     total = n * geo.tokens_per_patch + PROMPT_TOKENS
     out_tokens = 64
     p_rank, d_rank = 0, world - 1
     nblk = -(-(total + out_tokens) // 16) + 4
-    src = PagedKVCache(geo.num_layers, geo.kv_heads, geo.head_dim, 16, nblk, dev) if rank == p_rank else None
-    dst = PagedKVCache(geo.num_layers, geo.kv_heads, geo.head_dim, 16, nblk, dev) if rank == d_rank else None
+    transport = "local" if world == 1 else os.environ.get("EPD_KV", "nvlink-peer")
+    grp = None
+    if transport == "nccl" and world > 2:
+        import torch.distributed as dist
+        grp = dist.new_group([p_rank, d_rank])  # collective over the world: before the early return
     if rank not in (p_rank, d_rank):
         return None
+    comm = None
+    if transport == "nccl":
+        from paper_2501_05460_b200.comm import NcclComm
+        comm = NcclComm(dev, rank=0 if rank == p_rank else 1, world=2, group=grp)
+    src = PagedKVCache(geo.num_layers, geo.kv_heads, geo.head_dim, 16, nblk, dev) if rank == p_rank else None
+    dst = (PagedKVCache(geo.num_layers, geo.kv_heads, geo.head_dim, 16, nblk, dev, shareable=transport != "local")
+           if rank == d_rank else None)
+    h = KVHandoff(rank, p_rank, d_rank, src, dst, transport=transport, comm=comm, comm_ranks=(0, 1))
+    kv_source = "zeros"
+    if src is not None and pf is not None:
+        # the request's real KV: the LLM prefill writes every layer's post-RoPE K/V into the
+        # blocks; LIFO reuse hands the same ids back to every later allocation of this size
+        ids = src.manager.allocate(-1, total)
+        pf.prefill(mm, prompt, kv=src, block_ids=ids)
+        src.manager.free(-1)
+        kv_source = f"prefill ({pf.cfg.name})"
 
     def one(rid):
         if src is not None:
             src.manager.allocate(rid, total)
-        info = kv_handoff(rid, total, out_tokens, src, dst, p_rank, d_rank, rank)
+        info = h.try_reserve_decode(rid, total, out_tokens)
+        if info is None:
+            raise RuntimeError("decode pool could not reserve the request")
         if dst is not None:
             dst.manager.free(rid)
         return info
@@ -504,13 +605,22 @@ def kv_handoff_bench(wl, cfg, n, world, rank, dev, args):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    verified = None
+    if world == 1:
+        verified = bool(torch.equal(dst.blocks(info["dst_blocks"][:len(info["src_blocks"])]),
+                                    src.blocks(info["src_blocks"])))
+    h.close()
     if rank != 0:
         return None
     moved = info["moved_bytes"]
+    paths = {"local": "epd_kv_move: one block-to-block kernel (same GPU)",
+             "nvlink-peer": "epd_kv_move into the decode pool mapped over CUDA IPC (NVLink stores) + stream-memop flags",
+             "nccl": "epd_kv_handoff_send/recv: pack -> ncclSend/Recv -> unpack (C ABI)"}
     return {"tokens": total, "pd_bytes": total * geo.kv_bytes_per_token(), "moved_bytes_per_request": moved,
-            "ms_per_request": ms, "GBps": moved / (ms / 1e3) / 1e9,
-            "path": "epd_kv_move: one block-to-block kernel (same GPU)" if world == 1 else "pack -> NCCL P2P -> unpack",
-            "note": "whole 16-token blocks move; pd_bytes is the reference's token-exact count (engine.py:553-554)"}
+            "ms_per_request": ms, "GBps": moved / (ms / 1e3) / 1e9, "transport": transport,
+            "path": paths[transport], "kv_source": kv_source, "bit_exact": verified,
+            "note": "whole 16-token blocks move; pd_bytes is the reference's token-exact count (engine.py:553-554); "
+                    "each step includes the reservation handshake"}
 
 
 NVLINK_GBPS = 900.0  # NVLink 5 per GPU per direction (nominal; MEASURED_PEAKS.json has no NVLink figure)

@@ -176,6 +176,50 @@ epd_status_t epd_kv_move(const void* src_cache, int64_t src_segment_stride, void
                          int64_t dst_segment_stride, int32_t segments, int64_t block_bytes, const int32_t* src_ids,
                          const int32_t* dst_ids, int32_t nblocks, void* stream);
 
+/* ------------------------------------------------------------------ stage handoff over NCCL
+ * The NCCL legs of the stage-handoff interface, so a non-Python host can
+ * run them: the EP migration of MM tokens to the prefill rank (engine._send_ready_shards /
+ * _schedule_transfer, engine.py:511-526; prefill starts once all shards landed,
+ * _on_transfer_end("ep"), engine.py:424-435) and the PD migration of paged KV into the
+ * blocks the decode instance reserved (_try_reserve_decode, engine.py:542-555;
+ * _on_transfer_end("pd"), engine.py:436-439). NCCL is resolved at run time (the copy the
+ * process already loaded, else libnccl.so.2, or $EPD_NCCL_LIB); without it these calls return
+ * EPD_ERR_UNSUPPORTED. The unique id (EPD_COMM_ID_BYTES opaque bytes) is made on one rank
+ * and broadcast by the host (e.g. through the torch.distributed store). */
+#define EPD_COMM_ID_BYTES 128
+typedef struct epd_comm epd_comm_t;
+/* version = NCCL_VERSION_CODE of the loaded library (e.g. 22809 for 2.28.9). */
+epd_status_t epd_comm_version(int32_t* version);
+epd_status_t epd_comm_unique_id(uint8_t* id);
+/* Collective over nranks processes (ncclCommInitRank on `device`). */
+epd_status_t epd_comm_init(const uint8_t* id, int32_t nranks, int32_t rank, int32_t device, epd_comm_t** comm);
+void epd_comm_destroy(epd_comm_t* comm);
+/* EP gather of one request of n_tiles tiles (tile_bytes each = tokens_per_patch x
+ * mm_bytes_per_token, engine.py:524): rank k holds the shard epd_irp_ranges(n_tiles, nranks)
+ * assigns it (irp_shard, engine.py:55-62) in `shard`; the root receives every shard into
+ * packed[first_k * tile_bytes ...], i.e. request order whatever the arrival order. On the
+ * root, `shard` may alias its own slice of `packed` (no copy) or be any other buffer. Called
+ * by every rank of the communicator; ranks with an empty shard send nothing. */
+epd_status_t epd_gather_tokens(epd_comm_t* comm, const void* shard, int64_t n_tiles, int64_t tile_bytes,
+                               void* packed, int32_t root, void* stream);
+/* Raw bytes between two ranks (stream-ordered ncclSend / ncclRecv); the group calls bracket
+ * several of them into one NCCL group (e.g. a send to self and the matching receive). */
+epd_status_t epd_comm_send(epd_comm_t* comm, const void* buf, int64_t bytes, int32_t peer, void* stream);
+epd_status_t epd_comm_recv(epd_comm_t* comm, void* buf, int64_t bytes, int32_t peer, void* stream);
+epd_status_t epd_comm_group_start(void);
+epd_status_t epd_comm_group_end(void);
+/* PD handoff: the prefill rank packs blocks block_ids[0..nblocks) of its paged cache
+ * (geometry as epd_kv_pack) into `staging` (nblocks x segments x block_bytes) and sends it to
+ * `peer`; the decode rank receives into its staging buffer and unpacks into the block ids it
+ * reserved. Both sides must agree on nblocks (= blocks_needed(total_tokens), blocks.py:24-26)
+ * before calling -- the host's reservation handshake (handoff.py). */
+epd_status_t epd_kv_handoff_send(epd_comm_t* comm, const void* cache, int32_t segments, int64_t segment_stride,
+                                 int64_t block_bytes, const int32_t* block_ids, int32_t nblocks, void* staging,
+                                 int32_t peer, void* stream);
+epd_status_t epd_kv_handoff_recv(epd_comm_t* comm, void* cache, int32_t segments, int64_t segment_stride,
+                                 int64_t block_bytes, const int32_t* block_ids, int32_t nblocks, void* staging,
+                                 int32_t peer, void* stream);
+
 /* ------------------------------------------------------------------ EP gather over peer memory
  * The B200-native transport for the encode -> prefill MM-token transfer
  * (engine._send_ready_shards / _schedule_transfer, engine.py:511-526; arrival accounting

@@ -73,6 +73,17 @@ _SIGS = {
     "epd_mmcache_check": (_i32, [_vp, _vp]),
     "epd_gather_records": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
     "epd_scatter_records": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
+    "epd_comm_version": (_i32, [C.POINTER(_i32)]),
+    "epd_comm_unique_id": (_i32, [_vp]),
+    "epd_comm_init": (_i32, [_vp, _i32, _i32, _i32, C.POINTER(_vp)]),
+    "epd_comm_destroy": (None, [_vp]),
+    "epd_gather_tokens": (_i32, [_vp, _vp, _i64, _i64, _vp, _i32, _vp]),
+    "epd_comm_send": (_i32, [_vp, _vp, _i64, _i32, _vp]),
+    "epd_comm_recv": (_i32, [_vp, _vp, _i64, _i32, _vp]),
+    "epd_comm_group_start": (_i32, []),
+    "epd_comm_group_end": (_i32, []),
+    "epd_kv_handoff_send": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _i32, _vp, _i32, _vp]),
+    "epd_kv_handoff_recv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _i32, _vp, _i32, _vp]),
     "epd_peer_alloc": (_i32, [_i64, C.POINTER(_vp)]),
     "epd_peer_free": (_i32, [_vp]),
     "epd_peer_export": (_i32, [_vp, _vp]),

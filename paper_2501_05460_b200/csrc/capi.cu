@@ -29,6 +29,13 @@ epd_status_t cuda_status(int rc, const char* what) {
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+}  // namespace
+
+// shared with the other translation units of the ABI (comm.cu)
+epd_status_t epd_detail_fail(epd_status_t code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
+
 // Two-level record copy used by the KV handoff:
 //   pack:   out[i][s] = cache[s][ids[i]]
 //   unpack: cache[s][ids[i]] = in[i][s]
@@ -61,6 +68,7 @@ __global__ void kv_move_kernel(const uint8_t* __restrict__ src, uint8_t* __restr
   for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < vecs;
        v += (long long)gridDim.x * blockDim.x)
     b[v] = a[v];
+  __threadfence_system();  // dst may be a peer GPU's pool: the signal that follows must not overtake
 }
 
 __global__ void scatter_records_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ index,

@@ -66,7 +66,7 @@ class EncodeStage:
     """
 
     def __init__(self, encoder, device: torch.device, rank: int = 0, world: int = 1, prefill_rank: int = 0,
-                 cache=None, group=None, cached: bool | None = None):
+                 cache=None, group=None, cached: bool | None = None, comm=None):
         self.enc = encoder
         self.cfg = encoder.cfg
         self.device = torch.device(device)
@@ -75,6 +75,9 @@ class EncodeStage:
         self.prefill_rank = prefill_rank
         self.cache = cache
         self.group = group
+        # NCCL leg of the EP gather through the C ABI (comm.NcclComm -> epd_gather_tokens); without
+        # it the fallback is torch.distributed's grouped P2P
+        self.comm = comm
         if cache is not None and rank != prefill_rank:
             raise ValueError("the MM-token cache lives on the prefill rank")
         # Whether the prefill rank runs the MM-token cache: every rank must take the same
@@ -132,7 +135,11 @@ class EncodeStage:
 
     @property
     def transport(self) -> str:
-        return "nvlink-peer" if self._peer is not None else ("nccl-p2p" if self.world > 1 else "local")
+        if self._peer is not None:
+            return "nvlink-peer"
+        if self.world == 1:
+            return "local"
+        return "nccl-capi" if self.comm is not None else "nccl-p2p"
 
     def close(self) -> None:
         if self._peer is not None:
@@ -233,6 +240,10 @@ class EncodeStage:
     def _gather(self, local: torch.Tensor | None, dest: torch.Tensor | None, ranges) -> None:
         """Shards -> prefill rank at their unit offsets (grouped point-to-point)."""
         if self.world == 1:
+            return
+        if self.comm is not None:
+            n = sum(c for _, c in ranges)
+            self.comm.gather_tokens(local, n, dest, root=self.prefill_rank)
             return
         ops = []
         if self.rank == self.prefill_rank:
