@@ -9,6 +9,10 @@ Mirrors the reference's encode-side routing so tile partitioning is bit-exact:
 * :func:`plan_batch` -- the multi-request batch plan of engine._start_encode
   (engine.py:583-602): zero shards dropped, text-only requests -> [(0, 0)],
   every request restarts at worker 0;
+* :func:`assign_instance` -- engine.assign_instance (engine.py:65-78): which encode /
+  prefill / decode instance takes a request (round-robin counter or least-loaded);
+* :func:`form_batch` -- engine.form_batch (engine.py:81-93): the longest FCFS prefix that
+  fits (the first misfit stops the batch);
 * :func:`ep_bytes` / :func:`pd_bytes` -- EP/PD migration byte counts
   (engine.py:524, 553-554).
 """
@@ -49,6 +53,36 @@ def plan_batch(patches_per_request: list[int], width: int):
             worker_load[k] += c
             worker_reqs[k] += 1
     return shards, worker_load, worker_reqs
+
+
+def _policy_name(policy) -> str:
+    return getattr(policy, "value", policy)
+
+
+def assign_instance(policy, candidates, rr_counter: int = 0) -> tuple[int, int]:
+    """(instance id, next round-robin counter) from ordered (id, load) candidates.
+
+    ``policy``: "fcfs" / "round_robin" / "least_loaded" or the reference's SchedulePolicy.
+    Least-loaded takes the minimum load, ties to the lowest id, and leaves the counter;
+    any other policy cycles through the candidates with the counter (engine.py:65-78)."""
+    if not candidates:
+        raise ValueError("no candidate instances")
+    if _policy_name(policy) == "least_loaded":
+        iid, _ = min(candidates, key=lambda pair: (pair[1], pair[0]))
+        return iid, rr_counter
+    iid, _ = candidates[rr_counter % len(candidates)]
+    return iid, rr_counter + 1
+
+
+def form_batch(queue, max_batch: int, fits) -> list:
+    """Longest FCFS prefix of ``queue`` (up to ``max_batch``) whose members fit; ``fits`` is
+    called once per accepted head and may commit reservations (engine.py:81-93)."""
+    batch = []
+    for item in queue:
+        if len(batch) >= max_batch or not fits(item):
+            break
+        batch.append(item)
+    return batch
 
 
 def ep_bytes(tiles: int, tokens_per_patch: int, mm_bytes_per_token: int) -> int:

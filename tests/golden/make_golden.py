@@ -26,7 +26,8 @@ def main() -> None:
     sys.path.insert(0, str(REF))
     from disaggsim.blocks import BlockManager, CacheKind
     from disaggsim.costs import CostParams, transfer_latency, Channel
-    from disaggsim.engine import irp_shard, run_simulation
+    from disaggsim.engine import assign_instance, form_batch, irp_shard, run_simulation
+    from disaggsim.simconfig import SchedulePolicy
     from disaggsim.metrics import _percentile, ttft
     from disaggsim.models import (HardwareSpec, ModelSpec, StageRole, builtin_catalog, kv_bytes_per_token,
                                   mm_bytes_per_token, tokens_for_request)
@@ -49,6 +50,24 @@ def main() -> None:
         except ValueError:
             errs.append([p, w, "ValueError"])
     g["irp_shard_errors"] = errs
+
+    # --- assign_instance (engine.py:65-78) and form_batch (engine.py:81-93)
+    rng0 = random.Random(65)
+    assign = []
+    for _ in range(300):
+        cands = [[i, rng0.choice([0.0, 1.0, 2.0, round(rng0.random(), 6)])]
+                 for i in sorted(rng0.sample(range(10), rng0.randint(1, 6)))]
+        ctr = rng0.randrange(0, 20)
+        for pol in SchedulePolicy:
+            assign.append([pol.value, cands, ctr, list(assign_instance(pol, [tuple(c) for c in cands], ctr))])
+    g["assign_instance"] = assign
+    batches = []
+    for _ in range(100):
+        q = list(range(rng0.randint(0, 8)))
+        fit = {i: rng0.random() < 0.8 for i in q}
+        mb = rng0.randint(1, 5)
+        batches.append([q, mb, [fit[i] for i in q], form_batch(q, mb, lambda i: fit[i])])
+    g["form_batch"] = batches
 
     # --- BlockManager op sequences (blocks.py:14-61)
     rng = random.Random(20260808)

@@ -131,3 +131,14 @@ def test_percentile():
     for vals, q, expect in G["percentile"]:
         assert orr.percentile(vals, q) == expect
         assert bench._percentile(vals, q) == expect
+
+
+def test_assign_instance_and_form_batch_golden():
+    """engine.assign_instance / form_batch (engine.py:65-93) outputs recorded from the reference."""
+    from paper_2501_05460_b200.routing import assign_instance, form_batch
+    g = G
+    assert len(g["assign_instance"]) == 900
+    for pol, cands, ctr, out in g["assign_instance"]:
+        assert list(assign_instance(pol, [tuple(c) for c in cands], ctr)) == out
+    for q, mb, fit, out in g["form_batch"]:
+        assert form_batch(q, mb, lambda i: fit[i]) == out
