@@ -176,6 +176,10 @@ epd_status_t epd_kv_move(const void* src_cache, int64_t src_segment_stride, void
                          int64_t dst_segment_stride, int32_t segments, int64_t block_bytes, const int32_t* src_ids,
                          const int32_t* dst_ids, int32_t nblocks, void* stream);
 
+/* Trace clock (trace.ShardRecord / RequestRecord times, trace.py:18-53): *slot = the GPU's
+ * %globaltimer (ns) when the stream reaches this point. */
+epd_status_t epd_timestamp(uint64_t* slot, void* stream);
+
 /* ------------------------------------------------------------------ stage handoff over NCCL
  * The NCCL legs of the stage-handoff interface, so a non-Python host can
  * run them: the EP migration of MM tokens to the prefill rank (engine._send_ready_shards /

@@ -73,6 +73,7 @@ _SIGS = {
     "epd_mmcache_check": (_i32, [_vp, _vp]),
     "epd_gather_records": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
     "epd_scatter_records": (_i32, [_vp, _vp, _i32, _i64, _vp, _vp]),
+    "epd_timestamp": (_i32, [_vp, _vp]),
     "epd_comm_version": (_i32, [C.POINTER(_i32)]),
     "epd_comm_unique_id": (_i32, [_vp]),
     "epd_comm_init": (_i32, [_vp, _i32, _i32, _i32, C.POINTER(_vp)]),

@@ -79,6 +79,13 @@ __global__ void scatter_records_kernel(const uint4* __restrict__ src, const int3
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < vecs;
        i += (size_t)gridDim.x * blockDim.x)
     d[i] = s[i];
+  __threadfence_system();  // dst may be the prefill GPU's MM pool mapped over IPC (runtime.py)
+}
+
+__global__ void timestamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
 }
 
 epd_status_t kv_copy(const void* src, void* dst, int32_t segments, int64_t seg_stride, int64_t block_bytes,
@@ -415,6 +422,12 @@ epd_status_t epd_peer_signal(uint32_t* flag, uint32_t value, void* stream) {
 epd_status_t epd_stream_wait_geq(const uint32_t* flag, uint32_t value, void* stream) {
   if (!flag) return fail(EPD_ERR_VALUE, "stream_wait_geq: null flag");
   return cuda_status(epd::stream_wait_geq(flag, value, S(stream)), "stream_wait_geq (cuStreamWaitValue32)");
+}
+
+epd_status_t epd_timestamp(uint64_t* slot, void* stream) {
+  if (!slot) return fail(EPD_ERR_VALUE, "timestamp: null slot");
+  timestamp_kernel<<<1, 1, 0, S(stream)>>>(reinterpret_cast<unsigned long long*>(slot));
+  return cuda_status((int)cudaGetLastError(), "timestamp");
 }
 
 epd_status_t epd_kv_move(const void* src_cache, int64_t src_segment_stride, void* dst_cache,

@@ -119,6 +119,7 @@ class Prefiller:
         self.mm_in = torch.zeros(T, H, dtype=bf, device=dev)
         self.ids_in = torch.zeros(T, dtype=torch.int32, device=dev)
         self.blocks_in = torch.zeros(T, dtype=torch.int32, device=dev)
+        self.mm_rows = torch.zeros(T, dtype=torch.int32, device=dev)  # paged MM input: pool row per token
         self.iota = torch.arange(T, dtype=torch.int32, device=dev)
         # RoPE (cos, sin) for positions 0..max_tokens-1, built once
         self.rope_cs = kernels.rope_table(T, cfg.head_dim, cfg.rope_theta, device=dev)
@@ -126,11 +127,14 @@ class Prefiller:
         self._graphs: dict = {}
 
     # -- one forward over the static buffers -------------------------------------------
-    def _forward(self, n_mm: int, n_text: int, kv) -> None:
+    def _forward(self, n_mm: int, n_text: int, kv, mm_pool=None) -> None:
         cfg, w = self.cfg, self.w
         T, hd, Hq, Hk = n_mm + n_text, cfg.head_dim, cfg.q_heads, cfg.kv_heads
         h = self.h[:T]
-        if n_mm:
+        if n_mm and mm_pool is not None:
+            # MM tokens straight from the prefill instance's paged MM pool (runtime.py)
+            kernels.gather_rows_f32(mm_pool, self.mm_rows[:n_mm], self.h[:n_mm])
+        elif n_mm:
             kernels.gather_rows_f32(self.mm_in, self.iota[:n_mm], self.h[:n_mm])
         if n_text:
             kernels.gather_rows_f32(w["embed"], self.ids_in[:n_text], self.h[n_mm:T])
@@ -153,11 +157,19 @@ class Prefiller:
         kernels.argmax(self.logits[0, :cfg.vocab], out=self.token)
 
     def prefill(self, mm_tokens: torch.Tensor | None, text_ids: torch.Tensor, kv=None,
-                block_ids: list[int] | torch.Tensor | None = None) -> torch.Tensor:
+                block_ids: list[int] | torch.Tensor | None = None, mm_pool: torch.Tensor | None = None,
+                mm_rows: torch.Tensor | None = None) -> torch.Tensor:
         """mm_tokens: bf16 [n_mm, hidden] on the device (the packed encode output, flattened);
-        text_ids: int32 [n_text] on the device. Returns the first token id (int32 [1], device)."""
+        or, paged, ``mm_pool`` (bf16 [rows, hidden]) with ``mm_rows`` (int32, the pool row of
+        each MM token, in request order). text_ids: int32 [n_text] on the device. Returns the
+        first token id (int32 [1], device)."""
         cfg = self.cfg
-        n_mm = 0 if mm_tokens is None else mm_tokens.shape[0]
+        if mm_pool is not None:
+            if mm_tokens is not None or mm_rows is None:
+                raise ValueError("paged prefill takes mm_pool + mm_rows instead of mm_tokens")
+            if mm_pool.dtype != torch.bfloat16 or mm_pool.shape[1] != cfg.hidden:
+                raise ValueError(f"the MM pool must be bf16 [rows, {cfg.hidden}]")
+        n_mm = mm_rows.numel() if mm_pool is not None else (0 if mm_tokens is None else mm_tokens.shape[0])
         n_text = text_ids.numel()
         T = n_mm + n_text
         if T < 1 or T > self.max_tokens:
@@ -170,23 +182,26 @@ class Prefiller:
             if ids.numel() < nb:
                 raise ValueError(f"{T} tokens need {nb} KV blocks, got {ids.numel()}")
             self.blocks_in[:nb].copy_(ids[:nb], non_blocking=True)
-        if n_mm:
+        if n_mm and mm_pool is not None:
+            self.mm_rows[:n_mm].copy_(mm_rows, non_blocking=True)
+        elif n_mm:
             self.mm_in[:n_mm].copy_(mm_tokens)
         if n_text:
             self.ids_in[:n_text].copy_(text_ids.to(torch.int32))
-        key = (n_mm, n_text, kv is not None, id(kv) if kv is not None else 0)
+        key = (n_mm, n_text, kv is not None, id(kv) if kv is not None else 0,
+               id(mm_pool) if mm_pool is not None else 0)
         if not self.use_graphs:
-            self._forward(n_mm, n_text, kv)
+            self._forward(n_mm, n_text, kv, mm_pool)
             return self.token
         g = self._graphs.get(key)
         if g is None:
-            self._forward(n_mm, n_text, kv)  # warm-up (kernel attributes, tensor maps) outside capture
+            self._forward(n_mm, n_text, kv, mm_pool)  # warm-up (kernel attributes, tensor maps) outside capture
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream(self.device)
             s.wait_stream(torch.cuda.current_stream(self.device))
             with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):
-                    self._forward(n_mm, n_text, kv)
+                    self._forward(n_mm, n_text, kv, mm_pool)
             torch.cuda.current_stream(self.device).wait_stream(s)
             self._graphs[key] = g
         g.replay()
