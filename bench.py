@@ -475,8 +475,8 @@ def run_ours(args, wl, world, rank, local):
         return
 
     enc_share = 1.0
-    if cache is not None and last is not None and last.kinds is not None:
-        enc_share = last.kinds.count("miss") / n
+    if cache is not None and last is not None and last.cache_counts is not None:
+        enc_share = last.cache_counts["miss"] / n
     peaks, peak_src = measured_peaks()
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     gemm_tflops = fl[1] / (ms[1] / 1e3) / 1e12 if ms[1] > 0 else None
@@ -542,9 +542,10 @@ def run_ours(args, wl, world, rank, local):
         line["kv_handoff"] = kv
     if gather is not None:
         line["gather"] = gather
-    if cache is not None and last is not None and last.kinds is not None:
-        line["cache"] = {"hits": last.kinds.count("hit"), "misses": last.kinds.count("miss"),
-                         "dups": last.kinds.count("dup")}
+    if cache is not None and last is not None and last.cache_counts is not None:
+        line["cache"] = {"hits": last.cache_counts["hit"], "misses": last.cache_counts["miss"],
+                         "dups": last.cache_counts["dup"], "plan": "device (epd_mmcache_plan), keyed hash",
+                         "host_reads_per_request": "20-byte miss count"}
     print(json.dumps(line), flush=True)
 
 

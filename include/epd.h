@@ -131,13 +131,32 @@ int32_t epd_encoder_profile_launches(const epd_encoder_t* enc, int32_t* cls, flo
 typedef struct epd_mmcache epd_mmcache_t;
 
 /* keys[n][2] <- content hash of n records of rec_bytes each (pitch rec_stride).
- * scratch: device buffer of >= 16*n bytes. */
+ * scratch: device buffer of >= 16*n bytes. The unkeyed form is the known-answer mode
+ * (secret = 0); a serving cache keys the hash with a per-process random secret so
+ * collisions cannot be forged offline. */
 epd_status_t epd_hash_records(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
                               uint64_t* keys, void* scratch, void* stream);
-/* Table with at least 2*capacity slots (power of two). */
+epd_status_t epd_hash_records_keyed(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
+                                    uint64_t secret0, uint64_t secret1, uint64_t* keys, void* scratch,
+                                    void* stream);
+/* Table with at least 2*capacity slots (power of two) + the device planner's LRU list, free
+ * stack and entry keys. capacity <= 16384 entries. */
 epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t** out);
 void epd_mmcache_destroy(epd_mmcache_t* cache);
-/* entry[i] = value stored for keys[i] or -1; dup[i] = first j < i with the same
+/* One request's cache plan, entirely on the device (one CTA): classify its n tiles (keys[n][2])
+ * in tile order as hit (cached) / miss (first occurrence of an uncached key) / dup (repeat of an
+ * earlier miss), refresh the hits' recency, evict least-recently-used entries not referenced by
+ * the request, hand the misses entry ids from the LIFO free stack (the BlockManager discipline,
+ * blocks.py:29-61) and insert them. Outputs (device): entries[n], kinds[n] (0/1/2),
+ * miss_tiles[n] + miss_entries[n] (first counts[0] valid, tile order), victim_keys[n][2]
+ * (first counts[3] valid, eviction order), counts[5] = misses, hits, dups, victims, status
+ * (1: more distinct tiles than entries -- CapacityExceeded, nothing changed). n <= 4096.
+ * The only value a host needs back is counts (the number of tiles to encode). */
+epd_status_t epd_mmcache_plan(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, int32_t* entries,
+                              int32_t* kinds, int32_t* miss_tiles, int32_t* miss_entries, uint64_t* victim_keys,
+                              int32_t* counts, void* stream);
+/* Low-level table access (not mixed with epd_mmcache_plan on one cache):
+ * entry[i] = value stored for keys[i] or -1; dup[i] = first j < i with the same
  * key among misses, else -1 (in-batch repeats). */
 epd_status_t epd_mmcache_lookup(epd_mmcache_t* cache, const uint64_t* keys, int32_t n,
                                 int32_t* entry, int32_t* dup, void* stream);
@@ -145,6 +164,7 @@ epd_status_t epd_mmcache_lookup(epd_mmcache_t* cache, const uint64_t* keys, int3
 epd_status_t epd_mmcache_insert(epd_mmcache_t* cache, const uint64_t* keys, const int32_t* entries,
                                 int32_t n, void* stream);
 epd_status_t epd_mmcache_erase(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, void* stream);
+/* Empty the table and reset the planner (free stack 0, 1, 2, ... again). */
 epd_status_t epd_mmcache_clear(epd_mmcache_t* cache, void* stream);
 /* Synchronises `stream`; EPD_ERR_CAPACITY if any insert found no free slot. */
 epd_status_t epd_mmcache_check(epd_mmcache_t* cache, void* stream);

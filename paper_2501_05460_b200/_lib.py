@@ -64,6 +64,8 @@ _SIGS = {
     "epd_encoder_profile_read": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32]),
     "epd_encoder_profile_launches": (_i32, [_vp, _vp, _vp, _vp, _i32]),
     "epd_hash_records": (_i32, [_vp, _i32, _i64, _i64, _vp, _vp, _vp]),
+    "epd_hash_records_keyed": (_i32, [_vp, _i32, _i64, _i64, C.c_uint64, C.c_uint64, _vp, _vp, _vp]),
+    "epd_mmcache_plan": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "epd_mmcache_create": (_i32, [_i64, _i32, C.POINTER(_vp)]),
     "epd_mmcache_destroy": (None, [_vp]),
     "epd_mmcache_lookup": (_i32, [_vp, _vp, _i32, _vp, _vp, _vp]),

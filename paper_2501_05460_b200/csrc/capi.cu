@@ -116,7 +116,9 @@ struct epd_encoder {
 
 struct epd_mmcache {
   epd::DeviceTable t;
+  epd::DevicePlanner p;
   void* mem = nullptr;
+  void* pmem = nullptr;
   int device = 0;
 };
 
@@ -268,6 +270,12 @@ int32_t epd_encoder_profile_launches(const epd_encoder_t* enc, int32_t* cls, flo
 
 epd_status_t epd_hash_records(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
                               uint64_t* keys, void* scratch, void* stream) {
+  return epd_hash_records_keyed(data, n, rec_bytes, rec_stride, 0, 0, keys, scratch, stream);
+}
+
+epd_status_t epd_hash_records_keyed(const void* data, int32_t n, int64_t rec_bytes, int64_t rec_stride,
+                                    uint64_t secret0, uint64_t secret1, uint64_t* keys, void* scratch,
+                                    void* stream) {
   if (n < 0 || rec_bytes < 0 || rec_stride < rec_bytes) return fail(EPD_ERR_VALUE, "hash: bad geometry");
   if (rec_bytes % 8) return fail(EPD_ERR_VALUE, "hash: record length must be a multiple of 8 bytes");
   if (n == 0) return EPD_OK;
@@ -275,12 +283,14 @@ epd_status_t epd_hash_records(const void* data, int32_t n, int64_t rec_bytes, in
   if (n > 65535) return fail(EPD_ERR_VALUE, "hash: at most 65535 records per call");
   int rc = epd::hash_records(data, n, (size_t)rec_bytes, (size_t)rec_stride,
                              reinterpret_cast<unsigned long long*>(scratch),
-                             reinterpret_cast<unsigned long long*>(keys), S(stream));
+                             reinterpret_cast<unsigned long long*>(keys), S(stream), secret0, secret1);
   return cuda_status(rc, "hash_records");
 }
 
 epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t** out) {
   if (!out || capacity < 1) return fail(EPD_ERR_VALUE, "cache capacity must be >= 1");
+  if (capacity > epd::planner_max_capacity())
+    return fail(EPD_ERR_UNSUPPORTED, "cache capacity above " + std::to_string(epd::planner_max_capacity()));
   *out = nullptr;
   if (cudaSetDevice(device) != cudaSuccess) return fail(EPD_ERR_CUDA, "cudaSetDevice failed");
   unsigned long long slots = 16;
@@ -289,7 +299,11 @@ epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t*
   c->device = device;
   const size_t bytes = slots * 16 + slots * 4 + 256;
   cudaError_t e = cudaMalloc(&c->mem, bytes);
+  const size_t C = (size_t)capacity;
+  const size_t pbytes = C * 16 + 3 * C * 4 + 64;
+  if (e == cudaSuccess) e = cudaMalloc(&c->pmem, pbytes);
   if (e != cudaSuccess) {
+    if (c->mem) cudaFree(c->mem);
     delete c;
     return fail(EPD_ERR_CUDA, std::string("cudaMalloc(cache table): ") + cudaGetErrorString(e));
   }
@@ -298,6 +312,21 @@ epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t*
   c->t.keys = reinterpret_cast<unsigned long long*>(c->mem);
   c->t.vals = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->mem) + slots * 16);
   c->t.status = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c->mem) + slots * 20);
+  uint8_t* pm = reinterpret_cast<uint8_t*>(c->pmem);
+  c->p.capacity = (int32_t)capacity;
+  c->p.entry_key = reinterpret_cast<unsigned long long*>(pm);
+  c->p.prev = reinterpret_cast<int32_t*>(pm + C * 16);
+  c->p.next = c->p.prev + C;
+  c->p.free_stack = c->p.next + C;
+  c->p.state = c->p.free_stack + C;
+  int rc = epd::planner_reset(c->t, c->p, 0);
+  if (!rc) rc = (int)cudaDeviceSynchronize();
+  if (rc) {
+    cudaFree(c->mem);
+    cudaFree(c->pmem);
+    delete c;
+    return cuda_status(rc, "mmcache_create");
+  }
   *out = c;
   return EPD_OK;
 }
@@ -305,7 +334,24 @@ epd_status_t epd_mmcache_create(int64_t capacity, int32_t device, epd_mmcache_t*
 void epd_mmcache_destroy(epd_mmcache_t* cache) {
   if (!cache) return;
   if (cache->mem) cudaFree(cache->mem);
+  if (cache->pmem) cudaFree(cache->pmem);
   delete cache;
+}
+
+epd_status_t epd_mmcache_plan(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, int32_t* entries,
+                              int32_t* kinds, int32_t* miss_tiles, int32_t* miss_entries, uint64_t* victim_keys,
+                              int32_t* counts, void* stream) {
+  if (!cache || n < 0 || (n && (!keys || !entries || !kinds || !miss_tiles || !miss_entries || !victim_keys)) ||
+      !counts)
+    return fail(EPD_ERR_VALUE, "mmcache_plan: bad arguments");
+  if ((size_t)n > epd::planner_max_tiles())
+    return fail(EPD_ERR_UNSUPPORTED, "mmcache_plan: more than " + std::to_string(epd::planner_max_tiles()) +
+                                         " tiles in one request");
+  epd::PlanOut o{entries, kinds, miss_tiles, miss_entries, reinterpret_cast<unsigned long long*>(victim_keys),
+                 counts};
+  int rc = epd::planner_plan(cache->t, cache->p, reinterpret_cast<const unsigned long long*>(keys), n, o,
+                             S(stream));
+  return cuda_status(rc, "mmcache_plan");
 }
 
 epd_status_t epd_mmcache_lookup(epd_mmcache_t* cache, const uint64_t* keys, int32_t n, int32_t* entry,
@@ -335,8 +381,7 @@ epd_status_t epd_mmcache_erase(epd_mmcache_t* cache, const uint64_t* keys, int32
 
 epd_status_t epd_mmcache_clear(epd_mmcache_t* cache, void* stream) {
   if (!cache) return fail(EPD_ERR_VALUE, "clear: null cache");
-  int rc = (int)cudaMemsetAsync(cache->mem, 0, cache->t.capacity * 20 + 256, S(stream));
-  return cuda_status(rc, "mmcache_clear");
+  return cuda_status(epd::planner_reset(cache->t, cache->p, S(stream)), "mmcache_clear");
 }
 
 epd_status_t epd_mmcache_check(epd_mmcache_t* cache, void* stream) {

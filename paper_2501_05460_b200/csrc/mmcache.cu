@@ -1,12 +1,16 @@
 // Multimodal-token cache: tile-content hash (K11) and a GPU-resident
 // open-addressing hash table keyed by that hash (K12).
 //
-// Content hash (the cache key) of a byte record of length L (L % 8 == 0):
+// Content hash (the cache key) of a byte record of length L (L % 8 == 0), keyed with a
+// per-process secret (s0, s1) (0, 0 = the fixed known-answer mode):
 //   w_i  = little-endian u64 word i
-//   x_i  = w_i ^ (i * 0x9E3779B97F4A7C15 + 0x243F6A8885A308D3)
-//   a_i  = fmix64(x_i);  b_i = fmix64(a_i + 0x632BE59BD9B4E019)
-//   key0 = fmix64((sum a_i) ^ L);  key1 = fmix64((sum b_i) + L * 0xD6E8FEB86659FD93)
+//   x_i  = w_i ^ (i * 0x9E3779B97F4A7C15 + (0x243F6A8885A308D3 ^ s0))
+//   a_i  = fmix64(x_i);  b_i = fmix64(a_i + (0x632BE59BD9B4E019 ^ s1))
+//   key0 = fmix64((sum a_i) ^ L ^ s1);  key1 = fmix64((sum b_i) + L * 0xD6E8FEB86659FD93 + s0)
 //   if key0 == 0: key0 = 1          (key0 == 0 marks empty / tombstone slots)
+// Without the secret the key is a public sum of per-word terms, and a generalized-birthday
+// (k-sum) search can forge a tile that collides with a popular image; with it an attacker
+// cannot evaluate the per-word terms.
 // Sums are mod 2^64 and order-independent, so any thread/block decomposition
 // produces identical keys (bit-exact with oracle/hashing.py).
 //
@@ -36,7 +40,9 @@ __device__ __forceinline__ unsigned long long fmix64(unsigned long long k) {
 
 __global__ void __launch_bounds__(256) hash_accum_kernel(const uint8_t* __restrict__ data,
                                                          size_t rec_bytes, size_t rec_stride,
-                                                         unsigned long long* __restrict__ acc) {
+                                                         unsigned long long* __restrict__ acc,
+                                                         unsigned long long s0, unsigned long long s1) {
+  const unsigned long long kSeedK = kSeed ^ s0, kLaneK = kLaneB ^ s1;
   const int rec = blockIdx.y;
   const size_t nwords = rec_bytes / 8;
   const uint8_t* base = data + (size_t)rec * rec_stride;
@@ -51,25 +57,25 @@ __global__ void __launch_bounds__(256) hash_accum_kernel(const uint8_t* __restri
     for (size_t i = tid; i < npairs; i += nth) {
       ulonglong2 w = p[i];
       const unsigned long long i0 = 2 * i, i1 = 2 * i + 1;
-      unsigned long long a0 = fmix64(w.x ^ (i0 * kGolden + kSeed));
-      unsigned long long a1 = fmix64(w.y ^ (i1 * kGolden + kSeed));
+      unsigned long long a0 = fmix64(w.x ^ (i0 * kGolden + kSeedK));
+      unsigned long long a1 = fmix64(w.y ^ (i1 * kGolden + kSeedK));
       sa += a0 + a1;
-      sb += fmix64(a0 + kLaneB) + fmix64(a1 + kLaneB);
+      sb += fmix64(a0 + kLaneK) + fmix64(a1 + kLaneK);
     }
     if (tid == 0 && (nwords & 1)) {
       const size_t i = nwords - 1;
       unsigned long long w = reinterpret_cast<const unsigned long long*>(base)[i];
-      unsigned long long a = fmix64(w ^ (i * kGolden + kSeed));
+      unsigned long long a = fmix64(w ^ (i * kGolden + kSeedK));
       sa += a;
-      sb += fmix64(a + kLaneB);
+      sb += fmix64(a + kLaneK);
     }
   } else {
     for (size_t i = tid; i < nwords; i += nth) {
       unsigned long long w = 0;
       for (int j = 7; j >= 0; --j) w = (w << 8) | base[i * 8 + j];
-      unsigned long long a = fmix64(w ^ (i * kGolden + kSeed));
+      unsigned long long a = fmix64(w ^ (i * kGolden + kSeedK));
       sa += a;
-      sb += fmix64(a + kLaneB);
+      sb += fmix64(a + kLaneK);
     }
   }
 #pragma unroll
@@ -96,11 +102,12 @@ __global__ void __launch_bounds__(256) hash_accum_kernel(const uint8_t* __restri
 }
 
 __global__ void hash_finalize_kernel(const unsigned long long* __restrict__ acc, int n,
-                                     unsigned long long len, unsigned long long* __restrict__ keys) {
+                                     unsigned long long len, unsigned long long* __restrict__ keys,
+                                     unsigned long long s0, unsigned long long s1) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  unsigned long long k0 = fmix64(acc[2 * i] ^ len);
-  unsigned long long k1 = fmix64(acc[2 * i + 1] + len * kLenMul);
+  unsigned long long k0 = fmix64(acc[2 * i] ^ len ^ s1);
+  unsigned long long k1 = fmix64(acc[2 * i + 1] + len * kLenMul + s0);
   if (k0 == 0) k0 = 1;
   keys[2 * i] = k0;
   keys[2 * i + 1] = k1;
@@ -184,10 +191,269 @@ __global__ void table_erase_kernel(unsigned long long* __restrict__ tkeys, int32
   }
 }
 
+
+// ------------------------------------------------------------------ planner
+// The whole request plan on the GPU (oracle/mmcache.py is the specification): one CTA
+//   1. looks every tile's key up in the table and finds each key's first occurrence in the
+//      request (all threads);
+//   2. classifies tiles (hit / miss = first occurrence of an uncached key / dup) and numbers
+//      the misses in tile order (block scan);
+//   3. (one thread, the LRU list in shared memory) refreshes the distinct hits in tile order,
+//      evicts the least-recently-used unpinned entries the misses need (their ids go back on
+//      the LIFO free stack, their keys leave the table) and gives each miss, in tile order, the
+//      id on top of the stack;
+//   4. inserts the misses into the table (all threads, CAS) and resolves every tile's entry.
+// Erased keys leave tombstones; when they exceed a quarter of the slots the same CTA rebuilds
+// the table from the live entries, so probe chains cannot grow without bound under churn.
+constexpr int kPlanThreads = 1024;
+constexpr int kPlanMaxTiles = 4096;
+constexpr int kPlanMaxCapacity = 16384;
+
+__device__ __forceinline__ int table_find(const unsigned long long* tkeys, unsigned long long mask,
+                                          unsigned long long k0, unsigned long long k1) {
+  unsigned long long s = k0 & mask;
+  for (unsigned long long probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+    const unsigned long long a = tkeys[2 * s], b = tkeys[2 * s + 1];
+    if (a == 0 && b == 0) return -1;
+    if (a == k0 && b == k1) return (int)s;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void table_claim(unsigned long long* tkeys, int32_t* tvals, unsigned long long mask,
+                                            unsigned long long k0, unsigned long long k1, int32_t v,
+                                            int32_t* tombs, int32_t* status) {
+  unsigned long long s = k0 & mask;
+  for (unsigned long long probe = 0; probe <= mask; ++probe, s = (s + 1) & mask) {
+    if (atomicCAS(&tkeys[2 * s], 0ull, k0) == 0ull) {
+      if (atomicExch(&tkeys[2 * s + 1], k1) == 1ull) atomicSub(tombs, 1);  // reused a tombstone
+      tvals[s] = v;
+      return;
+    }
+  }
+  atomicExch(status, 1);
+}
+
+__global__ void __launch_bounds__(kPlanThreads) planner_reset_kernel(DevicePlanner p) {
+  for (int e = threadIdx.x; e < p.capacity; e += blockDim.x) {
+    p.prev[e] = -1;
+    p.next[e] = -1;
+    p.free_stack[e] = p.capacity - 1 - e;
+    p.entry_key[2 * e] = 0;
+    p.entry_key[2 * e + 1] = 0;
+  }
+  if (threadIdx.x == 0) {
+    p.state[0] = -1;  // head (least recently used)
+    p.state[1] = -1;  // tail (most recently used)
+    p.state[2] = p.capacity;
+    p.state[3] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(kPlanThreads) planner_kernel(DeviceTable t, DevicePlanner p,
+                                                              const unsigned long long* __restrict__ keys, int n,
+                                                              PlanOut out) {
+  extern __shared__ int32_t sm[];
+  const int C = p.capacity;
+  int32_t* prev = sm;           // [C]
+  int32_t* next = prev + C;     // [C]
+  int32_t* looked = next + C;   // [n]
+  int32_t* first = looked + n;  // [n]
+  int32_t* mpos = first + n;    // [n] miss number of a first-occurrence miss
+  __shared__ int32_t part[kPlanThreads];
+  __shared__ int32_t sh_m, sh_abort;
+  const unsigned long long mask = t.capacity - 1;
+  const int tid = threadIdx.x;
+
+  for (int e = tid; e < C; e += blockDim.x) {
+    prev[e] = p.prev[e];
+    next[e] = p.next[e];
+  }
+  for (int i = tid; i < n; i += blockDim.x) {
+    const unsigned long long k0 = keys[2 * i], k1 = keys[2 * i + 1];
+    const int s = table_find(t.keys, mask, k0, k1);
+    looked[i] = s < 0 ? -1 : t.vals[s];
+    int f = i;
+    for (int j = 0; j < i; ++j)
+      if (keys[2 * j] == k0 && keys[2 * j + 1] == k1) {
+        f = j;
+        break;
+      }
+    first[i] = f;
+  }
+  __syncthreads();
+  // miss numbering in tile order: each thread scans a contiguous chunk
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = tid * per, hi = min(n, lo + per);
+  int cnt = 0;
+  for (int i = lo; i < hi; ++i) cnt += (looked[i] < 0 && first[i] == i);
+  part[tid] = cnt;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {
+    const int v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int base = part[tid] - cnt;
+  for (int i = lo; i < hi; ++i)
+    if (looked[i] < 0 && first[i] == i) {
+      mpos[i] = base;
+      out.miss_tiles[base] = i;
+      ++base;
+    }
+  __syncthreads();
+
+  if (tid == 0) {
+    const int m = part[blockDim.x - 1];
+    int hits = 0, dups = 0, dhits = 0;
+    for (int i = 0; i < n; ++i) {
+      if (looked[i] >= 0) {
+        ++hits;
+        dhits += first[i] == i;
+      } else if (first[i] != i) {
+        ++dups;
+      }
+    }
+    sh_m = m;
+    sh_abort = 0;
+    int* st = p.state;
+    if (m + dhits > C) {  // more distinct tiles than entries: CapacityExceeded, state untouched
+      sh_abort = 1;
+      out.counts[0] = m;
+      out.counts[1] = hits;
+      out.counts[2] = dups;
+      out.counts[3] = 0;
+      out.counts[4] = 1;
+    } else {
+      int head = st[0], tail = st[1], top = st[2];
+      auto unlink = [&](int e) {
+        const int a = prev[e], b = next[e];
+        if (a >= 0) next[a] = b; else head = b;
+        if (b >= 0) prev[b] = a; else tail = a;
+        prev[e] = next[e] = -1;
+      };
+      auto append = [&](int e) {
+        prev[e] = tail;
+        next[e] = -1;
+        if (tail >= 0) next[tail] = e; else head = e;
+        tail = e;
+      };
+      for (int i = 0; i < n; ++i)  // refresh the distinct hits, tile order (pinned at the MRU end)
+        if (looked[i] >= 0 && first[i] == i) {
+          unlink(looked[i]);
+          append(looked[i]);
+        }
+      int nv = 0;
+      while (top < m) {  // evict least recently used; ids return to the free stack in that order
+        const int e = head;
+        unlink(e);
+        const unsigned long long k0 = p.entry_key[2 * e], k1 = p.entry_key[2 * e + 1];
+        const int s = table_find(t.keys, mask, k0, k1);
+        if (s >= 0) {
+          t.keys[2 * s + 1] = 1ull;  // tombstone (0, 1)
+          t.keys[2 * s] = 0ull;
+          t.vals[s] = -1;
+          st[3] += 1;
+        }
+        out.victim_keys[2 * nv] = k0;
+        out.victim_keys[2 * nv + 1] = k1;
+        ++nv;
+        p.free_stack[top++] = e;
+      }
+      for (int r = 0; r < m; ++r) {
+        const int e = p.free_stack[--top];
+        const int i = out.miss_tiles[r];
+        out.miss_entries[r] = e;
+        p.entry_key[2 * e] = keys[2 * i];
+        p.entry_key[2 * e + 1] = keys[2 * i + 1];
+        append(e);
+      }
+      st[0] = head;
+      st[1] = tail;
+      st[2] = top;
+      out.counts[0] = m;
+      out.counts[1] = hits;
+      out.counts[2] = dups;
+      out.counts[3] = nv;
+      out.counts[4] = 0;
+    }
+  }
+  __syncthreads();
+  if (sh_abort) return;
+  const int m = sh_m;
+  for (int e = tid; e < C; e += blockDim.x) {
+    p.prev[e] = prev[e];
+    p.next[e] = next[e];
+  }
+  for (int r = tid; r < m; r += blockDim.x) {
+    const int i = out.miss_tiles[r];
+    table_claim(t.keys, t.vals, mask, keys[2 * i], keys[2 * i + 1], out.miss_entries[r], &p.state[3], t.status);
+  }
+  for (int i = tid; i < n; i += blockDim.x) {
+    if (looked[i] >= 0) {
+      out.entries[i] = looked[i];
+      out.kinds[i] = 0;
+    } else {
+      out.entries[i] = out.miss_entries[mpos[first[i]]];
+      out.kinds[i] = first[i] == i ? 1 : 2;
+    }
+  }
+  __syncthreads();
+  // rebuild the table once tombstones exceed a quarter of the slots
+  if ((unsigned long long)p.state[3] * 4 > t.capacity) {
+    for (unsigned long long s = tid; s < t.capacity; s += blockDim.x) {
+      t.keys[2 * s] = 0;
+      t.keys[2 * s + 1] = 0;
+      t.vals[s] = -1;
+    }
+    __syncthreads();
+    if (tid == 0) p.state[3] = 0;
+    __syncthreads();
+    for (int e = tid; e < C; e += blockDim.x) {
+      const bool live = prev[e] >= 0 || next[e] >= 0 || p.state[0] == e;
+      if (live) table_claim(t.keys, t.vals, mask, p.entry_key[2 * e], p.entry_key[2 * e + 1], e, &p.state[3],
+                            t.status);
+    }
+  }
+}
+
+}  // namespace
+
+size_t planner_max_tiles() { return kPlanMaxTiles; }
+int32_t planner_max_capacity() { return kPlanMaxCapacity; }
+
+int planner_reset(const DeviceTable& t, const DevicePlanner& p, cudaStream_t stream) {
+  cudaError_t e = cudaMemsetAsync(t.keys, 0, t.capacity * 16, stream);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaMemsetAsync(t.vals, 0xff, t.capacity * 4, stream);
+  if (e != cudaSuccess) return (int)e;
+  e = cudaMemsetAsync(t.status, 0, 4, stream);
+  if (e != cudaSuccess) return (int)e;
+  planner_reset_kernel<<<1, kPlanThreads, 0, stream>>>(p);
+  return (int)cudaGetLastError();
+}
+
+int planner_plan(const DeviceTable& t, const DevicePlanner& p, const unsigned long long* keys, int n,
+                 const PlanOut& out, cudaStream_t stream) {
+  if (n < 0 || n > kPlanMaxTiles || p.capacity > kPlanMaxCapacity) return 1004;
+  const size_t smem = (size_t)(2 * p.capacity + 3 * n) * sizeof(int32_t);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(planner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((2 * kPlanMaxCapacity + 3 * kPlanMaxTiles) * sizeof(int32_t)));
+    attr = true;
+  }
+  planner_kernel<<<1, kPlanThreads, smem, stream>>>(t, p, keys, n, out);
+  return (int)cudaGetLastError();
+}
+
+namespace {
 }  // namespace
 
 int hash_records(const void* data, int n, size_t rec_bytes, size_t rec_stride,
-                 unsigned long long* acc_scratch, unsigned long long* keys, cudaStream_t stream) {
+                 unsigned long long* acc_scratch, unsigned long long* keys, cudaStream_t stream,
+                 unsigned long long s0, unsigned long long s1) {
   if (n <= 0) return 0;
   if (rec_bytes % 8) return 1002;
   cudaError_t e = cudaMemsetAsync(acc_scratch, 0, sizeof(unsigned long long) * 2 * n, stream);
@@ -197,9 +463,9 @@ int hash_records(const void* data, int n, size_t rec_bytes, size_t rec_stride,
   if (bx < 1) bx = 1;
   if (bx > 16) bx = 16;
   hash_accum_kernel<<<dim3(bx, n), 256, 0, stream>>>(reinterpret_cast<const uint8_t*>(data), rec_bytes,
-                                                     rec_stride, acc_scratch);
+                                                     rec_stride, acc_scratch, s0, s1);
   hash_finalize_kernel<<<(n + 127) / 128, 128, 0, stream>>>(acc_scratch, n, (unsigned long long)rec_bytes,
-                                                            keys);
+                                                            keys, s0, s1);
   return (int)cudaGetLastError();
 }
 

@@ -49,7 +49,8 @@ class RequestResult:
     n_tiles: int
     encoded_tiles: int
     shards: list = field(default_factory=list)
-    kinds: list | None = None           # cache classification per tile (hit/miss/dup)
+    cache_counts: dict | None = None     # MM-token cache: {"hit", "miss", "dup"} tile counts
+    plan: object | None = None           # the cache plan (device tensors; plan.kinds reads them back)
     ep_bytes: int = 0                    # bytes moved to the prefill rank (engine.py:524)
     tokens: torch.Tensor | None = None   # packed [n, tokens_per_tile, hidden] on the prefill rank
     readback: torch.cuda.Event | None = None  # set when tokens were copied into out_host
@@ -355,27 +356,32 @@ class EncodeStage:
             res.tokens = packed
             return res
 
-        # ---- cached path (cache on the prefill rank)
-        from .mmcache import hash_tiles
+        # ---- cached path (cache on the prefill rank): the plan stays on the device; the
+        # host learns only the miss count (the number of tiles to encode)
         plan = None
         release_all = release_mine = None
+        miss_dev = None
         if is_sink:
             if tiles_dev is not None:
                 all_dev = tiles_dev
             else:
                 all_dev, release_all = self._upload(tiles_host, None)
-            keys = hash_tiles(all_dev.contiguous())
-            plan = self.cache.plan(keys)
-            miss = torch.as_tensor(plan.miss_tiles, dtype=torch.int64)
+            plan = self.cache.plan(self.cache.hash(all_dev.contiguous()))
+            m = plan.n_miss
+            miss_dev = plan.miss_tiles.long()
         if self.world > 1:
-            cnt = torch.tensor([0 if plan is None else len(plan.miss_tiles)], dtype=torch.int64, device=self.device)
+            on_dev = dist.get_backend(self.group) == "nccl"
+            cnt = torch.tensor([0 if plan is None else m], dtype=torch.int64,
+                               device=self.device if on_dev else "cpu")
             dist.broadcast(cnt, self.prefill_rank, group=self.group)
             m = int(cnt.item())
-            midx = miss.to(self.device) if is_sink else torch.empty(m, dtype=torch.int64, device=self.device)
             if m:
+                if is_sink:
+                    midx = miss_dev if on_dev else miss_dev.cpu()
+                else:
+                    midx = torch.empty(m, dtype=torch.int64, device=self.device if on_dev else "cpu")
                 dist.broadcast(midx, self.prefill_rank, group=self.group)
-            miss = midx.cpu()
-        m = miss.numel()
+                miss_dev = midx.to(self.device)
         ranges = shard_ranges(m, self.world)
         first, count = ranges[self.rank]
         # every rank knows m, so every rank picks the same transport for this request
@@ -383,15 +389,15 @@ class EncodeStage:
         staging = ex["dest"]
         local = None
         if count > 0:
-            my = miss[first:first + count]
+            my = miss_dev[first:first + count]
             if is_sink:
-                src = all_dev.index_select(0, my.to(self.device))
+                src = all_dev.index_select(0, my)
                 local = staging[first:first + count]
             else:
                 if tiles_dev is not None:
-                    src = tiles_dev.index_select(0, my.to(self.device))
+                    src = tiles_dev.index_select(0, my)
                 else:
-                    src, release_mine = self._upload(tiles_host, my)
+                    src, release_mine = self._upload(tiles_host, my.cpu())  # host tiles: index on the host
                 local = self._buffer(count)
             self.enc.encode(src.contiguous(), local)
         for release in (release_all, release_mine):
@@ -407,14 +413,13 @@ class EncodeStage:
             rec = tpp * bpt
             s = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
             if m:
-                ent = torch.as_tensor(plan.miss_entries, dtype=torch.int32).to(self.device)
-                call("epd_scatter_records", C.c_void_p(staging.data_ptr()), C.c_void_p(ent.data_ptr()), m, rec,
-                     C.c_void_p(self.cache.store.data_ptr()), s)
+                call("epd_scatter_records", C.c_void_p(staging.data_ptr()), C.c_void_p(plan.miss_entries.data_ptr()),
+                     m, rec, C.c_void_p(self.cache.store.data_ptr()), s)
             packed = self._buffer(n)
-            idx = torch.as_tensor(plan.entries, dtype=torch.int32).to(self.device)
-            call("epd_gather_records", C.c_void_p(self.cache.store.data_ptr()), C.c_void_p(idx.data_ptr()), n, rec,
-                 C.c_void_p(packed.data_ptr()), s)
-            res.kinds = plan.kinds
+            call("epd_gather_records", C.c_void_p(self.cache.store.data_ptr()), C.c_void_p(plan.entries.data_ptr()),
+                 n, rec, C.c_void_p(packed.data_ptr()), s)
+            res.plan = plan
+            res.cache_counts = plan.counts
             res.tokens = packed
         return res
 

@@ -27,18 +27,62 @@ def test_cache_sequence_matches_oracle(cuda):
     from paper_2501_05460_b200.mmcache import MMTokenCache
     rng = np.random.default_rng(11)
     pool = rng.integers(0, 256, (30, 8 * 8 * 3), dtype=np.uint8)  # 30 distinct records
-    cache = MMTokenCache(capacity=12, tokens_per_tile=4, hidden=8, device=cuda)
+    secret = (0x0123456789ABCDEF, 0xFEDCBA9876543210)
+    cache = MMTokenCache(capacity=12, tokens_per_tile=4, hidden=8, device=cuda, secret=secret)
     oracle = MMCacheOracle(12)
-    from paper_2501_05460_b200.mmcache import hash_tiles
-    for step in range(40):
+    for step in range(400):
         n = int(rng.integers(1, 12))
         ids = rng.integers(0, 30 if step > 5 else 10, n)
         tiles = torch.from_numpy(pool[ids]).to(cuda)
-        plan = cache.plan(hash_tiles(tiles))
-        expect = oracle.process([content_hash(pool[i]) for i in ids])
+        plan = cache.plan(cache.hash(tiles))
+        expect = oracle.process([content_hash(pool[i], secret) for i in ids])
         got = list(zip(plan.kinds, [int(e) for e in plan.entries]))
         assert got == expect, step
         assert plan.victims == oracle.last_victims
+        assert plan.miss_tiles.tolist() == [i for i, (k, _) in enumerate(expect) if k == "miss"]
+        assert len(cache) == len(oracle)
+    cache.check()
+
+
+def test_keyed_hash_matches_oracle_and_differs_per_secret(cuda):
+    from paper_2501_05460_b200.mmcache import MMTokenCache, hash_tiles
+    rng = np.random.default_rng(4)
+    arr = rng.integers(0, 256, (3, 448, 448, 3), dtype=np.uint8)
+    t = torch.from_numpy(arr).to(cuda)
+    for secret in [(1, 2), (2 ** 64 - 1, 12345)]:
+        keys = hash_tiles(t, secret=secret).cpu().numpy().view(np.uint64)
+        for i in range(3):
+            assert tuple(int(k) for k in keys[i]) == content_hash(arr[i], secret)
+    a, b = MMTokenCache(4, 4, 8, cuda), MMTokenCache(4, 4, 8, cuda)
+    assert a.secret != b.secret  # random per cache: keys cannot be precomputed offline
+    assert not torch.equal(a.hash(t), b.hash(t))
+
+
+def test_cache_churn_keeps_probe_chains_short(cuda):
+    """Eviction churn: every request brings new tiles, so every plan evicts; the
+    planner rebuilds the table once tombstones pass a quarter of the slots, and plans stay
+    exact and fast after thousands of evictions."""
+    import time
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    rng = np.random.default_rng(5)
+    cache = MMTokenCache(capacity=64, tokens_per_tile=4, hidden=8, device=cuda, secret=0)
+    oracle = MMCacheOracle(64)
+    times = []
+    for step in range(600):
+        recs = rng.integers(0, 256, (16, 64), dtype=np.uint8)
+        recs[:4] = np.frombuffer(np.uint64(step // 3).tobytes() * 8, dtype=np.uint8)  # a few repeats
+        t = torch.from_numpy(recs).to(cuda)
+        keys = cache.hash(t)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan = cache.plan(keys)
+        times.append(time.perf_counter() - t0)
+        expect = oracle.process([content_hash(r) for r in recs])
+        assert list(zip(plan.kinds, [int(e) for e in plan.entries])) == expect, step
+    assert cache.stats["evicted"] > 4000
+    early, late = sorted(times[20:120])[50], sorted(times[-100:])[50]
+    print(f"plan p50: first {early * 1e6:.0f} us, last {late * 1e6:.0f} us")
+    assert late < 2 * early + 50e-6
     cache.check()
 
 
@@ -56,9 +100,10 @@ def test_cached_stage_bit_exact(cuda):
     cache = MMTokenCache(64, cfg.out_tokens, cfg.out_dim, cuda)
     st = EncodeStage(enc, cuda, cache=cache)
     r1 = st.process(tiles.pin_memory())
-    assert r1.kinds.count("miss") == 20 and r1.kinds.count("dup") == 20 and r1.encoded_tiles == 20
+    assert r1.cache_counts == {"hit": 0, "miss": 20, "dup": 20} and r1.encoded_tiles == 20
+    assert r1.plan.kinds == ["miss"] * 20 + ["dup"] * 20
     r2 = st.process(tiles.pin_memory())
-    assert r2.kinds == ["hit"] * 40 and r2.encoded_tiles == 0
+    assert r2.plan.kinds == ["hit"] * 40 and r2.encoded_tiles == 0
     torch.cuda.synchronize()
     assert torch.equal(r1.tokens, direct)
     assert torch.equal(r2.tokens, direct)
