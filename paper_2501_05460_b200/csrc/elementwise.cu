@@ -195,16 +195,33 @@ __global__ void __launch_bounds__(256, EPD_LN_MINB) layernorm_resid_kernel(const
 
 // One block per (tile, patch row). Stage p image rows in smem, then emit
 // S/p patches x Kpad columns in (c, ky, kx) order.
-__global__ void patchify_kernel(const uint8_t* __restrict__ tiles, int S, int C, int p, int Kpad,
-                                int row_offset, int rows_per_tile, float m0, float m1, float m2,
-                                float s0, float s1, float s2, bf16* __restrict__ out) {
-  extern __shared__ uint8_t strip[];  // p * S * C bytes
+// uint8 HWC tiles -> normalized bf16 im2col rows (K padded to Kpad, zeros beyond C*p*p).
+// One block per (tile, strip of p image rows): the strip is staged in shared memory with
+// 16-byte loads, a per-block table maps each of the Kpad columns to its strip offset and
+// channel, and every thread emits 8 consecutive columns as one 16-byte store.
+__global__ void __launch_bounds__(256) patchify_kernel(const uint8_t* __restrict__ tiles, int S, int C, int p,
+                                                     int Kpad, int row_offset, int rows_per_tile, float m0,
+                                                     float m1, float m2, float s0, float s1, float s2,
+                                                     bf16* __restrict__ out) {
+  extern __shared__ uint8_t strip[];  // p * S * C bytes, then Kpad int32 column offsets
+  const size_t strip_bytes = (size_t)p * S * C;
+  int32_t* tab = reinterpret_cast<int32_t*>(strip + ((strip_bytes + 15) & ~size_t(15)));
+  const int kreal = C * p * p;
+  for (int col = threadIdx.x; col < Kpad; col += blockDim.x) {
+    int t = -1;
+    if (col < kreal) {
+      const int c = col / (p * p);
+      const int r = col - c * p * p;
+      const int ky = r / p, kx = r - ky * p;
+      t = ((ky * S + kx) * C + c) | (c << 28);  // strip offset (< 2^28) and channel
+    }
+    tab[col] = t;
+  }
   pdl_trigger();
   pdl_wait();
   const int tile = blockIdx.y;
   const int py = blockIdx.x;
   const int np = S / p;
-  const size_t strip_bytes = (size_t)p * S * C;
   const uint8_t* src = tiles + (size_t)tile * S * S * C + (size_t)py * strip_bytes;
   for (size_t i = threadIdx.x * 16; i < strip_bytes; i += blockDim.x * 16) {
     if (i + 16 <= strip_bytes && ((reinterpret_cast<uintptr_t>(src + i) & 15) == 0))
@@ -215,21 +232,24 @@ __global__ void patchify_kernel(const uint8_t* __restrict__ tiles, int S, int C,
   __syncthreads();
   const float mean[3] = {m0, m1, m2};
   const float inv[3] = {1.f / s0, 1.f / s1, 1.f / s2};
-  const int kreal = C * p * p;
-  const int total = np * Kpad;
+  const int kv = Kpad >> 3;
   bf16* dst = out + ((size_t)tile * rows_per_tile + row_offset + (size_t)py * np) * Kpad;
-  for (int o = threadIdx.x; o < total; o += blockDim.x) {
-    const int px = o / Kpad;
-    const int col = o - px * Kpad;
-    float v = 0.f;
-    if (col < kreal) {
-      const int c = col / (p * p);
-      const int r = col - c * p * p;
-      const int ky = r / p, kx = r - ky * p;
-      const float u = (float)strip[((size_t)ky * S + px * p + kx) * C + c];
-      v = (u * (1.f / 255.f) - mean[c]) * inv[c];
+  for (int o = threadIdx.x; o < np * kv; o += blockDim.x) {
+    const int px = o / kv;
+    const int c8 = (o - px * kv) * 8;
+    const uint8_t* sp = strip + px * p * C;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = tab[c8 + j];
+      v[j] = 0.f;
+      if (t >= 0) {
+        const int c = t >> 28;
+        v[j] = ((float)sp[t & 0x0FFFFFFF] * (1.f / 255.f) - mean[c]) * inv[c];
+      }
     }
-    dst[o] = __float2bfloat16_rn(v);
+    *reinterpret_cast<uint4*>(dst + (size_t)o * 8) =
+        make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
   }
 }
 
@@ -308,8 +328,8 @@ int patchify_u8(const uint8_t* tiles, int n, int S, int C, int p, int Kpad, int 
                 int rows_per_tile, const float* mean, const float* stdv, bf16* out,
                 cudaStream_t stream) {
   if (n <= 0) return 0;
-  if (S % p || C > 3 || Kpad < C * p * p) return 1002;
-  const size_t smem = (size_t)p * S * C;
+  if (S % p || C > 3 || Kpad < C * p * p || Kpad % 8) return 1002;
+  const size_t smem = (((size_t)p * S * C + 15) & ~size_t(15)) + (size_t)Kpad * 4;
   dim3 grid(S / p, n);
   return launch_kernel(patchify_kernel, grid, dim3(256), smem, stream, 1, tiles, S, C, p, Kpad, row_offset,
                        rows_per_tile, mean[0], C > 1 ? mean[1] : 0.f, C > 2 ? mean[2] : 0.f, stdv[0],

@@ -570,17 +570,26 @@ int Encoder::encode(const uint8_t* tiles, int n, bf16* out, cudaStream_t s, std:
     if (_rc) return _rc;      \
   } while (0)
 
-// One CUDA graph per chunk size: the ~200 launches of a forward pass replay with a
-// single cudaGraphLaunch. The graph reads/writes the encoder-owned staging buffers
-// (in_buf / out_buf), so caller buffers only cost two device copies.
+// One CUDA graph per (chunk size, input, output): the ~200 launches of a forward pass replay
+// with a single cudaGraphLaunch that reads the caller's tiles and writes the caller's token
+// buffer in place (the stage's double-buffered rings keep the set of pointers small). Past
+// kMaxGraphs the graphs for new pointer pairs run on the encoder-owned staging buffers
+// (in_buf / out_buf) at the cost of two device copies.
 int Encoder::forward_graph(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s) {
+  constexpr size_t kMaxGraphs = 24;
   const size_t in_bytes = (size_t)nt * d.image_size * d.image_size * d.channels;
   const size_t out_bytes = (size_t)nt * Q * E * 2;
-  auto it = graphs.find(nt);
+  GraphKey key{nt, tiles, out};
+  auto it = graphs.find(key);
+  const bool staged = it == graphs.end() && graphs.size() >= kMaxGraphs;
+  if (staged) {
+    key = GraphKey{nt, in_buf, out_buf};
+    it = graphs.find(key);
+  }
   if (it == graphs.end()) {
     if (!cap_stream) EPD_TRY((int)cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
     EPD_TRY((int)cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
-    int rc = forward_chunk(in_buf, nt, out_buf, cap_stream);
+    int rc = forward_chunk(std::get<1>(key), nt, std::get<2>(key), cap_stream);
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(cap_stream, &g);
     if (rc) {
@@ -592,11 +601,11 @@ int Encoder::forward_graph(const uint8_t* tiles, int nt, bf16* out, cudaStream_t
     e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return (int)e;
-    it = graphs.emplace(nt, ex).first;
+    it = graphs.emplace(key, ex).first;
   }
-  if (tiles != in_buf) EPD_TRY((int)cudaMemcpyAsync(in_buf, tiles, in_bytes, cudaMemcpyDeviceToDevice, s));
+  if (staged) EPD_TRY((int)cudaMemcpyAsync(in_buf, tiles, in_bytes, cudaMemcpyDeviceToDevice, s));
   EPD_TRY((int)cudaGraphLaunch(it->second, s));
-  if (out != out_buf) EPD_TRY((int)cudaMemcpyAsync(out, out_buf, out_bytes, cudaMemcpyDeviceToDevice, s));
+  if (staged) EPD_TRY((int)cudaMemcpyAsync(out, out_buf, out_bytes, cudaMemcpyDeviceToDevice, s));
   return 0;
 }
 

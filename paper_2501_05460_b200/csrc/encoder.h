@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -101,7 +102,8 @@ class Encoder {
   int forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
   int forward_graph(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s);
   int forward_f32(const uint8_t* tiles, int nt, float* out, cudaStream_t s);
-  std::map<int, cudaGraphExec_t> graphs;
+  using GraphKey = std::tuple<int, const uint8_t*, bf16*>;  // chunk size, input, output
+  std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaStream_t cap_stream = nullptr;
   uint8_t* in_buf = nullptr;
   bf16* out_buf = nullptr;
