@@ -129,14 +129,17 @@ def layernorm_f32(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, eps:
 
 
 def patchify(tiles: torch.Tensor, patch: int, kpad: int, mean, std, row_offset: int = 0,
-             rows_per_tile: int | None = None) -> torch.Tensor:
+             rows_per_tile: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
     """uint8 [n,S,S,C] -> bf16 [n*rows_per_tile, kpad] normalised im2col rows."""
     _need_cuda(tiles)
     import ctypes
     n, S, _, Cc = tiles.shape
     npatch = (S // patch) ** 2
     rpt = rows_per_tile or npatch + row_offset
-    out = torch.zeros(n * rpt, kpad, dtype=torch.bfloat16, device=tiles.device)
+    if out is None:
+        out = torch.zeros(n * rpt, kpad, dtype=torch.bfloat16, device=tiles.device)
+    if out.shape != (n * rpt, kpad) or out.dtype != torch.bfloat16 or not out.is_contiguous():
+        raise ValueError(f"out must be contiguous bf16 [{n * rpt}, {kpad}]")
     m = (ctypes.c_float * 3)(*mean)
     s = (ctypes.c_float * 3)(*std)
     call("epd_patchify_u8", tiles.data_ptr(), n, S, Cc, patch, kpad, row_offset, rpt,
