@@ -1,6 +1,6 @@
 """Measured B200 encode latency per worker (seconds for p tiles, one GPU), both encoders,
 through VisionEncoder.encode_latency (the reference's costs.encode_latency signature).
-Writes argv[1] (default profiles/r01/encode_latency_b200.json); tools/calibrate_reference.py fits the
+Writes argv[1] (default profiles/r02/encode_latency_b200.json); tools/calibrate_reference.py fits the
 reference's CostParams from it."""
 import json
 import sys
@@ -23,6 +23,6 @@ for ref_name, cfg in [("minicpm-v-2.6", SIGLIP_MINICPM), ("internvl2-8b", INTERN
     out["models"][ref_name] = {"encoder": cfg.name, "samples": samples}
     enc.close()
     print(ref_name, [(p, round(s * 1e3, 3)) for p, s in samples])
-path = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "profiles" / "r01" / "encode_latency_b200.json"
+path = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "profiles" / "r02" / "encode_latency_b200.json"
 path.write_text(json.dumps(out, indent=1))
 print(path)
