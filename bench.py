@@ -62,6 +62,11 @@ def workload(name: str):
         return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b", image=(4032, 3024),
                     desc="C2 from pixels: one 4032x3024 photo per request, MiniCPM-V slicing on the GPU -> "
                          "10 tiles (448x448) -> SigLIP-400M + resampler")
+    if name == "c2s":
+        return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b", serve=(8, 4),
+                    desc="C2 served: bursts of 8 MiniCPM-V requests (10 tiles each) through EPDRuntime, encode "
+                         "batches of up to 4 requests (form_batch + E/P-side MM reservations), shards stored into "
+                         "the prefill instance's paged MM blocks, Qwen2-7B prefill to the first token")
     if name == "c4":
         return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True, llm="qwen2-7b",
                     desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
@@ -264,7 +269,78 @@ def main():
     if args.impl == "reference":
         reference_arm(args, wl, world, rank)
         return
+    if wl.get("serve"):
+        run_serve(args, wl, world, rank, local)
+        return
     run_ours(args, wl, world, rank, local)
+
+
+def run_serve(args, wl, world, rank, local):
+    """One step = one burst of requests served to their first tokens by runtime.EPDRuntime
+    (value = tiles of the burst / burst time, max over ranks; TTFT per request from the
+    measured RequestRecords, first_token_time - arrival, p50 by the reference's rule)."""
+    import torch.distributed as dist
+
+    from paper_2501_05460_b200.encoder import VisionEncoder, canonical_weights
+    from paper_2501_05460_b200.prefill import QWEN2_7B, Prefiller
+    from paper_2501_05460_b200.runtime import EPDRuntime, ServeRequest, check_causality
+    from paper_2501_05460_b200.stage import EncodeStage, tiles_for_request
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg, n = wl["cfg"], wl["tiles"]
+    n_req, max_batch = wl["serve"]
+    enc = VisionEncoder(cfg, dev, max_tiles=n * max_batch, weights=canonical_weights(cfg))
+    stage = EncodeStage(enc, dev, rank=rank, world=world)
+    T_pre = n * cfg.out_tokens + PROMPT_TOKENS
+    pf = Prefiller(QWEN2_7B, dev, max_tokens=T_pre) if rank == 0 else None
+    rt = EPDRuntime(stage, pf, max_batch=max_batch)
+    reqs = []
+    for i in range(n_req):
+        prompt = torch.randint(0, QWEN2_7B.vocab, (PROMPT_TOKENS,), dtype=torch.int32,
+                               generator=torch.Generator().manual_seed(100 + i)).to(dev)
+        reqs.append(ServeRequest(i, tiles_for_request(n, cfg, seed=20260808 + i).pin_memory(), prompt))
+    for _ in range(args.warmup):
+        rt.serve(reqs)
+    torch.cuda.synchronize()
+    ttft, walls = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = rt.serve(reqs)
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b)
+            if world > 1:
+                t = torch.tensor([ms], dtype=torch.float64, device=dev)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            walls.append(ms)
+            if rank == 0:
+                for rec in out["records"].values():
+                    check_causality(rec)
+                    ttft.append((rec.first_token_time - rec.arrival) * 1e3)
+    rt.close()
+    if rank != 0:
+        return
+    total_ms = sum(walls)
+    value = n_req * n * args.steps / (total_ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": bench_config(wl, world) | {"requests_per_burst": n_req, "max_batch": max_batch},
+            "p50_ttft_ms": _percentile(ttft, 0.5), "ttft_p90_ms": _percentile(ttft, 0.9), "ttft_n": len(ttft),
+            "ttft_note": "per request of a burst: first_token_time - arrival from the measured RequestRecords "
+                         "(%globaltimer), all requests arriving at the burst start; includes queueing behind "
+                         "earlier batches and prefills",
+            "ep_wait_per_burst": len(out["ep_wait"]), "clocks": clk.summary(),
+            "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": value, "unit": "tiles/s", "h2d_bytes_per_step": n_req * n * cfg.tile_bytes,
+                    "d2h_bytes_per_step": 4 * n_req}}
+    print(json.dumps(line), flush=True)
 
 
 def run_ours(args, wl, world, rank, local):
