@@ -40,45 +40,66 @@ EPD_DEVICE void load8(const bf16* src, float* x) {
 
 // Both GELU epilogues are relative-accurate on the negative tail, where 0.5 x (1 + t)
 // with a hardware tanh (abs error ~5e-4) cancels: at x = -3 that form is off by several
-// bf16 ulps. One MUFU op per element either way.
-//
+// bf16 ulps. One MUFU op per element either way; the FMA-pipe arithmetic runs on packed
+// pairs (FFMA2 / FMUL2 / FADD2), two elements per instruction.
+EPD_DEVICE float2 f2fma(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\nmov.b64 rc, {%6,%7};\n"
+      "fma.rn.f32x2 rd, ra, rb, rc;\nmov.b64 {%0,%1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+EPD_DEVICE float2 f2mul(float2 a, float2 b) {
+  float2 d;
+  asm("{\n.reg .b64 ra, rb, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\n"
+      "mul.rn.f32x2 rd, ra, rb;\nmov.b64 {%0,%1}, rd;\n}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+EPD_DEVICE float2 f2s(float v) { return make_float2(v, v); }
+EPD_DEVICE float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // GELU-tanh, 0.5 x (1 + tanh u) with u = k0 (x + k1 x^3), written as x * sigma(2u):
 // e = 2^(-2 u(|x|) log2 e) on the MUFU, r = 1 / (1 + e) by Newton on the FMA pipe
 // (1 + e lies in [1, 2]: linear minimax start, 3 steps -> fp32-exact), then
 // phi = r for x >= 0 and e r for x < 0.
-EPD_DEVICE float gelu_tanh_fast(float x) {
-  const float z = fabsf(x);
-  const float z2 = z * z;
+EPD_DEVICE float2 gelu_tanh_fast2(float2 x) {
+  const float2 z = make_float2(fabsf(x.x), fabsf(x.y));
   // -2 log2(e) k0 = -2.3022082, k1 = 0.044715
-  const float a = z * fmaf(0.044715f, z2, 1.f) * -2.302208198f;
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(a));
-  const float y = 1.f + e;
-  float r = fmaf(-0.470588235f, y, 1.411764706f);  // 24/17 - 8/17 y
-  r = fmaf(r, fmaf(-y, r, 1.f), r);
-  r = fmaf(r, fmaf(-y, r, 1.f), r);
-  r = fmaf(r, fmaf(-y, r, 1.f), r);
-  return x * (x >= 0.f ? r : e * r);
+  const float2 a = f2mul(f2mul(z, f2fma(f2s(0.044715f), f2mul(z, z), f2s(1.f))), f2s(-2.302208198f));
+  const float2 e = make_float2(ex2f(a.x), ex2f(a.y));
+  const float2 y = f2fma(e, f2s(1.f), f2s(1.f));
+  float2 r = f2fma(f2s(-0.470588235f), y, f2s(1.411764706f));  // 24/17 - 8/17 y
+  const float2 ny = make_float2(-y.x, -y.y);
+#pragma unroll
+  for (int it = 0; it < 3; ++it) r = f2fma(r, f2fma(ny, r, f2s(1.f)), r);
+  const float2 er = f2mul(e, r);
+  return f2mul(x, make_float2(x.x >= 0.f ? r.x : er.x, x.y >= 0.f ? r.y : er.y));
 }
 
 // GELU-erf, x Phi(x): Phi(-z) = 2^-F(z) for z = min(|x|, 8), F a degree-8 polynomial in
 // v = z/4 - 1 (tools/fit_gelu.py: max rel err 8.5e-6 against x Phi(x) on [-8, 8]; 0.025 %
 // of bf16 outputs round differently from the exact erf form, fp32 noise). Beyond |x| = 8
-// the result is x (x > 0) or below 1e-14 in magnitude.
-EPD_DEVICE float gelu_erf_fast(float x) {
-  const float v = fmaf(fminf(fabsf(x), 8.f), 0.25f, -1.f);
-  float f = -5.421509966e-03f;
-  f = fmaf(f, v, 2.080199681e-02f);
-  f = fmaf(f, v, -4.194424301e-02f);
-  f = fmaf(f, v, 7.617540658e-02f);
-  f = fmaf(f, v, -1.449510306e-01f);
-  f = fmaf(f, v, 2.748279572e-01f);
-  f = fmaf(f, v, 1.100269699e+01f);
-  f = fmaf(f, v, 2.438505554e+01f);
-  f = fmaf(f, v, 1.494647121e+01f);
-  float q;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(q) : "f"(-f));
-  return x * (x >= 0.f ? 1.f - q : q);
+// the result is x (x > 0) or below 1e-14 in magnitude. The polynomial carries -F.
+EPD_DEVICE float2 gelu_erf_fast2(float2 x) {
+  const float2 v = f2fma(make_float2(fminf(fabsf(x.x), 8.f), fminf(fabsf(x.y), 8.f)), f2s(0.25f), f2s(-1.f));
+  float2 f = f2s(5.421509966e-03f);
+  f = f2fma(f, v, f2s(-2.080199681e-02f));
+  f = f2fma(f, v, f2s(4.194424301e-02f));
+  f = f2fma(f, v, f2s(-7.617540658e-02f));
+  f = f2fma(f, v, f2s(1.449510306e-01f));
+  f = f2fma(f, v, f2s(-2.748279572e-01f));
+  f = f2fma(f, v, f2s(-1.100269699e+01f));
+  f = f2fma(f, v, f2s(-2.438505554e+01f));
+  f = f2fma(f, v, f2s(-1.494647121e+01f));
+  const float2 q = make_float2(ex2f(f.x), ex2f(f.y));
+  return f2mul(x, make_float2(x.x >= 0.f ? 1.f - q.x : q.x, x.y >= 0.f ? 1.f - q.y : q.y));
 }
 
 // Epilogue kinds (the output side of C = A B^T):
@@ -479,10 +500,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
             }
             if (ep.act == ACT_GELU_TANH) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) xg[j] = gelu_tanh_fast(xg[j]);
+              for (int j = 0; j < 8; j += 2) {
+                const float2 gv = gelu_tanh_fast2(make_float2(xg[j], xg[j + 1]));
+                xg[j] = gv.x;
+                xg[j + 1] = gv.y;
+              }
             } else if (ep.act == ACT_GELU_ERF) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) xg[j] = gelu_erf_fast(xg[j]);
+              for (int j = 0; j < 8; j += 2) {
+                const float2 gv = gelu_erf_fast2(make_float2(xg[j], xg[j + 1]));
+                xg[j] = gv.x;
+                xg[j + 1] = gv.y;
+              }
             }
             if (ep.lscale) {
               float s8[8];

@@ -20,9 +20,14 @@ This is the reference engine's encode branch with real work in place of modeled 
 * ``_on_batch_end`` (engine.py:385-407): prefill reads its MM tokens from those blocks
   (paged prefill), the first token ends it, and the P-side blocks are freed.
 
+* ``assign_instance`` / ``_arrival_load`` (engine.py:65-78, 277-286): with several encode
+  instances (the ranks split into equal groups, each one IRP instance), every arriving
+  request goes to the instance the reference's policy picks -- round robin, or least
+  loaded by outstanding tiles (queued + in flight), ties to the lowest id.
+
 Ranks run in lockstep: rank 0 is the prefill instance and the coordinator (it owns the
 queues and BlockManagers and broadcasts each round's commands); every rank is one IRP
-encode worker. Times come from the GPUs' %globaltimer (``epd_timestamp``) and fill
+encode worker of one encode instance. Times come from the GPUs' %globaltimer (``epd_timestamp``) and fill
 ``ShardRecord`` / ``RequestRecord`` (trace.py:18-53); :func:`check_causality` restates
 ``SimTrace._check_causality`` (trace.py:119-148) for the stages this path runs (decode is
 out of scope, so token times are not checked).
@@ -40,7 +45,7 @@ import torch.distributed as dist
 
 from ._lib import call
 from .blockpool import BlockManager, CacheKind
-from .routing import form_batch, plan_batch, shard_ranges
+from .routing import assign_instance, form_batch, plan_batch, shard_ranges
 
 
 @dataclass
@@ -258,7 +263,7 @@ class EPDRuntime:
     """Lockstep encode -> prefill runtime over the ranks of an :class:`~.stage.EncodeStage`."""
 
     def __init__(self, stage, prefiller, max_batch: int = 4, e_mm_tokens: int = 48_000, p_mm_tokens: int = 48_000,
-                 block_size: int = 16, group=None):
+                 block_size: int = 16, group=None, instances: int = 1, policy: str = "round_robin"):
         self.stage, self.pf = stage, prefiller
         self.cfg = stage.cfg
         self.rank, self.world, self.device = stage.rank, stage.world, stage.device
@@ -272,8 +277,15 @@ class EPDRuntime:
         self.is_coord = self.rank == 0
         if self.is_coord and prefiller is None:
             raise ValueError("the prefill rank needs a Prefiller")
-        # E-side MM blocks: the encode instance's reservation for each request's full mm_tokens
-        self.e_mm = BlockManager(CacheKind.MM, block_size, -(-e_mm_tokens // block_size)) if self.is_coord else None
+        if instances < 1 or self.world % instances:
+            raise ValueError(f"{self.world} ranks do not split into {instances} equal encode instances")
+        self.instances, self.policy = instances, policy
+        self.width = self.world // instances            # IRP width of every encode instance
+        self.inst, self.local = divmod(self.rank, self.width)
+        # E-side MM blocks: each encode instance's reservation for a request's full mm_tokens
+        self.e_mms = ([BlockManager(CacheKind.MM, block_size, -(-e_mm_tokens // block_size)) for _ in range(instances)]
+                      if self.is_coord else None)
+        self.e_mm = self.e_mms[0] if self.is_coord else None
         self.p = MMPool(self.device, self.rank, self.world, -(-p_mm_tokens // block_size), block_size,
                         self.cfg.out_dim, group)
         self.stamps = _Stamps(self.device)
@@ -313,15 +325,23 @@ class EPDRuntime:
         held: dict[int, torch.Tensor] = {}      # rid -> this rank's encoded shard, not yet sent
         marks: dict = {}                         # ("start"|"end"|"xfer"|"ep"|"pre0"|"pre1", rid[, k]) -> slot
         if self.is_coord:
-            geo = self.cfg.geometry
-            queue = deque(r.rid for r in requests)
+            # assign_instance on arrival (engine.py:270-283), load = outstanding tiles (_arrival_load)
+            queues = [deque() for _ in range(self.instances)]
+            load = [0] * self.instances
+            inst_of: dict[int, int] = {}
+            rr = 0
+            for r in requests:
+                iid, rr = assign_instance(self.policy, [(i, float(load[i])) for i in range(self.instances)], rr)
+                inst_of[r.rid] = iid
+                queues[iid].append(r.rid)
+                load[iid] += r.tiles.shape[0]
             ep_wait: deque = deque()
             ready: deque = deque()
             recs: dict[int, RequestRecord] = {}
             for r in requests:
                 mm = r.tiles.shape[0] * T
                 recs[r.rid] = RequestRecord(r.rid, 0.0, int(r.prompt.numel()), mm, mm + int(r.prompt.numel()),
-                                            r.output_tokens)
+                                            r.output_tokens, e_instance=inst_of[r.rid])
             p_blocks: dict[int, list[int]] = {}
             waited = []
         first_tok, kept = {}, {}
@@ -339,20 +359,25 @@ class EPDRuntime:
                     p_blocks[rid] = self.p.manager.allocate(rid, recs[rid].mm_tokens)
                     pre.append((rid, p_blocks[rid]))
 
-                def fits(rid):
-                    mm = recs[rid].mm_tokens
-                    if not self.e_mm.can_allocate(mm):
-                        return False
-                    self.e_mm.allocate(rid, mm)
-                    return True
-                batch = form_batch(list(queue), self.max_batch, fits)
-                for _ in batch:
-                    queue.popleft()
-                done = not (queue or ep_wait or batch or pre)
+                batch = []
+                for iid, queue in enumerate(queues):  # every idle encode instance starts a batch
+                    e_mm = self.e_mms[iid]
+
+                    def fits(rid, e_mm=e_mm):
+                        mm = recs[rid].mm_tokens
+                        if not e_mm.can_allocate(mm):
+                            return False
+                        e_mm.allocate(rid, mm)
+                        return True
+                    b = form_batch(list(queue), self.max_batch, fits)
+                    for _ in b:
+                        queue.popleft()
+                    batch += [(rid, reqs[rid].tiles.shape[0], iid) for rid in b]
+                done = not (any(queues) or ep_wait or batch or pre)
                 if not done and not batch and not pre:
                     # nothing in flight and nothing can start: a request larger than an MM pool
                     raise RuntimeError("the MM blocks cannot hold the head request (mm_capacity)")
-                cmd = {"pre": pre, "batch": [(rid, reqs[rid].tiles.shape[0]) for rid in batch], "done": done}
+                cmd = {"pre": [(rid, blocks, inst_of[rid]) for rid, blocks in pre], "batch": batch, "done": done}
             cmd = self._bcast(cmd)
             if cmd["done"]:
                 break
@@ -362,10 +387,10 @@ class EPDRuntime:
             post = None
             if self.is_coord:
                 post = []
-                for rid, _ in cmd["batch"]:
+                for rid, _, iid in cmd["batch"]:
                     if self.p.manager.can_allocate(recs[rid].mm_tokens):
                         p_blocks[rid] = self.p.manager.allocate(rid, recs[rid].mm_tokens)
-                        post.append((rid, p_blocks[rid]))
+                        post.append((rid, p_blocks[rid], iid))
                     else:
                         ep_wait.append(rid)
                         recs[rid].ep_waited = True
@@ -374,8 +399,8 @@ class EPDRuntime:
             self._send(post, held, marks, s)
             # ---- coordinator: every landed request -> prefill, first token, free P-side blocks
             if self.is_coord:
-                for rid, _ in cmd["pre"] + post:
-                    self.e_mm.free(rid)            # _on_transfer_end("ep"): all shards landed
+                for rid, _, iid in cmd["pre"] + post:
+                    self.e_mms[iid].free(rid)      # _on_transfer_end("ep"): all shards landed
                     ready.append(rid)
                 while ready:
                     rid = ready.popleft()
@@ -409,13 +434,14 @@ class EPDRuntime:
         for rid, rec in recs.items():
             rec.arrival = 0.0  # the burst arrives at the calibration stamp
             n = reqs[rid].tiles.shape[0]
+            base_rank = rec.e_instance * self.width
             shards = []
-            for k, (first, count) in enumerate(shard_ranges(n, self.world)):
+            for k, (first, count) in enumerate(shard_ranges(n, self.width)):
                 if count == 0:
                     continue
-                m = allmarks[k]
+                m = allmarks[base_rank + k]
                 shards.append(ShardRecord(k, count, sec(m[("start", rid)]), sec(m[("end", rid)]),
-                                          sec(st[marks[("xfer", rid, k)]])))
+                                          sec(st[marks[("xfer", rid, base_rank + k)]])))
             rec.shards = shards
             rec.encode_start = min(x.start for x in shards)
             rec.encode_end = max(x.end for x in shards)
@@ -425,7 +451,7 @@ class EPDRuntime:
             rec.first_token = int(first_tok[rid].item())
         self.stamps.n = 0
         return {"records": recs, "ep_wait": waited, "wall_s": wall, "mm": kept,
-                "plans": plan_batch([reqs[r].tiles.shape[0] for r in reqs], self.world)[0]}
+                "plans": plan_batch([reqs[r].tiles.shape[0] for r in reqs], self.width)[0]}
 
     # ---------------------------------------------------------------- per-rank work
     def _encode(self, batch, held, marks, s) -> None:
@@ -434,8 +460,10 @@ class EPDRuntime:
         if not batch:
             return
         parts = []
-        for rid, n in batch:
-            first, count = shard_ranges(n, self.world)[self.rank]
+        for rid, n, iid in batch:
+            if iid != self.inst:
+                continue
+            first, count = shard_ranges(n, self.width)[self.local]
             if count:
                 parts.append((rid, first, count))
         if not parts:
@@ -469,12 +497,13 @@ class EPDRuntime:
             self.p.release(self.seq, s)
         items = []
         has = [False] * self.world
-        for rid, blocks in sends:
+        for rid, blocks, iid in sends:
             n = self._tiles[rid].shape[0]
-            for k, (first, count) in enumerate(shard_ranges(n, self.world)):
+            ranges = shard_ranges(n, self.width)
+            for k, (first, count) in enumerate(ranges):
                 if count:
-                    has[k] = True
-            first, count = shard_ranges(n, self.world)[self.rank]
+                    has[iid * self.width + k] = True
+            first, count = ranges[self.local] if iid == self.inst else (0, 0)
             if count:
                 ids = torch.tensor(blocks[first * self.bpt:(first + count) * self.bpt], dtype=torch.int32).to(
                     self.device, non_blocking=True)
@@ -488,10 +517,10 @@ class EPDRuntime:
                     self.p.wait(self.seq, k, s)
                     xfer[k] = self.stamps.mark(s)
             ep = self.stamps.mark(s)
-            for rid, blocks in sends:
+            for rid, blocks, iid in sends:
                 n = self._tiles[rid].shape[0]
-                for k, (first, count) in enumerate(shard_ranges(n, self.world)):
+                for k, (first, count) in enumerate(shard_ranges(n, self.width)):
                     if count:
-                        marks[("xfer", rid, k)] = xfer[k]
+                        marks[("xfer", rid, iid * self.width + k)] = xfer[iid * self.width + k]
                 marks[("ep", rid)] = ep
 

@@ -32,15 +32,10 @@ import torch.distributed as dist
 from .routing import ep_bytes, shard_ranges
 
 
-@dataclass
-class ShardRecord:
-    """trace.ShardRecord (trace.py:18-24) with measured device times (seconds)."""
-
-    worker: int
-    patches: int
-    start: float | None = None
-    end: float | None = None
-    transfer_end: float | None = None
+# trace.ShardRecord (trace.py:18-24). The single-request path records worker and tiles; the
+# serving runtime (runtime.EPDRuntime) also fills start / end / transfer_end from the GPUs'
+# %globaltimer.
+from .runtime import ShardRecord  # noqa: E402
 
 
 @dataclass

@@ -23,7 +23,7 @@ def _port():
 
 
 @pytest.mark.parametrize("world,scenario", [(1, "plain"), (1, "pwait"), (1, "ewait"), (2, "plain"),
-                                            (3, "pwait")])
+                                            (3, "pwait"), (2, "inst_rr"), (3, "inst_ll")])
 def test_runtime(cuda, world, scenario):
     script = str(ROOT / "tools" / "runtime_check.py")
     if world == 1:

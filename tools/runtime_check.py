@@ -7,7 +7,9 @@ Scenarios (every rank passes the same requests; rank 0 checks):
              block is returned and the measured records satisfy the reference's causality rules;
   pwait   -- a prefill-side pool of 6 tiles: requests that do not fit wait in ep_wait (FIFO)
              while encoding continues; outputs stay exact;
-  ewait   -- an encode-side pool of 6 tiles: batches stop at the first misfit (form_batch).
+  ewait   -- an encode-side pool of 6 tiles: batches stop at the first misfit (form_batch);
+  inst_rr / inst_ll -- every rank its own encode instance (IRP width 1): requests assigned
+             round robin / least loaded by outstanding tiles (assign_instance, engine.py:65-78).
 
 usage: python tools/runtime_check.py [scenario]            (world 1)
        torchrun --nproc-per-node 2 --master-addr 127.0.0.1 --master-port P tools/runtime_check.py [scenario]
@@ -50,7 +52,9 @@ def main() -> None:
     lcfg = LLMConfig("test-llm", 2, QWEN2_7B.hidden, 28, 4, 128, 1024, 1000, 1e6, 1e-6, True)
     pf = Prefiller(lcfg, dev, max_tokens=max(TILES) * cfg.out_tokens + 16) if rank == 0 else None
     T = cfg.out_tokens
-    kw = {"plain": {}, "pwait": {"p_mm_tokens": 6 * T}, "ewait": {"e_mm_tokens": 6 * T}}[scenario]
+    kw = {"plain": {}, "pwait": {"p_mm_tokens": 6 * T}, "ewait": {"e_mm_tokens": 6 * T},
+          "inst_rr": {"instances": world, "policy": "round_robin"},
+          "inst_ll": {"instances": world, "policy": "least_loaded"}}[scenario]
     rt = EPDRuntime(stage, pf, max_batch=3, **kw)
     rt.keep_mm = True
     reqs = []
@@ -72,15 +76,26 @@ def main() -> None:
                     errs.append(f"request {r.rid}: MM tokens in the P-side blocks differ from a direct encode")
                 if rec.first_token != int(tok.item()):
                     errs.append(f"request {r.rid}: first token {rec.first_token} vs direct {int(tok.item())}")
-                want = [(k, c) for k, (_, c) in enumerate(shard_ranges(r.tiles.shape[0], world)) if c]
+                want = [(k, c) for k, (_, c) in enumerate(shard_ranges(r.tiles.shape[0], rt.width)) if c]
                 if [(s.worker, s.patches) for s in rec.shards] != want:
                     errs.append(f"request {r.rid}: shards {rec.shards} vs {want}")
                 try:
                     check_causality(rec)
                 except ValueError as e:
                     errs.append(str(e))
-        if rt.p.manager.used_blocks or rt.e_mm.used_blocks:
+        if rt.p.manager.used_blocks or any(m.used_blocks for m in rt.e_mms):
             errs.append("MM blocks leaked")
+        if scenario.startswith("inst"):
+            from paper_2501_05460_b200.routing import assign_instance
+            load, rr, want_inst = [0] * world, 0, []
+            for r in reqs:
+                iid, rr = assign_instance(kw["policy"], [(i, float(load[i])) for i in range(world)], rr)
+                want_inst.append(iid)
+                load[iid] += r.tiles.shape[0]
+            got_inst = [out["records"][r.rid].e_instance for r in reqs]
+            print(f"instances: {got_inst}", flush=True)
+            if got_inst != want_inst or len(set(got_inst)) != world:
+                errs.append(f"{scenario}: instances {got_inst}, expected {want_inst}")
         waited = out["ep_wait"]
         if scenario == "pwait":
             # P pool of 6 tiles, batches of 3 (tiles 3 1 4 | 2 5 1 | 2): r2 waits (3+1+4 > 6);
