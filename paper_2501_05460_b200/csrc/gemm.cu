@@ -453,6 +453,20 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         // a tile that straddles two images (T % 128 != 0) cannot be one TMA box
         straddle = tok0 + kBM > ep.T;
       }
+      // Per-column epilogue vectors (bias, layer scale) of the next 32-column chunk are loaded
+      // one chunk ahead, so their global-load latency overlaps the accumulator wait and the
+      // current chunk's arithmetic instead of stalling it.
+      uint4 bias_nx[4], ls_nx[4];
+      auto prefetch_vec = [&](int n) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const int col = n + g * 8;
+          const bool ok = KIND != EK_SWIGLU && col < N;
+          bias_nx[g] = ok && ep.bias ? *reinterpret_cast<const uint4*>(ep.bias + col) : make_uint4(0, 0, 0, 0);
+          ls_nx[g] = ok && ep.lscale ? *reinterpret_cast<const uint4*>(ep.lscale + col) : make_uint4(0, 0, 0, 0);
+        }
+      };
+      prefetch_vec(n0 + half * hw);
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #pragma unroll 1
@@ -460,6 +474,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
            c += (KIND == EK_SWIGLU ? 64 : 32)) {
         const int n = n0 + c;
         if (n >= N) break;  // warp-uniform
+        uint4 bias_cur[4], ls_cur[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          bias_cur[g] = bias_nx[g];
+          ls_cur[g] = ls_nx[g];
+        }
+        if (KIND != EK_SWIGLU && c + 32 < (half + 1) * hw) prefetch_vec(n + 32);
         float x[32];
         {
           uint32_t v[32];
@@ -493,10 +514,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           float* xg = x + g * 8;
           if (col < N) {
             if (ep.bias) {
-              float bb[8];
-              load8(ep.bias + col, bb);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) xg[j] += bb[j];
+              const uint4 bv = bias_cur[g];
+              const float2 b0 = unpack_bf16x2(bv.x), b1 = unpack_bf16x2(bv.y), b2 = unpack_bf16x2(bv.z),
+                           b3 = unpack_bf16x2(bv.w);
+              xg[0] += b0.x; xg[1] += b0.y; xg[2] += b1.x; xg[3] += b1.y;
+              xg[4] += b2.x; xg[5] += b2.y; xg[6] += b3.x; xg[7] += b3.y;
             }
             if (ep.act == ACT_GELU_TANH) {
 #pragma unroll
@@ -514,10 +536,11 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
               }
             }
             if (ep.lscale) {
-              float s8[8];
-              load8(ep.lscale + col, s8);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) xg[j] *= s8[j];
+              const uint4 sv = ls_cur[g];
+              const float2 s0 = unpack_bf16x2(sv.x), s1 = unpack_bf16x2(sv.y), s2 = unpack_bf16x2(sv.z),
+                           s3 = unpack_bf16x2(sv.w);
+              xg[0] *= s0.x; xg[1] *= s0.y; xg[2] *= s1.x; xg[3] *= s1.y;
+              xg[4] *= s2.x; xg[5] *= s2.y; xg[6] *= s3.x; xg[7] *= s3.y;
             }
             if (KIND != EK_ACC_F32 && ep.resid && row < M) {  // generic (direct-load) residual
               float rr[8];
