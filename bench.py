@@ -209,7 +209,9 @@ def init_dist(gpus: int):
 def bench_config(wl, world: int) -> dict:
     """The workload description both arms print (identical for --impl ours / reference)."""
     cfg = wl["cfg"]
+    reqs = world if (world > 1 and not wl["cache"] and not wl.get("image") and not wl.get("serve")) else 1
     return {"workload": wl["desc"], "encoder": cfg.name, "tiles_per_request": wl["tiles"],
+            "requests_per_step": reqs,
             "irp_width": world, "prefill_rank": 0, "parallelism": f"irp{world}",
             "l2": "working set > L2 (0.97 GB bf16 weights + ~0.5 GB activations streamed per step)",
             "weights": "random-init N(0,0.02), seed 20260808"}
@@ -240,7 +242,8 @@ def reference_arm(args, wl, world, rank):
     v = args.steps * per_step / dt
     line = {"metric": METRIC, "value": v, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if (wl["cache"] or wl.get("image")) else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
             "impl": "reference", "config": bench_config(wl, world), "sample_tiles_per_step": per_step,
             "cpu_baseline": {"value": v, "unit": "tiles/s", "cores": torch.get_num_threads(), "kind": "port",
                              "sample": f"{per_step} tile of the {wl['tiles']}-tile request per step (bounded "
@@ -356,7 +359,15 @@ def run_ours(args, wl, world, rank, local):
     cfg = wl["cfg"]
     n = wl["tiles"]
     weights = canonical_weights(cfg)
-    max_tiles = 32 if n > 32 else max(1, n)
+    # One request per GPU per step (weak scaling): at N > 1 the step is a batch of N requests,
+    # each IRP-sharded over all N ranks restarting at worker 0 (engine.py:583-602); every rank
+    # encodes all of its shards of the batch in one call (EncodeStage.process_batch). At N = 1
+    # this is the single request of round 1. Cached and photo workloads stay one request.
+    from paper_2501_05460_b200.routing import shard_ranges as _sr
+    batched = world > 1 and not wl["cache"] and not wl.get("image")
+    reqs = world if batched else 1
+    per_rank = max(sum(_sr(n, world)[k][1] for _ in range(reqs)) for k in range(world)) if batched else n
+    max_tiles = 32 if per_rank > 32 else max(1, per_rank)
     enc = VisionEncoder(cfg, dev, max_tiles=max_tiles, weights=weights)
     cache = None
     if wl["cache"] and rank == 0:
@@ -368,7 +379,7 @@ def run_ours(args, wl, world, rank, local):
     stage = EncodeStage(enc, dev, rank=rank, world=world, prefill_rank=0, cache=cache, cached=wl["cache"],
                         comm=comm)
     if world > 1 and os.environ.get("EPD_GATHER", "peer") != "nccl":
-        stage.enable_peer_gather(max(n, 16))  # shards stored into the prefill GPU over NVLink
+        stage.enable_peer_gather(max(n * reqs, 16))  # shards stored into the prefill GPU over NVLink
 
     rot = wl.get("rotate")
     if rot:
@@ -396,7 +407,10 @@ def run_ours(args, wl, world, rank, local):
         g = torch.Generator().manual_seed(20260808)
         image_host = torch.randint(0, 256, (ih, iw, cfg.channels), dtype=torch.uint8, generator=g).pin_memory()
     tiles_dev = tiles_host.to(dev)
-    out_host = torch.empty(n, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16).pin_memory()
+    out_host = torch.empty(n * reqs, cfg.out_tokens, cfg.out_dim, dtype=torch.bfloat16).pin_memory()
+    if batched:
+        batch_host = [tiles_host] + [tiles_for_request(n, cfg, seed=20260808 + r).pin_memory() for r in range(1, reqs)]
+        batch_dev = [t.to(dev) for t in batch_host]
 
     def barrier():
         if world > 1:
@@ -412,6 +426,8 @@ def run_ours(args, wl, world, rank, local):
         reset_cache()
         if rot:
             return stage.process(None, tiles_dev=pool_dev[window()])
+        if batched:
+            return stage.process_batch(tiles_dev=batch_dev)
         return stage.process(None, tiles_dev=tiles_dev)
 
     def step_e2e():
@@ -422,6 +438,8 @@ def run_ours(args, wl, world, rank, local):
             return stage.process_image(image_host, cfg.geometry.name, out_host=out_host if rank == 0 else None)
         if rot:
             return stage.process(tiles_pool[window()], out_host=out_host if rank == 0 else None)
+        if batched:
+            return stage.process_batch(tiles_host=batch_host, out_host=out_host if rank == 0 else None)
         return stage.process(tiles_host, out_host=out_host if rank == 0 else None)
 
     def max_over_ranks(x: float) -> float:
@@ -503,7 +521,7 @@ def run_ours(args, wl, world, rank, local):
 
         def step_prefill_only():
             if pf is not None:
-                pf.prefill(last.tokens.view(-1, cfg.out_dim), prompt)
+                pf.prefill(last.tokens[:n].reshape(-1, cfg.out_dim), prompt)
 
         for _ in range(3):
             mm_last = step_ttft().tokens
@@ -542,7 +560,7 @@ def run_ours(args, wl, world, rank, local):
           if wl.get("kv_handoff") else None)
     gather = gather_bench(stage, cfg, n, world, rank, dev, args) if not wl["cache"] else None
 
-    encoded_tiles = n  # tiles that complete the request per step (cache hits count as served)
+    encoded_tiles = n * reqs  # tiles that complete the step's requests (cache hits count as served)
     value = encoded_tiles * args.steps / (total_ms / 1e3)
     e2e_value = encoded_tiles * args.steps / (e2e_ms / 1e3)
     p50_ttft = _percentile(e2e_per, 0.5)
@@ -568,7 +586,9 @@ def run_ours(args, wl, world, rank, local):
     if tj.exists():
         traffic = json.loads(tj.read_text()).get(wl["cfg"].name, {}).get("gemm_dram_bytes_per_launch")
 
-    launches_per_step = enc.launches(stage_tiles_per_rank(n, world, rank)) + (2 if cache is not None else 0)
+    my_tiles = (sum(stage_tiles_per_rank(n, world, rank) for _ in range(reqs)) if batched
+                else stage_tiles_per_rank(n, world, rank))
+    launches_per_step = enc.launches(my_tiles) + (2 if cache is not None else 0)
     if stage.transport == "nvlink-peer":
         launches_per_step += world - 1  # the prefill rank's release-flag stores (peer.py)
     model = cfg.geometry.name
@@ -582,8 +602,8 @@ def run_ours(args, wl, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "tiles/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": bench_config(wl, world), "ep_transport": stage.transport,
+        "scaling": "strong" if (wl["cache"] or wl.get("image")) else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic", "config": bench_config(wl, world), "ep_transport": stage.transport,
         "p50_ttft_ms": prefill["p50_ttft_ms"] if prefill else p50_ttft,
         "p50_ttft_ms_encode_side": p50_ttft,
         "p50_ttft_ms_resident": p50_resident,
@@ -598,7 +618,7 @@ def run_ours(args, wl, world, rank, local):
                      "costs.prefill_latency with SYNTHETIC_COSTS (presets.py:53-61) instead.",
         "e2e": {"value": e2e_value, "unit": "tiles/s",
                 "h2d_bytes_per_step": int(image_host.numel() * world if image_host is not None
-                                          else n * cfg.tile_bytes),  # summed over ranks
+                                          else n * reqs * cfg.tile_bytes),  # summed over ranks
                 "d2h_bytes_per_step": int(out_host.numel() * 2)},
         "gpu_launches": int(launches_per_step * args.steps),
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all encoder GEMM launches, profiled pass)",

@@ -177,6 +177,20 @@ class PeerGather:
         call("epd_peer_put", C.c_void_p(local.data_ptr()), C.c_void_p(self.slots_remote + off), nbytes,
              C.c_void_p(self.data_remote + 4 * self.rank), seq, raw)
 
+    def put_many(self, seq: int, pieces, stream) -> None:
+        """Encode rank: several pieces [(local view, tile offset)] of one exchange, then one
+        flag (the batched path, EncodeStage.process_batch)."""
+        s = seq % SLOTS
+        raw = C.c_void_p(stream.cuda_stream)
+        call("epd_stream_wait_geq", C.c_void_p(self.rel_local + 4 * s), seq, raw)
+        for i, (local, first) in enumerate(pieces):
+            local = local.contiguous()
+            nbytes = local.numel() * local.element_size()
+            off = s * self.slot_bytes + first * (nbytes // max(local.shape[0], 1))
+            last = i == len(pieces) - 1
+            call("epd_peer_put", C.c_void_p(local.data_ptr()), C.c_void_p(self.slots_remote + off), nbytes,
+                 C.c_void_p(self.data_remote + 4 * self.rank if last else None), seq, raw)
+
     def wait(self, seq: int, ranges, stream) -> None:
         """Prefill rank: the stream waits until every other rank with a non-empty shard has
         landed its shard of request ``seq``."""

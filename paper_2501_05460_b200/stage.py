@@ -289,6 +289,111 @@ class EncodeStage:
         r["free"][k] = ev  # the tiles slot is reusable once this request's encode is queued
         return res
 
+    def process_batch(self, tiles_host: list | None = None, tiles_dev: list | None = None,
+                      out_host: torch.Tensor | None = None) -> RequestResult:
+        """Encode a batch of requests (``_start_encode``, engine.py:583-602): every request is
+        IRP-sharded over the ranks restarting at worker 0, each rank encodes all of its shards of
+        the batch in ONE encoder call, and the shards land on the prefill rank in one exchange,
+        packed request after request (request r at tile offset sum(n[:r])). Pass the requests'
+        host tiles (pinned) or device tiles; every rank passes the same batch. Uncached path."""
+        if self.cached:
+            raise ValueError("process_batch runs the uncached path")
+        src_list = tiles_dev if tiles_dev is not None else tiles_host
+        ns = [t.shape[0] for t in src_list]
+        offs = [sum(ns[:r]) for r in range(len(ns))]
+        m = sum(ns)
+        is_sink = self.rank == self.prefill_rank
+        parts, senders = [], set()
+        for r, n in enumerate(ns):
+            for k, (first, count) in enumerate(shard_ranges(n, self.world)):
+                if count:
+                    senders.add(k)
+                    if k == self.rank:
+                        parts.append((r, first, count))
+        mine = sum(c for _, _, c in parts)
+        ex = self._open_exchange(m, ring=True)
+        local = None
+        if mine:
+            S, Cc = self.cfg.image_size, self.cfg.channels
+            if tiles_dev is not None and len(parts) == 1:
+                r, first, count = parts[0]
+                src, release = tiles_dev[r][first:first + count], None
+            else:
+                ring, k = self._slot("bin", (mine, S, S, Cc), torch.uint8)
+                if ring["free"][k] is not None:  # the slot's previous encode has read it
+                    torch.cuda.current_stream(self.device).wait_event(ring["free"][k])
+                src = ring["bufs"][k]
+                o = 0
+                for r, first, count in parts:
+                    src[o:o + count].copy_(src_list[r][first:first + count], non_blocking=True)
+                    o += count
+
+                def release(ring=ring, k=k):
+                    ev = torch.cuda.Event()
+                    ev.record(torch.cuda.current_stream(self.device))
+                    ring["free"][k] = ev
+            local = self._buffer(mine)
+            self.enc.encode(src.contiguous(), local)
+            if release is not None:
+                release()
+        pieces, o = [], 0
+        for r, first, count in parts:
+            pieces.append((local[o:o + count], offs[r] + first))
+            o += count
+        self._close_pieces(ex, pieces, senders, ns, offs)
+        res = RequestResult(rid=0, n_tiles=m, encoded_tiles=mine)
+        res._slot = ex["slot"]
+        res.shards = [ShardRecord(k, c) for n in ns for k, (_, c) in enumerate(shard_ranges(n, self.world)) if c]
+        tpp, bpt = self.cfg.out_tokens, self.cfg.out_dim * 2
+        res.ep_bytes = sum(ep_bytes(c, tpp, bpt) for n in ns for k, (_, c) in enumerate(shard_ranges(n, self.world))
+                           if k != self.prefill_rank)
+        res.tokens = ex["dest"]
+        if out_host is not None and res.tokens is not None:
+            res.readback = self._readback(res.tokens, out_host, res._slot) if self._down is not None else None
+            if res.readback is None:
+                out_host.copy_(res.tokens)
+        return res
+
+    def _close_pieces(self, ex: dict, pieces, senders, ns, offs) -> None:
+        """process_batch's exchange: this rank's pieces (local view, tile offset in the batch)
+        reach the prefill rank; the prefill rank copies its own pieces in place."""
+        peer, is_sink = ex["peer"], self.rank == self.prefill_rank
+        s = torch.cuda.current_stream(self.device)
+        if is_sink:
+            for view, off in pieces:
+                ex["dest"][off:off + view.shape[0]].copy_(view)
+        if peer is not None:
+            if is_sink:
+                fake = [(0, 1 if k in senders else 0) for k in range(self.world)]
+                peer.wait(ex["seq"], fake, s)
+            elif pieces:
+                peer.put_many(ex["seq"], pieces, s)
+            return
+        if self.world == 1:
+            return
+        if self.comm is not None:  # one C-ABI gather per request (contiguous shards)
+            by_req = {}
+            for view, off in pieces:
+                r = max(i for i in range(len(offs)) if offs[i] <= off)
+                by_req[r] = view
+            for r, n in enumerate(ns):
+                dest = ex["dest"][offs[r]:offs[r] + n] if is_sink else None
+                self.comm.gather_tokens(None if is_sink else by_req.get(r), n, dest, root=self.prefill_rank)
+            return
+        ops = []
+        if is_sink:
+            for r, n in enumerate(ns):
+                for k, (first, count) in enumerate(shard_ranges(n, self.world)):
+                    if k != self.rank and count:
+                        dst = ex["dest"][offs[r] + first:offs[r] + first + count]
+                        ops.append(dist.P2POp(dist.irecv, dst, k, self.group))
+        else:
+            for view, _ in pieces:
+                ops.append(dist.P2POp(dist.isend, view.contiguous(), self.prefill_rank, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
     def _open_exchange(self, m: int, ring: bool) -> dict:
         """Start the EP exchange of an m-tile request on every rank: picks the transport
         (the peer slots when they are up and hold m tiles, else the collective) and, on the

@@ -21,7 +21,8 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,tiles,mode", [(2, 10, ""), (3, 13, ""), (3, 12, "cache")])
+@pytest.mark.parametrize("world,tiles,mode", [(2, 10, ""), (3, 13, ""), (3, 12, "cache"), (2, 10, "batch"),
+                                              (3, 10, "batch")])
 def test_irp_peer_gather_multiprocess(cuda, world, tiles, mode):
     """mode "cache": the prefill rank's MM-token cache plans the misses, which are sharded
     and land in the peer slot as staging before being scattered into the cache store."""
@@ -31,5 +32,5 @@ def test_irp_peer_gather_multiprocess(cuda, world, tiles, mode):
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=240)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
-    tag = f"irp_check world={world} tiles={tiles}" + (" cache" if mode else "")
+    tag = f"irp_check world={world} tiles={tiles}" + (f" {mode}" if mode else "")
     assert tag in out and "OK (transport nvlink-peer)" in out, out[-3000:]
