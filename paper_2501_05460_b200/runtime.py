@@ -57,7 +57,6 @@ class ServeRequest:
     tiles: torch.Tensor
     prompt: torch.Tensor            # int32 [prompt_tokens]
     output_tokens: int = 1
-    arrival: float = 0.0            # seconds (host clock, filled by serve())
 
 
 @dataclass
@@ -285,7 +284,6 @@ class EPDRuntime:
         # E-side MM blocks: each encode instance's reservation for a request's full mm_tokens
         self.e_mms = ([BlockManager(CacheKind.MM, block_size, -(-e_mm_tokens // block_size)) for _ in range(instances)]
                       if self.is_coord else None)
-        self.e_mm = self.e_mms[0] if self.is_coord else None
         self.p = MMPool(self.device, self.rank, self.world, -(-p_mm_tokens // block_size), block_size,
                         self.cfg.out_dim, group)
         self.stamps = _Stamps(self.device)
@@ -318,7 +316,7 @@ class EPDRuntime:
         s = torch.cuda.current_stream(self.device)
         T, D = self.cfg.out_tokens, self.cfg.out_dim
         reqs = {r.rid: r for r in requests}
-        # trace clock: %globaltimer ns; host arrivals mapped through one calibration stamp
+        # trace clock: %globaltimer ns from a calibration stamp taken when the burst arrives
         torch.cuda.synchronize(self.device)
         cal = self.stamps.mark(s)
         torch.cuda.synchronize(self.device)
