@@ -262,7 +262,10 @@ class EPDRuntime:
     """Lockstep encode -> prefill runtime over the ranks of an :class:`~.stage.EncodeStage`."""
 
     def __init__(self, stage, prefiller, max_batch: int = 4, e_mm_tokens: int = 48_000, p_mm_tokens: int = 48_000,
-                 block_size: int = 16, group=None, instances: int = 1, policy: str = "round_robin"):
+                 block_size: int = 16, group=None, instances: int = 1, policy: str = "round_robin",
+                 pool=None, stamps=None):
+        """``pool`` / ``stamps`` replace the device MM pool transport and the %globaltimer stamps
+        (the gloo CPU tier injects host stand-ins; production uses MMPool and _Stamps)."""
         self.stage, self.pf = stage, prefiller
         self.cfg = stage.cfg
         self.rank, self.world, self.device = stage.rank, stage.world, stage.device
@@ -284,9 +287,10 @@ class EPDRuntime:
         # E-side MM blocks: each encode instance's reservation for a request's full mm_tokens
         self.e_mms = ([BlockManager(CacheKind.MM, block_size, -(-e_mm_tokens // block_size)) for _ in range(instances)]
                       if self.is_coord else None)
-        self.p = MMPool(self.device, self.rank, self.world, -(-p_mm_tokens // block_size), block_size,
-                        self.cfg.out_dim, group)
-        self.stamps = _Stamps(self.device)
+        nblocks = -(-p_mm_tokens // block_size)
+        self.p = pool(self, nblocks) if pool is not None else MMPool(self.device, self.rank, self.world, nblocks,
+                                                                     block_size, self.cfg.out_dim, group)
+        self.stamps = stamps if stamps is not None else _Stamps(self.device)
         self.seq = 0
         self.keep_mm = False  # tests: keep a copy of each request's MM tokens as prefill read them
 
@@ -312,14 +316,18 @@ class EPDRuntime:
         finally:
             self._tiles = {}
 
+    def _sync(self) -> None:
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+
     def _serve(self, requests):
-        s = torch.cuda.current_stream(self.device)
+        s = torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
         T, D = self.cfg.out_tokens, self.cfg.out_dim
         reqs = {r.rid: r for r in requests}
         # trace clock: %globaltimer ns from a calibration stamp taken when the burst arrives
-        torch.cuda.synchronize(self.device)
+        self._sync()
         cal = self.stamps.mark(s)
-        torch.cuda.synchronize(self.device)
+        self._sync()
         held: dict[int, torch.Tensor] = {}      # rid -> this rank's encoded shard, not yet sent
         marks: dict = {}                         # ("start"|"end"|"xfer"|"ep"|"pre0"|"pre1", rid[, k]) -> slot
         if self.is_coord:
@@ -412,7 +420,7 @@ class EPDRuntime:
                     marks[("pre1", rid)] = self.stamps.mark(s)
                     first_tok[rid] = tok.clone()
                     self.p.manager.free(rid)       # _on_batch_end: P-side MM blocks free
-        torch.cuda.synchronize(self.device)
+        self._sync()
         wall = time.perf_counter() - t_wall0
         st = self.stamps.read()
         mine = {k: st[v] for k, v in marks.items() if k[0] in ("start", "end")}
