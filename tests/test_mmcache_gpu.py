@@ -129,3 +129,25 @@ def test_kv_pack_unpack_and_local_handoff(cuda):
     assert info["pd_bytes"] == total * p.kv_bytes_per_token
     assert info["moved_bytes"] == 5 * 16 * p.kv_bytes_per_token
     assert 1 not in p.manager.allocated  # prefill side freed after the send (engine.py:437)
+
+
+def test_cached_stage_bit_exact_siglip_c4_shape(cuda):
+    """C4's structure at the real encoder (SigLIP-400M + resampler, 27 layers): 40 tiles, tile
+    i + 20 repeating tile i. The cached path (device plan, keyed hash, miss gather, scatter into
+    the store, packing) returns exactly the tokens of encoding every tile directly; a second
+    request is served from the cache alone."""
+    from paper_2501_05460_b200.configs import SEED, SIGLIP_MINICPM
+    from paper_2501_05460_b200.encoder import VisionEncoder
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    from paper_2501_05460_b200.stage import EncodeStage, tiles_for_request
+    cfg = SIGLIP_MINICPM
+    enc = VisionEncoder(cfg, cuda, max_tiles=20)
+    tiles = tiles_for_request(40, cfg, SEED, repeat_period=20)
+    direct = torch.cat([enc.encode(tiles[i:i + 20].to(cuda)) for i in (0, 20)])
+    cache = MMTokenCache(64, cfg.out_tokens, cfg.out_dim, cuda)
+    st = EncodeStage(enc, cuda, cache=cache)
+    r1 = st.process(tiles.pin_memory())
+    r2 = st.process(tiles.pin_memory())
+    torch.cuda.synchronize()
+    assert r1.cache_counts == {"hit": 0, "miss": 20, "dup": 20} and r2.cache_counts["hit"] == 40
+    assert torch.equal(r1.tokens, direct) and torch.equal(r2.tokens, direct)

@@ -27,16 +27,19 @@ def _inputs(cfg, n_mm, n_text, dev, seed):
     return mm, ids
 
 
-@pytest.mark.parametrize("which,n_mm,n_text", [("tiny", 48, 22), ("tiny", 0, 5), ("qwen2-L2", 640, 22)])
+@pytest.mark.parametrize("which,n_mm,n_text", [("tiny", 48, 22), ("tiny", 0, 5), ("qwen2-L2", 640, 22),
+                                               ("internlm-L2", 3328, 22)])
 def test_prefill_matches_oracle(cuda, which, n_mm, n_text):
+    """qwen2-L2: the C2 prefill width (662 tokens); internlm-L2: the C5 one (13 tiles x 256 MM
+    tokens + prompt = 3350 tokens, grouped K/V 32 / 8 heads)."""
     import oracle.llm as ol
     from paper_2501_05460_b200.handoff import PagedKVCache
-    from paper_2501_05460_b200.prefill import QWEN2_7B, TINY_LLM, Prefiller
-    cfg = TINY_LLM if which == "tiny" else QWEN2_7B.with_layers(2)
-    pf = Prefiller(cfg, cuda, max_tokens=704)
+    from paper_2501_05460_b200.prefill import INTERNLM25_7B, QWEN2_7B, TINY_LLM, Prefiller
+    cfg = {"tiny": TINY_LLM, "qwen2-L2": QWEN2_7B.with_layers(2), "internlm-L2": INTERNLM25_7B.with_layers(2)}[which]
+    pf = Prefiller(cfg, cuda, max_tokens=max(704, n_mm + n_text))
     mm, ids = _inputs(cfg, n_mm, n_text, cuda, SEED + n_mm)
     T = n_mm + n_text
-    kv = PagedKVCache(cfg.layers, cfg.kv_heads, cfg.head_dim, 16, 64, cuda)
+    kv = PagedKVCache(cfg.layers, cfg.kv_heads, cfg.head_dim, 16, max(64, -(-(n_mm + n_text) // 16)), cuda)
     blocks = kv.manager.allocate(1, T)
     tok = int(pf.prefill(mm, ids, kv=kv, block_ids=blocks))
     torch.cuda.synchronize()
@@ -76,3 +79,22 @@ def test_prefill_graph_equals_direct_and_rejects_bad_input(cuda):
         pf.prefill(None, torch.zeros(200, dtype=torch.int32, device=cuda))
     with pytest.raises(ValueError):
         pf.prefill(torch.zeros(3, 7, dtype=torch.bfloat16, device=cuda), ids)
+
+
+def test_paged_mm_input_equals_packed(cuda):
+    """The runtime's paged MM input (rows gathered from the prefill instance's MM blocks in
+    any block order) gives the same hidden state, bit for bit, as the packed input."""
+    from paper_2501_05460_b200.prefill import QWEN2_7B, Prefiller
+    cfg = QWEN2_7B.with_layers(2)
+    pf = Prefiller(cfg, cuda, max_tokens=704)
+    mm, ids = _inputs(cfg, 640, 22, cuda, 5)
+    pf.prefill(mm, ids)
+    torch.cuda.synchronize()
+    packed = pf.h[:662].clone()
+    blocks = torch.randperm(100, generator=torch.Generator().manual_seed(1))[:40]  # 40 blocks of 16 tokens
+    pool = torch.zeros(100 * 16, cfg.hidden, dtype=torch.bfloat16, device=cuda)
+    rows = (blocks.view(-1, 1) * 16 + torch.arange(16)).view(-1)
+    pool[rows.to(cuda)] = mm
+    pf.prefill(None, ids, mm_pool=pool, mm_rows=rows.to(torch.int32))
+    torch.cuda.synchronize()
+    assert torch.equal(pf.h[:662], packed)

@@ -1,3 +1,7 @@
+#!/bin/bash
+# Round-end measurements into gpurun_out/r02 (copied into profiles/r02 afterwards):
+# bench lines of every workload, the reference arm, the N = 2 path on one GPU, ncu launch
+# lists and one-layer full captures of C2 / C5, small-shard encode times.
 set -x
 python -m paper_2501_05460_b200.build > /dev/null 2>&1
 mkdir -p gpurun_out/r02
