@@ -58,7 +58,10 @@ def test_prefill_matches_oracle(cuda, which, n_mm, n_text):
         got_k = torch.stack([kv.pool[2 * layer, blocks[t // 16], (t % 16) * row:(t % 16 + 1) * row] for t in range(T)])
         got_v = torch.stack([kv.pool[2 * layer + 1, blocks[t // 16], (t % 16) * row:(t % 16 + 1) * row]
                              for t in range(T)])
-        assert relerr(got_k, ref["k"][layer]) <= TOL and relerr(got_v, ref["v"][layer]) <= TOL
+        # layer 0's K/V carry only their own bf16 rounding; later layers also carry the hidden
+        # state's accumulated rounding (bounded like the hidden state)
+        tol = TOL if layer == 0 else TOL_H
+        assert relerr(got_k, ref["k"][layer]) <= tol and relerr(got_v, ref["v"][layer]) <= tol
 
 
 def test_prefill_graph_equals_direct_and_rejects_bad_input(cuda):
