@@ -117,6 +117,11 @@ enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS
 #endif
 
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
+#ifndef EPD_GEMM_EPI_WARPS
+#define EPD_GEMM_EPI_WARPS 8  // epilogue warps: 8 = two column halves x 4 lane quarters; 4 = one half
+#endif
+constexpr int kEpiWarps = EPD_GEMM_EPI_WARPS;
+constexpr int kEpiHalves = kEpiWarps / 4;
 
 template <int BN, int CG>
 struct GemmCfg {
@@ -127,7 +132,7 @@ struct GemmCfg {
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 2 * kEpiStageBytes + 1024 + 256;
-  static constexpr int THREADS = 64 + 256;
+  static constexpr int THREADS = 64 + 32 * kEpiWarps;
 };
 
 EPD_DEVICE uint32_t cluster_rank() {
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 8 * CG);  // one arrive per epilogue warp of every CTA in the pair
+      mbar_init(&tempty[s], kEpiWarps * CG);  // one arrive per epilogue warp of every CTA in the pair
     }
     fence_barrier_init();
     tma_prefetch_desc(&tmA);
@@ -422,7 +427,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     }
   } else {
     // ---------------- epilogue: 8 warps = 2 halves x 4 TMEM lane quarters
-    const int half = (warp - 2) >> 2;
+    const int half = kEpiHalves == 2 ? (warp - 2) >> 2 : 0;
     const int q = warp & 3;
     const int r = q * 32 + lane;  // row within the tile (TMEM lane)
     const bool leader = ((warp - 2) & 3) == 0 && lane == 0;
@@ -436,7 +441,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       const TileAt x = tile_at(sched, tile, BN);
       const int m0 = x.mt * (kBM * CL) + crank_full * kBM;
       const int n0 = x.n0;
-      const int hw = x.w / 2;  // columns per epilogue half (a multiple of 32)
+      const int hw = x.w / kEpiHalves;  // columns per epilogue half (a multiple of 32)
       const int row = m0 + r;
       // Heads bookkeeping, once per tile-half (no divisions inside the chunk loop):
       // section / head / head-dim of this half's first column, image and token of m0.
