@@ -318,6 +318,9 @@ class EncodeStage:
             if tiles_dev is not None and len(parts) == 1:
                 r, first, count = parts[0]
                 src, release = tiles_dev[r][first:first + count], None
+            elif self._up is None:  # host-side stage (gloo CPU tier)
+                src = torch.cat([src_list[r][first:first + count] for r, first, count in parts])
+                release = None
             else:
                 ring, k = self._slot("bin", (mine, S, S, Cc), torch.uint8)
                 if ring["free"][k] is not None:  # the slot's previous encode has read it
@@ -358,7 +361,7 @@ class EncodeStage:
         """process_batch's exchange: this rank's pieces (local view, tile offset in the batch)
         reach the prefill rank; the prefill rank copies its own pieces in place."""
         peer, is_sink = ex["peer"], self.rank == self.prefill_rank
-        s = torch.cuda.current_stream(self.device)
+        s = torch.cuda.current_stream(self.device) if peer is not None else None
         if is_sink:
             for view, off in pieces:
                 ex["dest"][off:off + view.shape[0]].copy_(view)

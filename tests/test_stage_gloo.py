@@ -105,3 +105,66 @@ def test_irp_gather_request_order(world, n):
     assert outs[0]["ep_bytes"] == sum(c for k, (_, c) in enumerate(ranges) if k != 0) * 4 * 8 * 2
     assert (outs[0]["tokens"] == outs[0]["expected"]).all()
     assert (outs[0]["gathered"] == outs[0]["expected"]).all()
+
+
+class _GlooComm:
+    """Stand-in for comm.NcclComm.gather_tokens over gloo (the C ABI's epd_gather_tokens
+    contract: rank k's shard of epd_irp_ranges(n, world) lands on the root at its offset)."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+    def gather_tokens(self, shard, n_tiles, packed, root=0):
+        ranges = shard_ranges(n_tiles, self.world)
+        if self.rank == root:
+            for k, (first, count) in enumerate(ranges):
+                if count and k != root:
+                    buf = torch.empty_like(packed[first:first + count])
+                    dist.recv(buf, k)
+                    packed[first:first + count] = buf
+        elif ranges[self.rank][1]:
+            dist.send(shard.contiguous(), root)
+
+
+def _batch_worker(rank, world, port, ns, use_comm, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2501_05460_b200.stage import EncodeStage
+        batch = [torch.randint(0, 256, (n, 8, 8, 3), dtype=torch.uint8, generator=torch.Generator().manual_seed(i))
+                 for i, n in enumerate(ns)]
+        enc = _StandInEncoder()
+        st = EncodeStage(enc, torch.device("cpu"), rank=rank, world=world, prefill_rank=0,
+                         comm=_GlooComm(rank, world) if use_comm else None)
+        res = st.process_batch(tiles_host=batch)
+        mine = sum(shard_ranges(n, world)[rank][1] for n in ns)
+        out = {"rank": rank, "calls": enc.calls[:], "mine": mine, "encoded": res.encoded_tiles}
+        if rank == 0:
+            out["tokens"] = res.tokens.float().numpy()
+            out["expected"] = torch.cat([_expected(t) for t in batch]).float().numpy()
+        q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,ns,use_comm", [(2, (10, 10), False), (3, (10, 13, 1), False), (3, (10, 10, 10), True),
+                                               (2, (1, 5), True)])
+def test_process_batch_gloo(world, ns, use_comm):
+    """EncodeStage.process_batch: every request IRP-sharded over all ranks from worker 0, one
+    encoder call per rank for all its shards, the batch packed request after request on the
+    prefill rank -- torch P2P and the C-ABI gather contract (per request)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batch_worker, args=(r, world, port, ns, use_comm, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=120) for _ in range(world)], key=lambda o: o["rank"])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for o in outs:
+        assert o["encoded"] == o["mine"]
+        assert o["calls"] == ([o["mine"]] if o["mine"] else [])  # one encoder call per rank
+    assert (outs[0]["tokens"] == outs[0]["expected"]).all()
