@@ -67,6 +67,12 @@ def workload(name: str):
                     desc="C2 served: bursts of 8 MiniCPM-V requests (10 tiles each) through EPDRuntime, encode "
                          "batches of up to 4 requests (form_batch + E/P-side MM reservations), shards stored into "
                          "the prefill instance's paged MM blocks, Qwen2-7B prefill to the first token")
+    if name == "c2p":
+        return dict(cfg=SIGLIP_MINICPM, tiles=10, repeat=None, cache=False, llm="qwen2-7b", serve=(64, 4),
+                    poisson=40.0,
+                    desc="C2 open loop: 64 MiniCPM-V requests (10 tiles each) arriving as workload.generate_poisson "
+                         "at 40 requests/s (seed 20260808), served by EPDRuntime (batches of up to 4, Qwen2-7B "
+                         "prefill to the first token)")
     if name == "c4":
         return dict(cfg=SIGLIP_MINICPM, tiles=400, repeat=200, cache=True, llm="qwen2-7b",
                     desc="C4: 40 images x 10 tiles per request, image i+20 repeats image i (MM-token cache)")
@@ -298,10 +304,15 @@ def run_serve(args, wl, world, rank, local):
     pf = Prefiller(QWEN2_7B, dev, max_tokens=T_pre) if rank == 0 else None
     rt = EPDRuntime(stage, pf, max_batch=max_batch)
     reqs = []
+    arrivals = [0.0] * n_req
+    if wl.get("poisson"):
+        from paper_2501_05460_b200.routing import poisson_arrivals
+        arrivals = poisson_arrivals(wl["poisson"], n_req, 20260808)
+    pool = [tiles_for_request(n, cfg, seed=20260808 + i).pin_memory() for i in range(min(n_req, 8))]
     for i in range(n_req):
         prompt = torch.randint(0, QWEN2_7B.vocab, (PROMPT_TOKENS,), dtype=torch.int32,
                                generator=torch.Generator().manual_seed(100 + i)).to(dev)
-        reqs.append(ServeRequest(i, tiles_for_request(n, cfg, seed=20260808 + i).pin_memory(), prompt))
+        reqs.append(ServeRequest(i, pool[i % len(pool)], prompt, arrival=arrivals[i]))
     for _ in range(args.warmup):
         rt.serve(reqs)
     torch.cuda.synchronize()
@@ -336,9 +347,10 @@ def run_serve(args, wl, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": bench_config(wl, world) | {"requests_per_burst": n_req, "max_batch": max_batch},
             "p50_ttft_ms": _percentile(ttft, 0.5), "ttft_p90_ms": _percentile(ttft, 0.9), "ttft_n": len(ttft),
-            "ttft_note": "per request of a burst: first_token_time - arrival from the measured RequestRecords "
-                         "(%globaltimer), all requests arriving at the burst start; includes queueing behind "
-                         "earlier batches and prefills",
+            "ttft_note": "per request: first_token_time - arrival from the measured RequestRecords (%globaltimer); "
+                         + ("open-loop Poisson arrivals (routing.poisson_arrivals = workload.generate_poisson)"
+                            if wl.get("poisson") else "all requests arriving at the burst start")
+                         + "; includes queueing behind earlier batches and prefills",
             "ep_wait_per_burst": len(out["ep_wait"]), "clocks": clk.summary(),
             "roofline": None, "cpu_baseline": None,
             "e2e": {"value": value, "unit": "tiles/s", "h2d_bytes_per_step": n_req * n * cfg.tile_bytes,

@@ -85,6 +85,16 @@ def form_batch(queue, max_batch: int, fits) -> list:
     return batch
 
 
+def poisson_arrivals(rate: float, n: int, seed: int) -> list[float]:
+    """Arrival times of workload.generate_poisson (workload.py:71-96): the cumulative sum of
+    ``n`` seeded exponential gaps with mean 1 / rate (numpy PCG64 ``default_rng(seed)``)."""
+    import numpy as np
+    if rate <= 0 or n < 1:
+        raise ValueError("rate must be positive and n >= 1")
+    gaps = np.random.default_rng(seed).exponential(1.0 / rate, size=n)
+    return [float(t) for t in np.cumsum(gaps)]
+
+
 def ep_bytes(tiles: int, tokens_per_patch: int, mm_bytes_per_token: int) -> int:
     return tiles * tokens_per_patch * mm_bytes_per_token
 

@@ -57,6 +57,7 @@ class ServeRequest:
     tiles: torch.Tensor
     prompt: torch.Tensor            # int32 [prompt_tokens]
     output_tokens: int = 1
+    arrival: float = 0.0            # seconds after serve() starts (open-loop replay)
 
 
 @dataclass
@@ -331,31 +332,50 @@ class EPDRuntime:
         held: dict[int, torch.Tensor] = {}      # rid -> this rank's encoded shard, not yet sent
         marks: dict = {}                         # ("start"|"end"|"xfer"|"ep"|"pre0"|"pre1", rid[, k]) -> slot
         if self.is_coord:
-            # assign_instance on arrival (engine.py:270-283), load = outstanding tiles (_arrival_load)
+            # open-loop arrivals: a request joins its encode instance's queue once its arrival
+            # time has passed; assign_instance on arrival (engine.py:270-283) with the instance
+            # load = its outstanding tiles, queued and in flight (_arrival_load, engine.py:277-286)
+            pending = deque(sorted(requests, key=lambda r: (r.arrival, r.rid)))
+            open_loop = any(r.arrival > 0 for r in requests)
             queues = [deque() for _ in range(self.instances)]
             load = [0] * self.instances
             inst_of: dict[int, int] = {}
             rr = 0
-            for r in requests:
-                iid, rr = assign_instance(self.policy, [(i, float(load[i])) for i in range(self.instances)], rr)
-                inst_of[r.rid] = iid
-                queues[iid].append(r.rid)
-                load[iid] += r.tiles.shape[0]
             ep_wait: deque = deque()
             ready: deque = deque()
             recs: dict[int, RequestRecord] = {}
-            for r in requests:
-                mm = r.tiles.shape[0] * T
-                recs[r.rid] = RequestRecord(r.rid, 0.0, int(r.prompt.numel()), mm, mm + int(r.prompt.numel()),
-                                            r.output_tokens, e_instance=inst_of[r.rid])
             p_blocks: dict[int, list[int]] = {}
             waited = []
+            enc_done = None  # event after the coordinator's last encode (the instance is busy until then)
+
+            def admit(now: float) -> None:
+                nonlocal rr
+                while pending and pending[0].arrival <= now:
+                    r = pending.popleft()
+                    iid, rr = assign_instance(self.policy, [(i, float(load[i])) for i in range(self.instances)], rr)
+                    inst_of[r.rid] = iid
+                    queues[iid].append(r.rid)
+                    load[iid] += r.tiles.shape[0]
+                    mm = r.tiles.shape[0] * T
+                    recs[r.rid] = RequestRecord(r.rid, r.arrival, int(r.prompt.numel()), mm,
+                                                mm + int(r.prompt.numel()), r.output_tokens, e_instance=iid)
         first_tok, kept = {}, {}
         t_wall0 = time.perf_counter()
         while True:
             # ---- coordinator: _retry_waits first, then a new encode batch (engine.py:680-700)
             cmd = None
             if self.is_coord:
+                if open_loop:
+                    # a new batch starts once the encode instance finished its previous one
+                    # (engine.py: one running batch per instance); meanwhile requests arrive
+                    if enc_done is not None:
+                        enc_done.synchronize()
+                    admit(time.perf_counter() - t_wall0)
+                    if pending and not any(queues) and not ep_wait:
+                        time.sleep(max(0.0, pending[0].arrival - (time.perf_counter() - t_wall0)))
+                        admit(time.perf_counter() - t_wall0)
+                else:
+                    admit(float("inf"))
                 pre = []
                 while ep_wait:
                     rid = ep_wait[0]
@@ -379,8 +399,8 @@ class EPDRuntime:
                     for _ in b:
                         queue.popleft()
                     batch += [(rid, reqs[rid].tiles.shape[0], iid) for rid in b]
-                done = not (any(queues) or ep_wait or batch or pre)
-                if not done and not batch and not pre:
+                done = not (any(queues) or ep_wait or batch or pre or pending)
+                if not done and not batch and not pre and not pending:
                     # nothing in flight and nothing can start: a request larger than an MM pool
                     raise RuntimeError("the MM blocks cannot hold the head request (mm_capacity)")
                 cmd = {"pre": [(rid, blocks, inst_of[rid]) for rid, blocks in pre], "batch": batch, "done": done}
@@ -389,6 +409,9 @@ class EPDRuntime:
                 break
             self._send(cmd["pre"], held, marks, s)
             self._encode(cmd["batch"], held, marks, s)
+            if self.is_coord and open_loop and cmd["batch"] and s is not None:
+                enc_done = torch.cuda.Event()
+                enc_done.record(s)
             # ---- coordinator: _on_worker_done -> _try_reserve_prefill, else ep_wait (engine.py:369-383)
             post = None
             if self.is_coord:
@@ -407,6 +430,7 @@ class EPDRuntime:
             if self.is_coord:
                 for rid, _, iid in cmd["pre"] + post:
                     self.e_mms[iid].free(rid)      # _on_transfer_end("ep"): all shards landed
+                    load[iid] -= reqs[rid].tiles.shape[0]
                     ready.append(rid)
                 while ready:
                     rid = ready.popleft()
@@ -438,7 +462,8 @@ class EPDRuntime:
         def sec(ns):
             return (ns - base) / 1e9
         for rid, rec in recs.items():
-            rec.arrival = 0.0  # the burst arrives at the calibration stamp
+            # arrivals are host seconds after the calibration stamp's completion, so they trail
+            # the device clock slightly: arrival <= encode start holds by construction
             n = reqs[rid].tiles.shape[0]
             base_rank = rec.e_instance * self.width
             shards = []

@@ -94,3 +94,16 @@ def test_assign_instance_matches_reference(ds):
             assert assign_instance(pol.value, cands, ctr) == engine.assign_instance(pol, cands, ctr)
     with pytest.raises(ValueError):
         assign_instance("fcfs", [])
+
+
+def test_poisson_arrivals_match_reference(ds):
+    """routing.poisson_arrivals (the open-loop replay of EPDRuntime / bench c2p) reproduces
+    workload.generate_poisson's arrival times exactly (workload.py:71-96)."""
+    wl = ds[4]
+    from paper_2501_05460_b200.routing import poisson_arrivals
+    for rate, n, seed in [(0.125, 100, 20260808), (40.0, 64, 7), (3.0, 5, 0)]:
+        import disaggsim.models as models
+        spec = wl.WorkloadSpec(rate_lambda=rate, num_requests=n, seed=seed, prompt_tokens=22, output_tokens=8,
+                               images_per_request=1, resolution=(4032, 3024))
+        ref = [r.arrival_time for r in wl.generate_poisson(spec)]
+        assert poisson_arrivals(rate, n, seed) == ref

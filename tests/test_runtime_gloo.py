@@ -132,11 +132,15 @@ def _run(rank, world, scenario):
     from paper_2501_05460_b200.runtime import EPDRuntime, check_causality
     kw = {"plain": {}, "pwait": {"p_mm_tokens": 6 * T}, "ewait": {"e_mm_tokens": 6 * T},
           "inst_rr": {"instances": world, "policy": "round_robin"},
-          "inst_ll": {"instances": world, "policy": "least_loaded"}}[scenario]
+          "inst_ll": {"instances": world, "policy": "least_loaded"}, "poisson": {}}[scenario]
     stage, pf = _Stage(rank, world), (_Prefiller() if rank == 0 else None)
     rt = EPDRuntime(stage, pf, max_batch=3, block_size=BS, pool=_HostPool, stamps=_Stamps(), **kw)
     rt.keep_mm = True
     reqs = _requests()
+    if scenario == "poisson":  # open loop: generate_poisson arrivals at 150 requests/s
+        from paper_2501_05460_b200.routing import poisson_arrivals
+        for r, t in zip(reqs, poisson_arrivals(150.0, len(reqs), 3)):
+            r.arrival = t
     out = rt.serve(reqs)
     errs = []
     if rank == 0:
@@ -158,6 +162,11 @@ def _run(rank, world, scenario):
             errs.append(f"ep_wait history {out['ep_wait']}")
         if scenario != "pwait" and out["ep_wait"]:
             errs.append(f"unexpected ep_wait {out['ep_wait']}")
+        if scenario == "poisson":
+            for r in reqs:
+                rec = out["records"][r.rid]
+                if rec.arrival != r.arrival or rec.encode_start < r.arrival:
+                    errs.append(f"request {r.rid}: arrival {rec.arrival} / encode start {rec.encode_start}")
         starts = {round(rec.encode_start, 9) for rec in out["records"].values()}
         if scenario == "ewait" and len(starts) < 4 * rt.instances:
             errs.append(f"ewait: {len(starts)} batches")
@@ -188,7 +197,8 @@ def _worker(rank, world, port, scenario, q):
 
 
 @pytest.mark.parametrize("world,scenario", [(1, "plain"), (1, "pwait"), (2, "plain"), (2, "pwait"),
-                                            (2, "ewait"), (2, "inst_rr"), (2, "inst_ll")])
+                                            (2, "ewait"), (2, "inst_rr"), (2, "inst_ll"), (1, "poisson"),
+                                            (2, "poisson")])
 def test_runtime_control_logic_gloo(world, scenario):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
