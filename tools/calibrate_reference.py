@@ -10,9 +10,12 @@ on the product path or the GPU box reads it). Steps:
      (a 10- or 13-tile request over 1..8 workers) -- minimising the largest RELATIVE
      residual (calibrate's plain least squares over 1..32 tiles missed the 1-3 tile shards
      by up to 41 %); it is passed to calibrate as overrides;
-  2. rerun the reference's irp_ablation (ablations.py:31-58) with the synthetic and with
-     the B200-calibrated MiniCPM encode costs;
-  3. write profiles/r02/calibration_b200.json.
+  2. fit the prefill polynomial the same way from measured B200 prefill latencies
+     (profiles/r02/prefill_latency_b200.json, tools/measure_prefill_latency.py: Qwen2-7B /
+     InternLM2.5-7B on one GPU, 128..8192 tokens);
+  3. rerun the reference's irp_ablation (ablations.py:31-58) with the synthetic costs, with
+     the B200-calibrated MiniCPM encode costs, and with B200 encode AND prefill costs;
+  4. write profiles/r02/calibration_b200.json.
 """
 import json
 import sys
@@ -84,18 +87,47 @@ def main():
         }
     # irp_ablation reads SYNTHETIC_COSTS[MINICPM] at call time: run it as shipped, then with
     # the calibrated entry swapped in (restored afterwards).
+    # measured prefill: refit the prefill polynomial with the reference's calibrate (least squares
+    # over [1, t, t^2]) from the B200 samples; decode stays synthetic (out of scope)
+    pre_meas = json.loads((ROOT / "profiles" / "r02" / "prefill_latency_b200.json").read_text())
+    full = {}
+    for name, m in pre_meas["models"].items():
+        syn = presets.SYNTHETIC_COSTS[name]
+        _, dec = poly_samples(syn)
+        pre = [(float(t), float(sec)) for t, sec in m["samples"]]
+        cal = costs.calibrate([(1.0, 1.0), (2.0, 2.0)], pre, dec, enc_base=calibrated[name].enc_base,
+                              enc_per_patch=calibrated[name].enc_per_patch)
+        full[name] = cal
+        resid = max(abs(costs.prefill_latency(cal, int(t)) - sec) / sec for t, sec in pre)
+        out["models"][name]["prefill"] = {
+            "llm": m["llm"], "source": "profiles/r02/prefill_latency_b200.json",
+            "synthetic": {"prefill_base": syn.prefill_base, "prefill_per_token": syn.prefill_per_token,
+                          "prefill_quad": syn.prefill_quad},
+            "b200_calibrated": {"prefill_base": float(cal.prefill_base),
+                                "prefill_per_token": float(cal.prefill_per_token),
+                                "prefill_quad": float(cal.prefill_quad)},
+            "fit_max_rel_residual": float(resid),
+            "prefill_latency_662_tokens_s": {"synthetic": float(costs.prefill_latency(syn, 662)),
+                                             "b200_calibrated": float(costs.prefill_latency(cal, 662))}}
     rows_syn = ablations.irp_ablation()
     saved = presets.SYNTHETIC_COSTS[presets.MINICPM]
     try:
         presets.SYNTHETIC_COSTS[presets.MINICPM] = replace(saved, enc_base=calibrated[presets.MINICPM].enc_base,
                                                            enc_per_patch=calibrated[presets.MINICPM].enc_per_patch)
         rows_b200 = ablations.irp_ablation()
+        f = full[presets.MINICPM]
+        presets.SYNTHETIC_COSTS[presets.MINICPM] = replace(
+            saved, enc_base=f.enc_base, enc_per_patch=f.enc_per_patch, prefill_base=f.prefill_base,
+            prefill_per_token=f.prefill_per_token, prefill_quad=f.prefill_quad)
+        rows_b200_full = ablations.irp_ablation()
     finally:
         presets.SYNTHETIC_COSTS[presets.MINICPM] = saved
     out["irp_ablation"] = {"synthetic_encode_costs": rows_syn, "b200_calibrated_encode_costs": rows_b200,
+                           "b200_calibrated_encode_and_prefill_costs": rows_b200_full,
                            "note": "reference ablations.irp_ablation (5-worker IRP encode instance vs width-1 "
-                                   "instances, MiniCPM 4K images, Poisson 0.125 req/s, 100 requests); prefill and "
-                                   "decode remain the reference's synthetic calibration"}
+                                   "instances, MiniCPM 4K images, Poisson 0.125 req/s, 100 requests); decode stays "
+                                   "the reference's synthetic calibration; the encode-only row keeps the synthetic "
+                                   "prefill too"}
     path = ROOT / "profiles" / "r02" / "calibration_b200.json"
     path.write_text(json.dumps(out, indent=1))
     print(json.dumps(out, indent=1))
