@@ -40,8 +40,8 @@ EPD_DEVICE void load8(const bf16* src, float* x) {
 
 // Both GELU epilogues are relative-accurate on the negative tail, where 0.5 x (1 + t)
 // with a hardware tanh (abs error ~5e-4) cancels: at x = -3 that form is off by several
-// bf16 ulps. One MUFU op per element either way; the FMA-pipe arithmetic runs on packed
-// pairs (FFMA2 / FMUL2 / FADD2), two elements per instruction.
+// bf16 ulps. The FMA-pipe arithmetic runs on packed pairs (FFMA2 / FMUL2), two elements
+// per instruction.
 EPD_DEVICE float2 f2fma(float2 a, float2 b, float2 c) {
   float2 d;
   asm("{\n.reg .b64 ra, rb, rc, rd;\nmov.b64 ra, {%2,%3};\nmov.b64 rb, {%4,%5};\nmov.b64 rc, {%6,%7};\n"
@@ -65,41 +65,67 @@ EPD_DEVICE float ex2f(float x) {
   return y;
 }
 
-// GELU-tanh, 0.5 x (1 + tanh u) with u = k0 (x + k1 x^3), written as x * sigma(2u):
-// e = 2^(-2 u(|x|) log2 e) on the MUFU, r = 1 / (1 + e) by Newton on the FMA pipe
-// (1 + e lies in [1, 2]: linear minimax start, 3 steps -> fp32-exact), then
-// phi = r for x >= 0 and e r for x < 0.
-EPD_DEVICE float2 gelu_tanh_fast2(float2 x) {
-  const float2 z = make_float2(fabsf(x.x), fabsf(x.y));
-  // -2 log2(e) k0 = -2.3022082, k1 = 0.044715
-  const float2 a = f2mul(f2mul(z, f2fma(f2s(0.044715f), f2mul(z, z), f2s(1.f))), f2s(-2.302208198f));
-  const float2 e = make_float2(ex2f(a.x), ex2f(a.y));
-  const float2 y = f2fma(e, f2s(1.f), f2s(1.f));
-  float2 r = f2fma(f2s(-0.470588235f), y, f2s(1.411764706f));  // 24/17 - 8/17 y
-  const float2 ny = make_float2(-y.x, -y.y);
-#pragma unroll
-  for (int it = 0; it < 3; ++it) r = f2fma(r, f2fma(ny, r, f2s(1.f)), r);
-  const float2 er = f2mul(e, r);
-  return f2mul(x, make_float2(x.x >= 0.f ? r.x : er.x, x.y >= 0.f ? r.y : er.y));
+EPD_DEVICE float rcpf(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
+// The GELUs run over the NP packed pairs of an epilogue chunk stage by stage, so that the NP
+// dependency chains interleave (per-pair calls left the compiler ~2 chains in flight and
+// the epilogue warps, two per SM sub-partition, latency-bound: profiles/r02/ab.txt).
+//
+// GELU-tanh, 0.5 x (1 + tanh u) with u = k0 (x + k1 x^3), written as x * sigma(2u):
+// e = 2^(-2 u(|x|) log2 e) and r = 1 / (1 + e) on the MUFU (ex2, rcp), then
+// phi = r for x >= 0 and e r for x < 0.
+template <int NP>
+EPD_DEVICE void gelu_tanh_chunk(float* x) {
+  float2 a[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const float2 z = make_float2(fabsf(x[2 * p]), fabsf(x[2 * p + 1]));
+    // -2 log2(e) k0 (z + k1 z^3) = z (C0 + C1 z^2)
+    a[p] = f2mul(z, f2fma(f2mul(z, z), f2s(-0.10294324159622192f), f2s(-2.302208185195923f)));
+  }
+#pragma unroll
+  for (int p = 0; p < NP; ++p) a[p] = make_float2(ex2f(a[p].x), ex2f(a[p].y));  // e
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const float2 y = f2fma(a[p], f2s(1.f), f2s(1.f));
+    const float2 r = make_float2(rcpf(y.x), rcpf(y.y));
+    const float2 er = f2mul(a[p], r);
+    const float2 xv = make_float2(x[2 * p], x[2 * p + 1]);
+    const float2 g = f2mul(xv, make_float2(xv.x >= 0.f ? r.x : er.x, xv.y >= 0.f ? r.y : er.y));
+    x[2 * p] = g.x;
+    x[2 * p + 1] = g.y;
+  }
+}
 // GELU-erf, x Phi(x): Phi(-z) = 2^-F(z) for z = min(|x|, 8), F a degree-8 polynomial in
 // v = z/4 - 1 (tools/fit_gelu.py: max rel err 8.5e-6 against x Phi(x) on [-8, 8]; 0.025 %
 // of bf16 outputs round differently from the exact erf form, fp32 noise). Beyond |x| = 8
 // the result is x (x > 0) or below 1e-14 in magnitude. The polynomial carries -F.
-EPD_DEVICE float2 gelu_erf_fast2(float2 x) {
-  const float2 v = f2fma(make_float2(fminf(fabsf(x.x), 8.f), fminf(fabsf(x.y), 8.f)), f2s(0.25f), f2s(-1.f));
-  float2 f = f2s(5.421509966e-03f);
-  f = f2fma(f, v, f2s(-2.080199681e-02f));
-  f = f2fma(f, v, f2s(4.194424301e-02f));
-  f = f2fma(f, v, f2s(-7.617540658e-02f));
-  f = f2fma(f, v, f2s(1.449510306e-01f));
-  f = f2fma(f, v, f2s(-2.748279572e-01f));
-  f = f2fma(f, v, f2s(-1.100269699e+01f));
-  f = f2fma(f, v, f2s(-2.438505554e+01f));
-  f = f2fma(f, v, f2s(-1.494647121e+01f));
-  const float2 q = make_float2(ex2f(f.x), ex2f(f.y));
-  return f2mul(x, make_float2(x.x >= 0.f ? 1.f - q.x : q.x, x.y >= 0.f ? 1.f - q.y : q.y));
+template <int NP>
+EPD_DEVICE void gelu_erf_chunk(float* x) {
+  float2 f[NP], v[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    v[p] = f2fma(make_float2(fminf(fabsf(x[2 * p]), 8.f), fminf(fabsf(x[2 * p + 1]), 8.f)), f2s(0.25f), f2s(-1.f));
+    f[p] = f2fma(f2s(5.421509966e-03f), v[p], f2s(-2.080199681e-02f));
+  }
+  constexpr float c[7] = {4.194424301e-02f, -7.617540658e-02f, 1.449510306e-01f, -2.748279572e-01f,
+                          -1.100269699e+01f, -2.438505554e+01f, -1.494647121e+01f};
+#pragma unroll
+  for (int k = 0; k < 7; ++k)
+#pragma unroll
+    for (int p = 0; p < NP; ++p) f[p] = f2fma(f[p], v[p], f2s(c[k]));
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const float qx = ex2f(f[p].x), qy = ex2f(f[p].y);
+    const float2 xv = make_float2(x[2 * p], x[2 * p + 1]);
+    const float2 g = f2mul(xv, make_float2(xv.x >= 0.f ? 1.f - qx : qx, xv.y >= 0.f ? 1.f - qy : qy));
+    x[2 * p] = g.x;
+    x[2 * p + 1] = g.y;
+  }
 }
 
 // Epilogue kinds (the output side of C = A B^T):
@@ -149,8 +175,12 @@ EPD_DEVICE uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Relaxed arrive on the pair leader's accumulator-empty barrier: it only hands TMEM back
+// to the MMA warp, which the tcgen05 fences around the barrier order. A release.cluster
+// arrive compiles to MEMBAR.ALL.GPU + ERRBAR, a stall of every epilogue warp once per tile
+// that cost 3-8 % on every GEMM (profiles/r02/ab.txt).
 EPD_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load issued by either CTA of a pair; the transaction bytes land on the leader's barrier.
 EPD_DEVICE void tma_load_2d_pair(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -525,21 +555,17 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
               xg[0] += b0.x; xg[1] += b0.y; xg[2] += b1.x; xg[3] += b1.y;
               xg[4] += b2.x; xg[5] += b2.y; xg[6] += b3.x; xg[7] += b3.y;
             }
-            if (ep.act == ACT_GELU_TANH) {
+          }
+        }
+        if (KIND != EK_SWIGLU) {
+          if (ep.act == ACT_GELU_TANH) gelu_tanh_chunk<16>(x);
+          else if (ep.act == ACT_GELU_ERF) gelu_erf_chunk<16>(x);
+        }
 #pragma unroll
-              for (int j = 0; j < 8; j += 2) {
-                const float2 gv = gelu_tanh_fast2(make_float2(xg[j], xg[j + 1]));
-                xg[j] = gv.x;
-                xg[j + 1] = gv.y;
-              }
-            } else if (ep.act == ACT_GELU_ERF) {
-#pragma unroll
-              for (int j = 0; j < 8; j += 2) {
-                const float2 gv = gelu_erf_fast2(make_float2(xg[j], xg[j + 1]));
-                xg[j] = gv.x;
-                xg[j + 1] = gv.y;
-              }
-            }
+        for (int g = 0; g < 4 && KIND != EK_SWIGLU; ++g) {
+          const int col = n + g * 8;
+          float* xg = x + g * 8;
+          if (col < N) {
             if (ep.lscale) {
               const uint4 sv = ls_cur[g];
               const float2 s0 = unpack_bf16x2(sv.x), s1 = unpack_bf16x2(sv.y), s2 = unpack_bf16x2(sv.z),

@@ -2,7 +2,7 @@
 """Fit the GELU epilogue polynomials (csrc/gemm.cu gelu_poly): for z = min(|x|, 8),
 phi(-z) = 2^-F(z) with F a degree-8 polynomial in v = z/4 - 1, so GELU(x) = x * phi(x) costs
 one MUFU ex2 and stays relative-accurate on the negative tail (no 1 + tanh cancellation).
-GELU-tanh uses the exact sigma(2u) form instead (ex2 + Newton reciprocal, emulated below).
+GELU-tanh uses the exact sigma(2u) form instead (ex2 + rcp on the MUFU, emulated below).
 Prints the fp32 coefficients (highest power first) and the fp32-emulated accuracy."""
 import numpy as np
 import torch
@@ -54,23 +54,22 @@ if __name__ == "__main__":
         print("  {" + ", ".join(f"{c:.9e}f" for c in p) + "}")
 
 
-def emulate_tanh_newton(x):
-    """fp32 emulation of gemm.cu gelu_tanh_fast (ex2 + Newton reciprocal)."""
+def emulate_tanh_rcp(x):
+    """fp32 emulation of gemm.cu gelu_tanh_chunk (ex2 + reciprocal, both MUFU; emulated as
+    correctly rounded, the hardware approximations are within ~2 ulp)."""
     f = np.float32
     z = np.abs(x)
-    a = (z * (f(0.044715) * (z * z) + f(1)) * f(-2.302208198)).astype(np.float32)
+    a = (z * (f(-0.10294324159622192) * (z * z) + f(-2.302208185195923))).astype(np.float32)
     e = np.exp2(a.astype(np.float64)).astype(np.float32)
     y = (f(1) + e).astype(np.float32)
-    r = (f(-0.470588235) * y + f(1.411764706)).astype(np.float32)
-    for _ in range(3):
-        r = (r * (f(1) - y * r) + r).astype(np.float32)
+    r = (f(1) / y).astype(np.float32)
     return (x * np.where(x >= 0, r, e * r)).astype(np.float32)
 
 
 if __name__ == "__main__":
-    g = emulate_tanh_newton(x)
+    g = emulate_tanh_rcp(x)
     ex = x.astype(np.float64) * exact_phi("tanh", x.astype(np.float64))
     m = np.abs(ex) > 1e-30
     mis = (torch.from_numpy(g).bfloat16() != torch.from_numpy(ex.astype(np.float32)).bfloat16()).float().mean()
-    print(f"tanh (ex2 + Newton): max rel err {(np.abs(g[m] - ex[m]) / np.abs(ex[m])).max():.2e}, "
+    print(f"tanh (ex2 + rcp): max rel err {(np.abs(g[m] - ex[m]) / np.abs(ex[m])).max():.2e}, "
           f"bf16 outputs differing {float(mis):.5f}")

@@ -33,7 +33,7 @@ dev = torch.device("cuda")
 M = int(os.environ.get("M", "10240"))
 line = []
 for (N, K, act, name, acc) in [(3840, 1152, "none", "qkv", False), (1152, 1152, "none", "o+acc", True),
-                               (4304, 1152, "gelu_tanh", "fc1", False), (1152, 4304, "none", "fc2+acc", True),
+                               (4304, 1152, "gelu_tanh", "fc1", False), (4304, 1152, "none", "fc1-none", False), (1152, 4304, "none", "fc2+acc", True),
                                (4096, 1024, "gelu_erf", "ivit_fc1", False)]:
     a = torch.randn(M, K, device=dev).to(torch.bfloat16)
     w = (torch.randn(N, K, device=dev) * K ** -0.5).to(torch.bfloat16)
