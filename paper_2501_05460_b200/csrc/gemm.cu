@@ -76,7 +76,7 @@ EPD_DEVICE float rcpf(float x) {
 // the epilogue warps, two per SM sub-partition, latency-bound: profiles/r02/ab.txt).
 //
 // GELU-tanh, 0.5 x (1 + tanh u) with u = k0 (x + k1 x^3), written as x * sigma(2u):
-// e = 2^(-2 u(|x|) log2 e) and r = 1 / (1 + e) on the MUFU (ex2, rcp), then
+// e = 2^(-2 u(|x|) log2 e) and r = 1 / (1 + e) on the MUFU (ex2; one rcp per pair), then
 // phi = r for x >= 0 and e r for x < 0.
 template <int NP>
 EPD_DEVICE void gelu_tanh_chunk(float* x) {
@@ -92,7 +92,8 @@ EPD_DEVICE void gelu_tanh_chunk(float* x) {
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
     const float2 y = f2fma(a[p], f2s(1.f), f2s(1.f));
-    const float2 r = make_float2(rcpf(y.x), rcpf(y.y));
+    // both reciprocals from one MUFU op: 1/y0 = y1 / (y0 y1), 1/y1 = y0 / (y0 y1)
+    const float2 r = f2mul(f2s(rcpf(y.x * y.y)), make_float2(y.y, y.x));
     const float2 er = f2mul(a[p], r);
     const float2 xv = make_float2(x[2 * p], x[2 * p + 1]);
     const float2 g = f2mul(xv, make_float2(xv.x >= 0.f ? r.x : er.x, xv.y >= 0.f ? r.y : er.y));
@@ -552,8 +553,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
               const uint4 bv = bias_cur[g];
               const float2 b0 = unpack_bf16x2(bv.x), b1 = unpack_bf16x2(bv.y), b2 = unpack_bf16x2(bv.z),
                            b3 = unpack_bf16x2(bv.w);
-              xg[0] += b0.x; xg[1] += b0.y; xg[2] += b1.x; xg[3] += b1.y;
-              xg[4] += b2.x; xg[5] += b2.y; xg[6] += b3.x; xg[7] += b3.y;
+              const float2 bb[4] = {b0, b1, b2, b3};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {  // packed adds (FFMA2 with 1)
+                const float2 v = f2fma(make_float2(xg[2 * j], xg[2 * j + 1]), f2s(1.f), bb[j]);
+                xg[2 * j] = v.x;
+                xg[2 * j + 1] = v.y;
+              }
             }
           }
         }

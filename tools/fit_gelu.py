@@ -62,7 +62,8 @@ def emulate_tanh_rcp(x):
     a = (z * (f(-0.10294324159622192) * (z * z) + f(-2.302208185195923))).astype(np.float32)
     e = np.exp2(a.astype(np.float64)).astype(np.float32)
     y = (f(1) + e).astype(np.float32)
-    r = (f(1) / y).astype(np.float32)
+    yy = (y * np.roll(y, 1)).astype(np.float32)  # the pair product (neighbours stand in for the pair)
+    r = ((f(1) / yy).astype(np.float32) * np.roll(y, 1)).astype(np.float32)
     return (x * np.where(x >= 0, r, e * r)).astype(np.float32)
 
 

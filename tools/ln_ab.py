@@ -12,19 +12,19 @@ tag = Path(os.environ.get("EPD_LIB_PATH", "libepd.so")).stem
 dev = torch.device("cuda")
 res = []
 for rows, D in [(10240, 1152), (12300, 1024)]:
-    x = torch.randn(rows, D, device=dev)
+    xs = [torch.randn(rows, D, device=dev) for _ in range(4)]  # 4 x 47 MB rotate through the 126 MB L2
     g = torch.ones(D, device=dev, dtype=torch.bfloat16)
     y = torch.empty(rows, D, device=dev, dtype=torch.bfloat16)
-    for _ in range(5):
-        kernels.layernorm_f32(x, g, g, 1e-6, out=y)
+    for i in range(5):
+        kernels.layernorm_f32(xs[i % 4], g, g, 1e-6, out=y)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda._sleep(100_000_000)  # launches queue behind it: events time kernels, not the host
     s.record()
-    for _ in range(50):
-        kernels.layernorm_f32(x, g, g, 1e-6, out=y)
+    for i in range(48):
+        kernels.layernorm_f32(xs[i % 4], g, g, 1e-6, out=y)
     e.record()
     torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / 50
+    ms = s.elapsed_time(e) / 48
     res.append(f"{rows}x{D}: {ms * 1e3:6.1f} us {rows * D * 6 / ms / 1e6:6.0f} GB/s")
 print(f"{tag:6s} " + " | ".join(res))
