@@ -11,6 +11,7 @@ timeout 600 python bench.py --workload c4 --no-cpu-baseline > gpurun_out/r02/ben
 timeout 600 python bench.py --workload c4w --no-cpu-baseline > gpurun_out/r02/bench_c4w.log 2>&1
 timeout 600 python bench.py --workload c2i --no-cpu-baseline > gpurun_out/r02/bench_c2i.log 2>&1
 timeout 600 python bench.py --workload c2s --steps 5 > gpurun_out/r02/bench_c2s.log 2>&1
+timeout 600 python bench.py --workload c2p --steps 3 > gpurun_out/r02/bench_c2p.log 2>&1
 timeout 600 python bench.py --impl reference > gpurun_out/r02/bench_ref.log 2>&1
 EPD_BENCH_ONE_GPU=1 timeout 600 python bench.py --gpus 2 --steps 5 --no-prefill > gpurun_out/r02/bench_n2_onegpu.log 2>&1
 timeout 300 python tools/small_shard.py siglip 1,2,3,5,10 > gpurun_out/r02/small_shard.txt 2>&1
@@ -19,4 +20,5 @@ timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
 timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02/launches_c5.csv python tools/one_step.py internvit 13 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off --launch-skip 37 --launch-count 7 -o gpurun_out/r02/full_c2_layer python tools/one_step.py siglip 10 > gpurun_out/r02/ncu_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --profile-from-start off --launch-skip 33 --launch-count 7 -o gpurun_out/r02/full_c5_layer python tools/one_step.py internvit 13 > gpurun_out/r02/ncu_full5.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/ubench/xu_rate.cu -o /tmp/xu_rate && /tmp/xu_rate > gpurun_out/r02/xu_rate.txt 2>&1
 ls gpurun_out/r02
