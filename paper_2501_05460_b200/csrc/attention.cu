@@ -404,12 +404,19 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
         }
         for (int j = 0; j < nkb; ++j) {
           const int sv = (vc + j) % C::KVS;
-          for (int g = 0; g < x.nq; ++g) {
+          bool v_ok = false, k_ok = false;
+          uint32_t pending = (1u << x.nq) - 1u;
+          for (int n_served = 0; n_served < x.nq; ++n_served) {
+            const int g = __ffs(pending) - 1;
+            pending &= ~(1u << g);
             const int pb = 2 * g + (j & 1);
             mbar_wait(&p_ready[pb], (pr_ph >> pb) & 1);
             ATR(2, g, mit, j);
             pr_ph ^= 1u << pb;
-            if (g == 0) mbar_wait(&v_full[sv], ((vc + j) / C::KVS) & 1);
+            if (!v_ok) {
+              mbar_wait(&v_full[sv], ((vc + j) / C::KVS) & 1);
+              v_ok = true;
+            }
             tc_fence_after();
             const uint64_t vb = v_base0 + (uint64_t)((sv * C::V_AL) >> 4);
             const uint32_t od = tmem + C::o_col(g), pa = tmem + C::s_col(g, j & 1);
@@ -424,7 +431,10 @@ __global__ void __launch_bounds__(Cfg<DP, NQ>::THREADS, 1)
             if (j + 2 < nkb) {
               // S_g(j+2) overwrites P_g(j) only after PV_g(j) (in-order tensor pipe)
               const int ks = (kc + j + 2) % C::KS;
-              if (g == 0) mbar_wait(&k_full[ks], ((kc + j + 2) / C::KS) & 1);
+              if (!k_ok) {
+                mbar_wait(&k_full[ks], ((kc + j + 2) / C::KS) & 1);
+                k_ok = true;
+              }
               tc_fence_after();
               issue_s(g, j + 2, ks);
               ATR(3, g, mit, j);

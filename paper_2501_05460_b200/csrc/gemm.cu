@@ -144,6 +144,9 @@ enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS
 #endif
 
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
+#ifndef EPD_EPI_PERWARP
+#define EPD_EPI_PERWARP 1  // row kinds: one TMA box per warp (32 rows) instead of per 4-warp half
+#endif
 #ifndef EPD_GEMM_EPI_WARPS
 #define EPD_GEMM_EPI_WARPS 8  // epilogue warps: 8 = two column halves x 4 lane quarters; 4 = one half
 #endif
@@ -326,6 +329,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
                      const __grid_constant__ CUtensorMap tmO2, int M, int N, int K, const EpiParams ep,
                      const TileSched sched) {
   using Cfg = GemmCfg<BN, CG>;
+  constexpr bool kPerWarpStore = EPD_EPI_PERWARP && KIND != EK_HEADS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -628,8 +632,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         // the previous TMA store(s) must have finished reading the staging buffer
         // (double-buffering the bf16 chunks measured neutral)
         uint8_t* sbuf = stg;
-        if (leader) bulk_wait_read0();
-        named_bar(bar_id, 128);
+        if (kPerWarpStore) {  // each warp waits only for its own previous store
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+        } else {
+          if (leader) bulk_wait_read0();
+          named_bar(bar_id, 128);
+        }
         if (KIND == EK_ROWS_BF16 || KIND == EK_SWIGLU) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
@@ -668,6 +677,19 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           }
         }
         fence_proxy_async_smem();
+        if (kPerWarpStore) {
+          // the warp's 32 rows leave as their own TMA box (no cross-warp barrier per chunk)
+          __syncwarp();
+          if (lane == 0 && m0 + q * 32 < M) {
+            constexpr int slab = (KIND == EK_ROWS_F32 || KIND == EK_ACC_F32) ? 4096 : 2048;
+            uint8_t* wb = stg + q * slab;
+            if (KIND == EK_ROWS_BF16 || KIND == EK_ROWS_F32) tma_store_2d(&tmO0, wb, n, m0 + q * 32);
+            else if (KIND == EK_SWIGLU) tma_store_2d(&tmO0, wb, n / 2, m0 + q * 32);
+            else tma_reduce_add_2d(&tmO0, wb, n, m0 + q * 32);
+            bulk_commit();
+          }
+          continue;
+        }
         named_bar(bar_id, 128);
         if (leader) {
           if (KIND == EK_ROWS_BF16 || KIND == EK_ROWS_F32) {
@@ -699,7 +721,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         else mbar_arrive(&tempty[as]);
       }
     }
-    if (leader) bulk_wait_all0();
+    if (kPerWarpStore ? lane == 0 : leader) bulk_wait_all0();
   }
 
   tc_fence_before();
@@ -797,11 +819,11 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   if (rc) return rc;
   if (KIND == EK_ROWS_BF16 || KIND == EK_SWIGLU) {
     rc = make_tmap_2d(&t0, ep.out, (uint64_t)(KIND == EK_SWIGLU ? N / 2 : N), (uint64_t)M, (uint64_t)ep.ldo * 2,
-                      32, kBM, CU_TENSOR_MAP_SWIZZLE_64B);
+                      32, EPD_EPI_PERWARP ? 32 : kBM, CU_TENSOR_MAP_SWIZZLE_64B);
     t1 = t2 = t0;
   } else if (KIND == EK_ROWS_F32 || KIND == EK_ACC_F32) {
-    rc = make_tmap_2d_f32(&t0, ep.out_f, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 4, 32, kBM,
-                          CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = make_tmap_2d_f32(&t0, ep.out_f, (uint64_t)N, (uint64_t)M, (uint64_t)ep.ldo * 4, 32,
+                          EPD_EPI_PERWARP ? 32 : kBM, CU_TENSOR_MAP_SWIZZLE_128B);
     t1 = t2 = t0;
   } else {
     const uint64_t nb = (uint64_t)(M + ep.T - 1) / ep.T;
