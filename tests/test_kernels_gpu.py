@@ -113,6 +113,8 @@ def _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale, kv_heads=None, cau
     (2, 16, 1024, 1024, 72, 72, False, 1.0),   # SigLIP: packed 72-wide heads (Dp 80 reads the next head)
     (2, 16, 1024, 1024, 72, 80, False, 1.0),   # padded 80-wide heads
     (1, 16, 1025, 1025, 64, 64, False, 1.0),   # InternViT (CLS -> ragged last key block, rows cross images)
+    (2, 16, 1025, 1025, 64, 64, False, 1.0),   # ... two images: the 1-row tail goes to the CUDA-core row kernel
+    (3, 4, 133, 133, 72, 80, False, 4.0),      # 5 tail rows per image, padded heads, peaked scores
     (2, 28, 64, 1024, 128, 128, True, 1.0),    # MiniCPM resampler cross-attention (shared queries)
     (1, 1, 4, 16, 8, 8, True, 1.0),            # tiny
     (3, 2, 300, 200, 64, 64, False, 1.0),
