@@ -408,6 +408,10 @@ class EPDRuntime:
             if cmd["done"]:
                 break
             self._send(cmd["pre"], held, marks, s)
+            if self.is_coord and cmd["batch"]:
+                disp = self.stamps.mark(s)  # batch start: a text-only request's (empty) encode
+                for rid, _, _ in cmd["batch"]:
+                    marks[("disp", rid)] = disp
             self._encode(cmd["batch"], held, marks, s)
             if self.is_coord and open_loop and cmd["batch"] and s is not None:
                 enc_done = torch.cuda.Event()
@@ -473,10 +477,15 @@ class EPDRuntime:
                 m = allmarks[base_rank + k]
                 shards.append(ShardRecord(k, count, sec(m[("start", rid)]), sec(m[("end", rid)]),
                                           sec(st[marks[("xfer", rid, base_rank + k)]])))
+            rec.ep_transfer_end = sec(st[marks[("ep", rid)]])
+            if not shards:
+                # text-only request: one empty shard on worker 0 that starts with its batch and
+                # "transfers" at once (engine.py:589-590: shards [(0, 0)], no EP bytes)
+                t = sec(st[marks[("disp", rid)]])
+                shards = [ShardRecord(0, 0, t, t, t)]
             rec.shards = shards
             rec.encode_start = min(x.start for x in shards)
             rec.encode_end = max(x.end for x in shards)
-            rec.ep_transfer_end = sec(st[marks[("ep", rid)]])
             rec.prefill_start = sec(st[marks[("pre0", rid)]])
             rec.prefill_end = rec.first_token_time = sec(st[marks[("pre1", rid)]])
             rec.first_token = int(first_tok[rid].item())

@@ -15,7 +15,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-TILES = [3, 1, 4, 2, 5, 1, 2]
+TILES = [3, 1, 4, 0, 2, 5, 1, 2]  # request 3 is text-only (engine.py:589-590)
 T, D, BS = 16, 8, 16  # tokens per tile (one 16-token block), token width, block size
 
 
@@ -149,7 +149,7 @@ def _run(rank, world, scenario):
             want = _Encoder().encode(r.tiles, torch.empty(r.tiles.shape[0], T, D, dtype=torch.bfloat16))
             if not torch.equal(out["mm"][r.rid], want):
                 errs.append(f"request {r.rid}: MM tokens in the P-side blocks differ")
-            exp = [(k, c) for k, (_, c) in enumerate(shard_ranges(r.tiles.shape[0], rt.width)) if c]
+            exp = [(k, c) for k, (_, c) in enumerate(shard_ranges(r.tiles.shape[0], rt.width)) if c] or [(0, 0)]
             if [(s.worker, s.patches) for s in rec.shards] != exp:
                 errs.append(f"request {r.rid}: shards {rec.shards}")
             try:
@@ -158,7 +158,9 @@ def _run(rank, world, scenario):
                 errs.append(str(e))
         if rt.p.manager.used_blocks or any(m.used_blocks for m in rt.e_mms):
             errs.append("MM blocks leaked")
-        if scenario == "pwait" and out["ep_wait"] != [2, 4, 5, 6]:
+        # P side holds 6 tiles: batch (0,1,2) -> 2 waits; (3,4,5) -> text-only 3 reserves 0
+        # blocks, 5 waits; (6,7) -> 7 waits (_try_reserve_prefill, FIFO retries first)
+        if scenario == "pwait" and out["ep_wait"] != [2, 5, 7]:
             errs.append(f"ep_wait history {out['ep_wait']}")
         if scenario != "pwait" and out["ep_wait"]:
             errs.append(f"unexpected ep_wait {out['ep_wait']}")

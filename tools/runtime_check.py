@@ -27,7 +27,7 @@ ROOT = Path(__file__).resolve().parent.parent
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
-TILES = [3, 1, 4, 2, 5, 1, 2]
+TILES = [3, 1, 4, 0, 2, 5, 1, 2]  # request 3 is text-only (engine.py:589-590)
 
 
 def main() -> None:
@@ -76,7 +76,7 @@ def main() -> None:
                     errs.append(f"request {r.rid}: MM tokens in the P-side blocks differ from a direct encode")
                 if rec.first_token != int(tok.item()):
                     errs.append(f"request {r.rid}: first token {rec.first_token} vs direct {int(tok.item())}")
-                want = [(k, c) for k, (_, c) in enumerate(shard_ranges(r.tiles.shape[0], rt.width)) if c]
+                want = [(k, c) for k, (_, c) in enumerate(shard_ranges(r.tiles.shape[0], rt.width)) if c] or [(0, 0)]
                 if [(s.worker, s.patches) for s in rec.shards] != want:
                     errs.append(f"request {r.rid}: shards {rec.shards} vs {want}")
                 try:
@@ -98,11 +98,12 @@ def main() -> None:
                 errs.append(f"{scenario}: instances {got_inst}, expected {want_inst}")
         waited = out["ep_wait"]
         if scenario == "pwait":
-            # P pool of 6 tiles, batches of 3 (tiles 3 1 4 | 2 5 1 | 2): r2 waits (3+1+4 > 6);
-            # round 2 sends r2 first, then r3 fits and r4, r5 wait (each tries on its own,
-            # engine.py:381-383); round 3 sends r4, r5 and r6 waits (engine.py:680-685)
-            if waited != [2, 4, 5, 6]:
-                errs.append(f"pwait: ep_wait history {waited}, expected [2, 4, 5, 6]")
+            # P pool of 6 tiles, batches of 3 (tiles 3 1 4 | 0 2 5 | 1 2): r2 waits (3+1+4 > 6);
+            # round 2 sends r2 first, then text-only r3 reserves 0 blocks, r4 fits and r5 waits
+            # (each tries on its own, engine.py:381-383); round 3 sends r5, r6 fits, r7 waits
+            # (engine.py:680-685)
+            if waited != [2, 5, 7]:
+                errs.append(f"pwait: ep_wait history {waited}, expected [2, 5, 7]")
         elif waited:
             errs.append(f"{scenario}: unexpected ep_wait {waited}")
         encs = sorted({round(r.encode_start, 9) for r in out["records"].values()})
