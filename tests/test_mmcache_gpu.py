@@ -109,6 +109,32 @@ def test_cached_stage_bit_exact(cuda):
     assert torch.equal(r2.tokens, direct)
 
 
+@pytest.mark.parametrize("cached", [False, True])
+def test_stage_text_only_request(cuda, cached):
+    """A request with no images (engine.py:589-590: text-only) encodes nothing, returns an
+    empty packed buffer, and leaves the stage (and its cache) usable for the next request."""
+    from paper_2501_05460_b200.configs import SEED, TINY_VIT
+    from paper_2501_05460_b200.encoder import VisionEncoder
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    from paper_2501_05460_b200.stage import EncodeStage, tiles_for_request
+    cfg = TINY_VIT
+    enc = VisionEncoder(cfg, cuda, max_tiles=8)
+    cache = MMTokenCache(16, cfg.out_tokens, cfg.out_dim, cuda) if cached else None
+    st = EncodeStage(enc, cuda, cache=cache)
+    empty = tiles_for_request(0, cfg, SEED)
+    r0 = st.process(empty.pin_memory())
+    assert r0.encoded_tiles == 0 and tuple(r0.tokens.shape) == (0, cfg.out_tokens, cfg.out_dim)
+    tiles = tiles_for_request(5, cfg, SEED)
+    r1 = st.process(tiles.pin_memory())
+    r2 = st.process(None, tiles_dev=empty.to(cuda))
+    torch.cuda.synchronize()
+    assert r2.tokens.shape[0] == 0
+    assert torch.equal(r1.tokens, enc.encode(tiles.to(cuda)))
+    if cached:
+        assert r0.cache_counts == {"hit": 0, "miss": 0, "dup": 0} and len(cache) == 5
+        cache.check()
+
+
 def test_kv_pack_unpack_and_local_handoff(cuda):
     from paper_2501_05460_b200.handoff import PagedKVCache, kv_handoff
     p = PagedKVCache(num_layers=4, kv_heads=2, head_dim=16, block_size=16, num_blocks=40, device=cuda)

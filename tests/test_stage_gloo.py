@@ -149,7 +149,7 @@ def _batch_worker(rank, world, port, ns, use_comm, q):
 
 
 @pytest.mark.parametrize("world,ns,use_comm", [(2, (10, 10), False), (3, (10, 13, 1), False), (3, (10, 10, 10), True),
-                                               (2, (1, 5), True)])
+                                               (2, (1, 5), True), (3, (4, 0, 2), False), (2, (0, 3, 0), True)])
 def test_process_batch_gloo(world, ns, use_comm):
     """EncodeStage.process_batch: every request IRP-sharded over all ranks from worker 0, one
     encoder call per rank for all its shards, the batch packed request after request on the
