@@ -44,6 +44,32 @@ def test_cache_sequence_matches_oracle(cuda):
     cache.check()
 
 
+def test_cache_capacity_exceeded_leaves_state_untouched(cuda):
+    """A request with more distinct tiles than entries raises CapacityExceeded (the oracle's
+    rule) without touching the cache; the next requests classify as from that state."""
+    from paper_2501_05460_b200._lib import CapacityExceeded as DevCapacityExceeded
+    from paper_2501_05460_b200.mmcache import MMTokenCache
+    from oracle.mmcache import CapacityExceeded
+    rng = np.random.default_rng(5)
+    pool = rng.integers(0, 256, (6, 8 * 8 * 3), dtype=np.uint8)
+    cache = MMTokenCache(capacity=2, tokens_per_tile=4, hidden=8, device=cuda, secret=0)
+    oracle = MMCacheOracle(2)
+    for ids in ([0], [0, 1, 2], [1, 1, 0], [3, 4, 5], [2, 3], [2, 2, 2, 2]):
+        tiles = torch.from_numpy(pool[ids]).to(cuda)
+        keys = [content_hash(pool[i], (0, 0)) for i in ids]
+        try:
+            expect = oracle.process(keys)
+        except CapacityExceeded:
+            with pytest.raises(DevCapacityExceeded):
+                cache.plan(cache.hash(tiles))
+            assert len(cache) == len(oracle)
+            continue
+        plan = cache.plan(cache.hash(tiles))
+        assert list(zip(plan.kinds, [int(e) for e in plan.entries])) == expect, ids
+        assert plan.victims == oracle.last_victims
+    cache.check()
+
+
 def test_keyed_hash_matches_oracle_and_differs_per_secret(cuda):
     from paper_2501_05460_b200.mmcache import MMTokenCache, hash_tiles
     rng = np.random.default_rng(4)
