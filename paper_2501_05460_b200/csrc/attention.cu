@@ -100,12 +100,13 @@ __device__ uint32_t g_attn_trace[8][8][48];
   do {                         \
   } while (0)
 #endif
+// Pairs (of every 8) whose exponentials run on the FMA pipe, per head-dim padding. Same-box
+// A/B (profiles/r02/ab.txt, tools/attn_ab.py): SigLIP (Dp 80) 2/8 74.7 us, 3/8 73.7 us, 4/8
+// 78.3 us; InternViT (Dp 64) 2/8 97.3 us, 3/8 95.3 us, 4/8 103 us.
 #ifndef EPD_POLY_EIGHTHS
-#define EPD_POLY_EIGHTHS 2  // pairs (of every 8) whose exponentials run on the FMA pipe
+#define EPD_POLY_EIGHTHS 3
 #endif
 #ifndef EPD_POLY_EIGHTHS_64
-// head dim 64 (InternViT): 3/8 measured 1.5 % faster on the 12-tile encode (same box,
-// alternating runs); SigLIP (head dim 72) showed no difference, so it keeps 2/8
 #define EPD_POLY_EIGHTHS_64 3
 #endif
 
