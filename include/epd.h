@@ -290,6 +290,13 @@ epd_status_t epd_set_gemm_cta_group(int32_t policy);
 epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
                                 int32_t K, const void* bias, const void* lscale, float* h, int32_t ldh, int32_t bn,
                                 void* stream);
+/* The same, allowed to split K over up to max_split work items per output tile when the tiles
+ * alone leave SMs idle (small M, long K: the LLM prefill's down / O projections). The splits
+ * add into h in a fixed order, so results are run-to-run deterministic, but the split count
+ * follows M: not batch invariant (the encoder path never splits). */
+epd_status_t epd_linear_acc_f32_split(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M,
+                                      int32_t N, int32_t K, const void* bias, const void* lscale, float* h,
+                                      int32_t ldh, int32_t bn, int32_t max_split, void* stream);
 /* Projection straight into attention layouts: column n of A W^T + bias (+ resid[row % r_mod])
  * splits into section s = n / sec_cols, head h, dim d (head dim padded to Dp); row = b*T + t.
  * Section s writes out_s[((b*H + h)*T + t)*Dp + d], or, when bit s of trans_mask is set,

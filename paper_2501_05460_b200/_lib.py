@@ -102,6 +102,7 @@ _SIGS = {
                                _vp, _i32, _i32, _vp]),
     "epd_set_gemm_cta_group": (_i32, [_i32]),
     "epd_linear_acc_f32": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _vp]),
+    "epd_linear_acc_f32_split": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _i32, _i32, _vp]),
     "epd_linear_heads_bf16": (_i32, [_vp, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _i32, _i32,
                                      _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
     "epd_attention_bf16": (_i32, [_vp, _i32, _vp, _i32, _vp, _i32, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,

@@ -540,7 +540,14 @@ epd_status_t epd_set_gemm_cta_group(int32_t policy) {
 epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M, int32_t N,
                                 int32_t K, const void* bias, const void* lscale, float* h, int32_t ldh, int32_t bn,
                                 void* stream) {
+  return epd_linear_acc_f32_split(A, lda, W, ldw, M, N, K, bias, lscale, h, ldh, bn, 0, stream);
+}
+
+epd_status_t epd_linear_acc_f32_split(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M,
+                                      int32_t N, int32_t K, const void* bias, const void* lscale, float* h,
+                                      int32_t ldh, int32_t bn, int32_t max_split, void* stream) {
   if (M <= 0 || N <= 0 || K <= 0 || !h) return fail(EPD_ERR_VALUE, "linear_acc: empty shape or null output");
+  if (max_split < 0 || max_split > 16) return fail(EPD_ERR_VALUE, "linear_acc: max_split must be 0..16");
   if (ldh % 4 || (reinterpret_cast<uintptr_t>(h) & 15)) return fail(EPD_ERR_VALUE, "linear_acc: h must be 16-byte aligned");
   epd::EpiParams ep;
   ep.bias = reinterpret_cast<const epd::bf16*>(bias);
@@ -549,6 +556,7 @@ epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32
   ep.out_f = h;
   ep.ldr = ldh;
   ep.ldo = ldh;
+  ep.max_split = max_split;
   int rc = epd::gemm_bf16(reinterpret_cast<const epd::bf16*>(A), lda, reinterpret_cast<const epd::bf16*>(W), ldw,
                           M, N, K, ep, S(stream), bn);
   return cuda_status(rc, "linear_acc_f32");

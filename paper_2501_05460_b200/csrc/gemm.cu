@@ -242,6 +242,15 @@ EPD_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"
 EPD_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 EPD_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 EPD_DEVICE void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+EPD_DEVICE int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+EPD_DEVICE void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+EPD_DEVICE void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 EPD_DEVICE void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
@@ -375,14 +384,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   pdl_trigger();
   pdl_wait();  // A, the residual stream and the outputs belong to the previous kernels
 
-  const int num_tiles = sched.total;
   const int nk = (K + kBK - 1) / kBK;
+  // split-K (fp32 reduce-add only): work item = (tile, split), the splits of a tile adjacent
+  const int nsplit = (KIND == EK_ACC_F32 && ep.ksplit > 1) ? ep.ksplit : 1;
+  const int num_tiles = sched.total * nsplit;
 
   if (warp == 0) {
     // TMA producer: the whole warp walks the schedule (uniform operands), one elected lane issues
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = pid; tile < num_tiles; tile += npid) {
+    for (int item = pid; item < num_tiles; item += npid) {
+      const int tile = item / nsplit, sp = item - tile * nsplit;
+      const int kb_lo = sp * nk / nsplit, kb_hi = (sp + 1) * nk / nsplit;
       const TileAt x = tile_at(sched, tile, BN);
       const int m0 = x.mt * (kBM * CL) + crank_full * kBM;
       // each CTA of a pair holds half of the tile's B rows; a half-width tile loads only
@@ -391,7 +404,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       const bool hw = x.w != BN;
       const CUtensorMap* tb = hw ? &tmBh : &tmB;
       const uint32_t stage_bytes = Cfg::A_BYTES + (hw ? Cfg::B_BYTES / 2 : Cfg::B_BYTES);
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = kb_lo; kb < kb_hi; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
 #if EPD_GEMM_EXP == 1  // experiment: no operand loads (MMA + epilogue alone)
         if (elect_one() && crank == 0) mbar_arrive(&full[stage]);
@@ -427,14 +440,16 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
+      for (int item = pid; item < num_tiles; item += npid, ++local) {
+        const int tile = item / nsplit, sp = item - tile * nsplit;
+        const int kb_lo = sp * nk / nsplit, kb_hi = (sp + 1) * nk / nsplit;
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         const uint32_t idesc = tile_at(sched, tile, BN).w == BN ? idesc_full : idesc_half;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t dtmem = tmem_base + as * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ao = a0 + (uint64_t)((stage * Cfg::A_BYTES) >> 4);
@@ -442,8 +457,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           if (elect_one()) {
 #pragma unroll
             for (int k = 0; k < (EPD_GEMM_EXP == 2 ? 0 : kBK / 16); ++k) {  // EXP 2: no MMAs
-              if (CG == 2) umma_bf16_pair(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
-              else umma_bf16(dtmem, ao + 2 * k, bo + 2 * k, idesc, (kb | k) != 0);
+              if (CG == 2) umma_bf16_pair(dtmem, ao + 2 * k, bo + 2 * k, idesc, kb != kb_lo || k != 0);
+              else umma_bf16(dtmem, ao + 2 * k, bo + 2 * k, idesc, kb != kb_lo || k != 0);
             }
             if (CL == 4) tc_commit_pair_mask(&empty[stage], 0xF);  // the stage is free in all 4 CTAs
             else if (CG == 2) tc_commit_pair(&empty[stage]);
@@ -470,7 +485,13 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     const int bar_id = 1 + half;
     const uint32_t tempty_leader = mapa_rank(smem_u32(&tempty[0]), crank_full & ~1u);  // pair leader
     int local = 0;
-    for (int tile = pid; tile < num_tiles; tile += npid, ++local) {
+    for (int item = pid; item < num_tiles; item += npid, ++local) {
+      const int tile = item / nsplit, sp = item - tile * nsplit;
+      const bf16* bias_p = sp == 0 ? ep.bias : nullptr;  // the first split adds the bias
+      // split-K: this warp's slab of the tile is reduce-added in split order; the counter
+      // holds the number of splits done (reset to 0 by the last one, so graph replays start clean)
+      int* slab_flag = nsplit > 1 ? ep.split_flags + (size_t)tile * (kEpiWarps * CG) + crank * kEpiWarps + (warp - 2)
+                                  : nullptr;
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       const TileAt x = tile_at(sched, tile, BN);
@@ -502,11 +523,18 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         for (int g = 0; g < 4; ++g) {
           const int col = n + g * 8;
           const bool ok = KIND != EK_SWIGLU && col < N;
-          bias_nx[g] = ok && ep.bias ? *reinterpret_cast<const uint4*>(ep.bias + col) : make_uint4(0, 0, 0, 0);
+          bias_nx[g] = ok && bias_p ? *reinterpret_cast<const uint4*>(bias_p + col) : make_uint4(0, 0, 0, 0);
           ls_nx[g] = ok && ep.lscale ? *reinterpret_cast<const uint4*>(ep.lscale + col) : make_uint4(0, 0, 0, 0);
         }
       };
       prefetch_vec(n0 + half * hw);
+      if (nsplit > 1 && sp > 0) {  // the previous split's adds into this slab come first
+        if (lane == 0) {
+          while (ld_acquire_gpu(slab_flag) < sp) __nanosleep(64);
+          fence_proxy_async_global();
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
 #pragma unroll 1
@@ -553,7 +581,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
           const int col = n + g * 8;
           float* xg = x + g * 8;
           if (col < N) {
-            if (ep.bias) {
+            if (bias_p) {
               const uint4 bv = bias_cur[g];
               const float2 b0 = unpack_bf16x2(bv.x), b1 = unpack_bf16x2(bv.y), b2 = unpack_bf16x2(bv.z),
                            b3 = unpack_bf16x2(bv.w);
@@ -720,6 +748,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         if (CG == 2) mbar_arrive_cluster(tempty_leader + as * 8);
         else mbar_arrive(&tempty[as]);
       }
+      if (nsplit > 1) {
+        if (lane == 0) {
+          bulk_wait_all0();  // this warp's reduce-adds of the item are complete in memory
+          fence_proxy_async_global();
+          st_release_gpu(slab_flag, sp + 1 == nsplit ? 0 : sp + 1);
+        }
+        __syncwarp();
+      }
     }
     if (kPerWarpStore ? lane == 0 : leader) bulk_wait_all0();
   }
@@ -853,7 +889,8 @@ int launch(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K, 
   const int cap = cluster_units(CL);
   const TileSched sched = make_sched(M, N, BN, CL, KIND != EK_HEADS, cap);
   int units = cap;
-  if (sched.total < units) units = sched.total;
+  const int items = sched.total * (KIND == EK_ACC_F32 && ep.ksplit > 1 ? ep.ksplit : 1);
+  if (items < units) units = items;
   const int rc2 = launch_kernel(gemm_bf16_kernel<BN, KIND, CG, CL>, dim3(units * CL), dim3(Cfg::THREADS),
                                 Cfg::SMEM, stream, CL, ta, tb, tbh, t0, t1, t2, M, N, K, ep, sched);
   if (rc2) return rc2;
@@ -878,6 +915,25 @@ int g_cta_group_policy = 0;  // 0 auto; else the cluster size: 1 single CTAs, 2 
 
 void set_gemm_cta_group(int policy) { g_cta_group_policy = policy; }
 
+// Zeroed split-K progress counters (grown, never freed: queued kernels may still use an old
+// buffer). Not allocated during stream capture -- the GEMM then runs unsplit.
+static int* split_flags(int need, cudaStream_t stream) {
+  static int* buf[16] = {};
+  static int cap[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  if (buf[dev] && need <= cap[dev]) return buf[dev];
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return nullptr;
+  const int n = need < (1 << 16) ? (1 << 16) : need;
+  int* p = nullptr;
+  if (cudaMalloc(&p, (size_t)n * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  if (cudaMemsetAsync(p, 0, (size_t)n * sizeof(int), stream) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  buf[dev] = p;
+  cap[dev] = n;
+  return p;
+}
+
 int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int K,
               const EpiParams& ep, cudaStream_t stream, int bn_hint) {
   if (M <= 0 || N <= 0 || K <= 0) return 1001;
@@ -890,19 +946,33 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
   int cl = g_cta_group_policy ? g_cta_group_policy : (M > 256 ? (M >= EPD_CL4_MIN_M ? 4 : 2) : 1);
   if (cl != 1 && cl != 2 && cl != 4) return 1001;
   if (ep.mode == EPI_HEADS && cl == 4) cl = 2;
-  int bn = bn_hint;
-  if (bn == 0) {
+  int bn = bn_hint, nsplit = 1;
+  // split-K only where the caller allows it (fp32 reduce-add, per-warp stores)
+  const bool can_split = ep.max_split > 1 && ep.out_f && ep.resid_f && ep.mode != EPI_HEADS && EPD_EPI_PERWARP;
+  if (bn == 0 || can_split) {
     // Wide tiles amortise the epilogue and operand traffic best; step down only when the
-    // schedule's rounds (half tiles included) favour a narrower tile.
+    // schedule's rounds (half tiles included) favour a narrower tile. With split-K allowed,
+    // S splits of every tile run as separate work items: rounds ceil(S T / U) of 1/S the
+    // K each, plus ~8 % per extra split for the ordered epilogue chain.
     double best = 1e30;
     const int cands[3] = {256, 192, 128};
+    const int nkb = (K + kBK - 1) / kBK;
     for (int i = 0; i < 3; ++i) {
       const int c = cands[i];
+      if (bn_hint && c != bn_hint) continue;
       if (cl > 1 && c == 128) continue;
       const int u = cluster_units(cl);
-      const double rounds = sched_rounds(make_sched(M, N, c, cl, ep.mode != EPI_HEADS, u), u);
-      const double cost = rounds * c * (c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0));
-      if (cost < best) { best = cost; bn = c; }
+      const TileSched t = make_sched(M, N, c, cl, ep.mode != EPI_HEADS, u);
+      const double eff = c == 128 ? 1.35 : (c == 192 ? 1.12 : 1.0);
+      for (int sp = 1; sp <= (can_split ? ep.max_split : 1); ++sp) {
+        // >= 64 k-blocks (4096 of K) per split: below that the ordered fp32 reduce-add chain
+        // costs more than the idle pairs (tools/split_ab.py: the 662 x 3584 x 3584 O
+        // projection 26 -> 37 us at 3 splits; the 18944-deep down projection 97 -> 87 us)
+        if (sp > 1 && nkb / sp < 64) break;
+        const double rounds = sp == 1 ? sched_rounds(t, u) : (double)((t.total * sp + u - 1) / u) / sp;
+        const double cost = rounds * c * eff * (1.0 + 0.08 * (sp - 1));
+        if (cost < best - 1e-9) { best = cost; bn = c; nsplit = sp; }
+      }
     }
   }
   if (ep.act == ACT_SWIGLU) {
@@ -929,24 +999,39 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
     if (!ep.out || ep.resid_f) return 1005;
     kind = EK_ROWS_BF16;
   }
+  static const int force_split = [] {
+    const char* e = getenv("EPD_GEMM_SPLIT");  // A/B override of the split count
+    return e ? atoi(e) : 0;
+  }();
+  if (can_split && force_split > 0) nsplit = force_split;
+  EpiParams epx = ep;
+  epx.ksplit = 1;
+  epx.split_flags = nullptr;
+  if (nsplit > 1 && kind == EK_ACC_F32) {
+    const int u = cluster_units(cl);
+    const TileSched t = make_sched(M, N, bn, cl, true, u);
+    epx.split_flags = split_flags(t.total * kEpiWarps * (cl == 1 ? 1 : 2), stream);
+    if (epx.split_flags) epx.ksplit = nsplit;
+  }
+  const EpiParams& epl = epx;
   if (cl == 4) {
     switch (bn) {
-      case 256: return launch_kind<256, 4>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-      case 192: return launch_kind<192, 4>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+      case 256: return launch_kind<256, 4>(kind, A, lda, B, ldb, M, N, K, epl, stream);
+      case 192: return launch_kind<192, 4>(kind, A, lda, B, ldb, M, N, K, epl, stream);
       default: return 1004;
     }
   }
   if (cl == 2) {
     switch (bn) {
-      case 256: return launch_kind<256, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-      case 192: return launch_kind<192, 2>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+      case 256: return launch_kind<256, 2>(kind, A, lda, B, ldb, M, N, K, epl, stream);
+      case 192: return launch_kind<192, 2>(kind, A, lda, B, ldb, M, N, K, epl, stream);
       default: return 1004;
     }
   }
   switch (bn) {
-    case 256: return launch_kind<256, 1>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-    case 192: return launch_kind<192, 1>(kind, A, lda, B, ldb, M, N, K, ep, stream);
-    case 128: return launch_kind<128, 1>(kind, A, lda, B, ldb, M, N, K, ep, stream);
+    case 256: return launch_kind<256, 1>(kind, A, lda, B, ldb, M, N, K, epl, stream);
+    case 192: return launch_kind<192, 1>(kind, A, lda, B, ldb, M, N, K, epl, stream);
+    case 128: return launch_kind<128, 1>(kind, A, lda, B, ldb, M, N, K, epl, stream);
     default: return 1004;
   }
 }

@@ -39,6 +39,13 @@ struct EpiParams {
   int H = 0, Dp = 0, T = 0, Tpad = 0, sec_cols = 0;
   bf16* sec_out[3] = {nullptr, nullptr, nullptr};
   int sec_trans[3] = {0, 0, 0};
+  // fp32 reduce-add only: allow splitting K over up to max_split work items per output tile
+  // (chosen when the tiles alone leave SMs idle). The splits add into the output in a fixed
+  // order (run-to-run deterministic), but the split count depends on M, so results are not
+  // batch invariant -- the encoder never sets it.
+  int max_split = 0;
+  int ksplit = 1;        // internal: chosen split count
+  int* split_flags = nullptr;  // internal: per (tile, epilogue warp) progress counters
 };
 
 // Returns a cudaError_t-compatible code (0 = success); 1000+ for argument errors.

@@ -46,15 +46,16 @@ def linear(a: torch.Tensor, w: torch.Tensor, bias: torch.Tensor | None = None, a
 
 
 def linear_acc(a: torch.Tensor, w: torch.Tensor, h: torch.Tensor, bias: torch.Tensor | None = None,
-               lscale: torch.Tensor | None = None, bn: int = 0) -> torch.Tensor:
-    """h (fp32, in place) += lscale * (a @ w.T + bias)."""
+               lscale: torch.Tensor | None = None, bn: int = 0, max_split: int = 0) -> torch.Tensor:
+    """h (fp32, in place) += lscale * (a @ w.T + bias). ``max_split`` > 1 lets the GEMM split
+    K (deterministic order, not batch invariant; for the LLM prefill)."""
     _need_cuda(a, w, h, bias, lscale)
     if h.dtype != torch.float32:
         raise ValueError("h must be fp32")
     M, K = a.shape
     N = w.shape[0]
-    call("epd_linear_acc_f32", a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K, _ptr(bias),
-         _ptr(lscale), h.data_ptr(), h.stride(0), bn, _stream(a))
+    call("epd_linear_acc_f32_split", a.data_ptr(), a.stride(0), w.data_ptr(), w.stride(0), M, N, K, _ptr(bias),
+         _ptr(lscale), h.data_ptr(), h.stride(0), bn, max_split, _stream(a))
     return h
 
 

@@ -16,6 +16,7 @@ CUDA graph per prompt shape. K/V land in the paged pool that the P->D handoff
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -64,6 +65,11 @@ class LLMConfig:
 QWEN2_7B = LLMConfig("qwen2-7b", 28, 3584, 28, 4, 128, 18944, 152064, 1e6, 1e-6, True, MINICPM_V26)
 INTERNLM25_7B = LLMConfig("internlm2.5-7b", 32, 4096, 32, 8, 128, 14336, 92553, 1e6, 1e-5, False, INTERNVL2_8B)
 TINY_LLM = LLMConfig("tiny-llm", 2, 256, 4, 2, 64, 512, 1000, 1e4, 1e-6, True)
+
+# The O and down projections run at M = prompt length (662 tokens for C2): their output tiles
+# alone leave CTA pairs idle, so they may split K (epd_linear_acc_f32_split; deterministic
+# order). The encoder never splits (its results are batch invariant).
+PREFILL_MAX_SPLIT = int(os.environ.get("EPD_PREFILL_MAX_SPLIT", "8"))  # A/B: 0 = never split
 
 
 def llm_weights(cfg: LLMConfig, device, seed: int = SEED) -> dict[str, torch.Tensor]:
@@ -148,10 +154,10 @@ class Prefiller:
                 kernels.kv_write_paged(qkv[:, Hq * hd:], Hk * hd, Hk * hd, self.blocks_in, kv.block_size, kv.pool, i)
             kernels.attention(qkv[:, :Hq * hd], qkv[:, Hq * hd:(Hq + Hk) * hd], qkv[:, (Hq + Hk) * hd:], 1, Hq, T, T,
                               hd, hd ** -0.5, out=attn, kv_heads=Hk, causal=True)
-            kernels.linear_acc(attn, w[p + "wo"], h)
+            kernels.linear_acc(attn, w[p + "wo"], h, max_split=PREFILL_MAX_SPLIT)
             kernels.rmsnorm_f32(h, w[p + "mlp_norm"], cfg.rms_eps, out=xn)
             kernels.linear(xn, w[p + "wgu"], act="swiglu", out=act)  # silu(gate) * up in the epilogue
-            kernels.linear_acc(act, w[p + "wd"], h)
+            kernels.linear_acc(act, w[p + "wd"], h, max_split=PREFILL_MAX_SPLIT)
         kernels.rmsnorm_f32(h[T - 1:T], w["final_norm"], cfg.rms_eps, out=xn[:1])
         kernels.linear(xn[:1], w["lm_head"], out=self.logits)
         kernels.argmax(self.logits[0, :cfg.vocab], out=self.token)

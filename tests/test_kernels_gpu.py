@@ -88,6 +88,46 @@ def test_linear_acc_f32(cuda, M, N, K, bn, ls):
     assert relerr(h, ref) <= 2e-3
 
 
+@pytest.mark.parametrize("M,N,K,ls", [(662, 3584, 18944, False),   # Qwen2-7B down projection (C2 prefill)
+                                        (662, 3584, 3584, True),      # Qwen2-7B O projection
+                                        (3350, 4096, 14336, False),   # InternLM2.5-7B down (C5 prefill)
+                                        (300, 1024, 8192, False)])
+def test_linear_acc_split_k(cuda, M, N, K, ls):
+    """Split-K reduce-add (LLM prefill): matches the fp32 reference, is bit-identical across
+    runs (the splits add in a fixed order) and across CUDA-graph replays (the per-slab
+    counters reset themselves), and agrees with the unsplit GEMM to fp32 rounding."""
+    from paper_2501_05460_b200 import kernels
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    a = _bf(M, K, gen=g)
+    w = _bf(N, K, scale=K ** -0.5, gen=g)
+    b = _bf(N, gen=g)
+    s = _bf(N, scale=0.1, gen=g) if ls else None
+    h0 = torch.randn(M, N, generator=g, device=cuda)
+    ref = h0.clone() + (a.float() @ w.float().t() + b.float()) * (s.float() if ls else 1.0)
+    outs = []
+    for _ in range(3):
+        h = h0.clone()
+        kernels.linear_acc(a, w, h, bias=b, lscale=s, max_split=8)
+        outs.append(h)
+    h1 = h0.clone()
+    kernels.linear_acc(a, w, h1, bias=b, lscale=s)  # unsplit
+    hg = h0.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        kernels.linear_acc(a, w, hg, bias=b, lscale=s, max_split=8)
+    graphs = []
+    for _ in range(3):
+        hg.copy_(h0)
+        graph.replay()
+        torch.cuda.synchronize()
+        graphs.append(hg.clone())
+    torch.cuda.synchronize()
+    assert relerr(outs[0], ref) <= 2e-3
+    assert all(torch.equal(o, outs[0]) for o in outs[1:])
+    assert all(torch.equal(x, outs[0]) for x in graphs)
+    assert (outs[0] - h1).abs().max().item() <= 1e-3 * ref.abs().max().item()
+
+
 def _attn_ref(q, k, v, B, H, Tq, Tk, Dv, hs, q_shared, scale, kv_heads=None, causal=False):
     """fp32 reference on the row-major layout (head h = columns [h*hs, h*hs + Dv))."""
     Hk = kv_heads or H

@@ -1,7 +1,5 @@
 # scratch GPU script for the current A/B round (overwritten per experiment)
-mkdir -p gpurun_out/ab8
-EPD_LIB_PATH=ab/s1.so timeout 300 python -m pytest tests/test_kernels_gpu.py -x -q -k "attention" > gpurun_out/ab8/tests.txt 2>&1
-echo "tests rc=$?" >> gpurun_out/ab8/tests.txt
-if grep -q "passed" gpurun_out/ab8/tests.txt && ! grep -q "failed" gpurun_out/ab8/tests.txt; then
-for r in 1 2 3; do for v in s0 s1; do EPD_LIB_PATH=ab/$v.so timeout 120 python tools/attn_ab.py; done; done > gpurun_out/ab8/attn.txt 2>&1
-fi
+mkdir -p gpurun_out/ab10
+timeout 600 python -m pytest tests/test_kernels_gpu.py -x -q -k "linear_acc" > gpurun_out/ab10/tests.txt 2>&1
+timeout 120 python tools/split_ab.py >> gpurun_out/ab10/tests.txt 2>&1
+for r in 1 2 3; do for sp in 0 8; do echo "split $sp"; EPD_PREFILL_MAX_SPLIT=$sp timeout 300 python tools/measure_prefill_latency.py gpurun_out/ab10/pl_$sp.json 2>&1 | grep -E " 662 | 3350 "; done; done > gpurun_out/ab10/prefill.txt 2>&1
