@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       const bf16* bias_p = sp == 0 ? ep.bias : nullptr;  // the first split adds the bias
       // split-K: this warp's slab of the tile is reduce-added in split order; the counter
       // holds the number of splits done (reset to 0 by the last one, so graph replays start clean)
-      int* slab_flag = nsplit > 1 ? ep.split_flags + (size_t)tile * (kEpiWarps * CG) + crank * kEpiWarps + (warp - 2)
+      int* slab_flag = nsplit > 1 ? ep.split_flags + (size_t)tile * (kEpiWarps * CL) + crank_full * kEpiWarps + (warp - 2)
                                   : nullptr;
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
@@ -1010,7 +1010,7 @@ int gemm_bf16(const bf16* A, int lda, const bf16* B, int ldb, int M, int N, int 
   if (nsplit > 1 && kind == EK_ACC_F32) {
     const int u = cluster_units(cl);
     const TileSched t = make_sched(M, N, bn, cl, true, u);
-    epx.split_flags = split_flags(t.total * kEpiWarps * (cl == 1 ? 1 : 2), stream);
+    epx.split_flags = split_flags(t.total * kEpiWarps * cl, stream);
     if (epx.split_flags) epx.ksplit = nsplit;
   }
   const EpiParams& epl = epx;
