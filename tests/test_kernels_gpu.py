@@ -88,11 +88,13 @@ def test_linear_acc_f32(cuda, M, N, K, bn, ls):
     assert relerr(h, ref) <= 2e-3
 
 
-@pytest.mark.parametrize("M,N,K,ls", [(662, 3584, 18944, False),   # Qwen2-7B down projection (C2 prefill)
-                                        (662, 3584, 3584, True),      # Qwen2-7B O projection
-                                        (3350, 4096, 14336, False),   # InternLM2.5-7B down (C5 prefill)
-                                        (300, 1024, 8192, False)])
-def test_linear_acc_split_k(cuda, M, N, K, ls):
+@pytest.mark.parametrize("M,N,K,ls,policy", [(662, 3584, 18944, False, 0),   # Qwen2-7B down projection (C2 prefill)
+                                               (662, 3584, 3584, True, 0),      # Qwen2-7B O projection
+                                               (3350, 4096, 14336, False, 0),   # InternLM2.5-7B down (C5 prefill)
+                                               (300, 1024, 8192, False, 0),
+                                               (662, 3584, 18944, True, 4),     # clusters of 4 (forced policy)
+                                               (300, 1024, 8192, False, 1)])    # single-CTA tiles
+def test_linear_acc_split_k(cuda, M, N, K, ls, policy):
     """Split-K reduce-add (LLM prefill): matches the fp32 reference, is bit-identical across
     runs (the splits add in a fixed order) and across CUDA-graph replays (the per-slab
     counters reset themselves), and agrees with the unsplit GEMM to fp32 rounding."""
@@ -104,6 +106,16 @@ def test_linear_acc_split_k(cuda, M, N, K, ls):
     s = _bf(N, scale=0.1, gen=g) if ls else None
     h0 = torch.randn(M, N, generator=g, device=cuda)
     ref = h0.clone() + (a.float() @ w.float().t() + b.float()) * (s.float() if ls else 1.0)
+    from paper_2501_05460_b200._lib import call
+    call("epd_set_gemm_cta_group", policy)
+    try:
+        _split_k_checks(cuda, a, w, b, s, h0, ref)
+    finally:
+        call("epd_set_gemm_cta_group", 0)
+
+
+def _split_k_checks(cuda, a, w, b, s, h0, ref):
+    from paper_2501_05460_b200 import kernels
     outs = []
     for _ in range(3):
         h = h0.clone()
