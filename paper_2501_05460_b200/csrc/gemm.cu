@@ -144,6 +144,9 @@ enum EpiKind : int { EK_ROWS_BF16 = 0, EK_ROWS_F32 = 1, EK_ACC_F32 = 2, EK_HEADS
 #endif
 
 constexpr int kEpiStageBytes = 16384;  // per epilogue half: 128 rows x 128 B
+#ifndef EPD_GEMM_BPREFETCH
+#define EPD_GEMM_BPREFETCH 1  // producer fetches the first item's B tiles before the PDL wait
+#endif
 #ifndef EPD_EPI_PERWARP
 #define EPD_EPI_PERWARP 1  // row kinds: one TMA box per warp (32 rows) instead of per 4-warp half
 #endif
@@ -242,6 +245,10 @@ EPD_DEVICE void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"
 EPD_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 EPD_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 EPD_DEVICE void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// tx bytes without an arrival (the arrival comes with the stage's other loads)
+EPD_DEVICE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 EPD_DEVICE int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -382,7 +389,10 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   pdl_trigger();
-  pdl_wait();  // A, the residual stream and the outputs belong to the previous kernels
+  // A, the residual stream and the outputs belong to the previous kernels; the producer
+  // waits only after it has started fetching the first item's weights (B), which no kernel
+  // writes -- with programmatic dependent launch that fetch overlaps the previous kernel's tail
+  if (warp != 0 || !EPD_GEMM_BPREFETCH) pdl_wait();
 
   const int nk = (K + kBK - 1) / kBK;
   // split-K (fp32 reduce-add only): work item = (tile, split), the splits of a tile adjacent
@@ -393,7 +403,34 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
     // TMA producer: the whole warp walks the schedule (uniform operands), one elected lane issues
     int stage = 0;
     uint32_t phase = 0;
-    for (int item = pid; item < num_tiles; item += npid) {
+    int pre = 0;  // k-blocks of this CTA's first item whose B tiles were fetched before the wait
+#if EPD_GEMM_BPREFETCH
+    if (CL <= 2 && pid < num_tiles) {
+      const int tile = pid / nsplit, sp = pid - tile * nsplit;
+      const int kb_lo = sp * nk / nsplit, kb_hi = (sp + 1) * nk / nsplit;
+      const TileAt x = tile_at(sched, tile, BN);
+      const int n0 = x.n0 + crank * (x.w / CG);
+      const bool hw = x.w != BN;
+      const CUtensorMap* tb = hw ? &tmBh : &tmB;
+      const uint32_t b_bytes = hw ? Cfg::B_BYTES / 2 : Cfg::B_BYTES;
+      pre = kb_hi - kb_lo < Cfg::STAGES ? kb_hi - kb_lo : Cfg::STAGES;
+      for (int i = 0; i < pre; ++i) {  // fresh stages: no empty wait
+        if (elect_one()) {
+          if (CG == 1) {
+            mbar_expect_tx(&full[i], b_bytes);
+            tma_load_2d(sB + i * Cfg::B_BYTES, tb, &full[i], (kb_lo + i) * kBK, n0);
+          } else {
+            if (crank == 0) mbar_expect_tx(&full[i], 2 * b_bytes);
+            tma_load_2d_pair(sB + i * Cfg::B_BYTES, tb, &full[i], (kb_lo + i) * kBK, n0);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    pdl_wait();
+#endif
+    bool first = true;
+    for (int item = pid; item < num_tiles; item += npid, first = false) {
       const int tile = item / nsplit, sp = item - tile * nsplit;
       const int kb_lo = sp * nk / nsplit, kb_hi = (sp + 1) * nk / nsplit;
       const TileAt x = tile_at(sched, tile, BN);
@@ -406,6 +443,8 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
       const uint32_t stage_bytes = Cfg::A_BYTES + (hw ? Cfg::B_BYTES / 2 : Cfg::B_BYTES);
       for (int kb = kb_lo; kb < kb_hi; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
+        const bool b_done = first && kb - kb_lo < pre;  // B already in flight (prefetch)
+        const uint32_t bytes = b_done ? (uint32_t)Cfg::A_BYTES : stage_bytes;
 #if EPD_GEMM_EXP == 1  // experiment: no operand loads (MMA + epilogue alone)
         if (elect_one() && crank == 0) mbar_arrive(&full[stage]);
         if (false) {
@@ -413,13 +452,14 @@ __global__ void __launch_bounds__(GemmCfg<BN, CG>::THREADS, 1)
         if (elect_one()) {
 #endif
           if (CG == 1) {
-            mbar_arrive_expect_tx(&full[stage], stage_bytes);
+            mbar_arrive_expect_tx(&full[stage], bytes);
             tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
-            tma_load_2d(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0);
+            if (!b_done) tma_load_2d(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0);
           } else {
-            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * stage_bytes);
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], 2 * bytes);
             tma_load_2d_pair(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * kBK, m0);
-            if (CL == 2)
+            if (b_done) {
+            } else if (CL == 2)
               tma_load_2d_pair(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0);
             else if (pair == 0)  // this half of B, for both pairs
               tma_load_2d_pair_mc(sB + stage * Cfg::B_BYTES, tb, &full[stage], kb * kBK, n0,
