@@ -293,7 +293,8 @@ epd_status_t epd_linear_acc_f32(const void* A, int32_t lda, const void* W, int32
 /* The same, allowed to split K over up to max_split work items per output tile when the tiles
  * alone leave SMs idle (small M, long K: the LLM prefill's down / O projections). The splits
  * add into h in a fixed order, so results are run-to-run deterministic, but the split count
- * follows M: not batch invariant (the encoder path never splits). */
+ * follows M: not batch invariant (the encoder path never splits). Split launches on one device
+ * share a progress-counter buffer: issue them on one stream (or serialize them). */
 epd_status_t epd_linear_acc_f32_split(const void* A, int32_t lda, const void* W, int32_t ldw, int32_t M,
                                       int32_t N, int32_t K, const void* bias, const void* lscale, float* h,
                                       int32_t ldh, int32_t bn, int32_t max_split, void* stream);

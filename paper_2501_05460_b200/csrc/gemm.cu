@@ -956,7 +956,8 @@ int g_cta_group_policy = 0;  // 0 auto; else the cluster size: 1 single CTAs, 2 
 void set_gemm_cta_group(int policy) { g_cta_group_policy = policy; }
 
 // Zeroed split-K progress counters (grown, never freed: queued kernels may still use an old
-// buffer). Not allocated during stream capture -- the GEMM then runs unsplit.
+// buffer). Not allocated during stream capture -- the GEMM then runs unsplit. One buffer per
+// device: split launches must not run concurrently on two streams of the same device.
 static int* split_flags(int need, cudaStream_t stream) {
   static int* buf[16] = {};
   static int cap[16] = {};
