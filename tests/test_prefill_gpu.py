@@ -101,3 +101,26 @@ def test_paged_mm_input_equals_packed(cuda):
     pf.prefill(None, ids, mm_pool=pool, mm_rows=rows.to(torch.int32))
     torch.cuda.synchronize()
     assert torch.equal(pf.h[:662], packed)
+
+
+def test_prefill_matches_transformers_fixture(cuda):
+    """The B200 prefill on the golden weights and inputs of tests/golden/llm_golden.json
+    (transformers Qwen2ForCausalLM, fp32): last-position logits within the bf16 bound."""
+    import importlib.util
+    import json
+    from pathlib import Path
+
+    from paper_2501_05460_b200.prefill import Prefiller
+    golden = Path(__file__).parent / "golden"
+    spec = importlib.util.spec_from_file_location("make_llm_golden", golden / "make_llm_golden.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    cfg, w, mm, ids = mod.golden_inputs()
+    fx = json.loads((golden / "llm_golden.json").read_text())
+    pf = Prefiller(cfg, cuda, max_tokens=64, weights={k: v.to(cuda) for k, v in w.items()})
+    tok = int(pf.prefill(mm.to(cuda), ids.to(cuda, torch.int32)))
+    torch.cuda.synchronize()
+    lg = pf.logits[0, :cfg.vocab].float().cpu()
+    err = float((lg[torch.tensor(fx["logits_idx"])] - torch.tensor(fx["logits"])).abs().max()) / fx["logits_absmax"]
+    print(f"B200 prefill vs transformers Qwen2: logits {err:.2e}, token {tok} vs {fx['token']}")
+    assert err <= TOL_H
