@@ -20,6 +20,11 @@ This is the reference engine's encode branch with real work in place of modeled 
 * ``_on_batch_end`` (engine.py:385-407): prefill reads its MM tokens from those blocks
   (paged prefill), the first token ends it, and the P-side blocks are freed.
 
+* ``_on_arrival`` / ``_admission_reason`` (engine.py:319-355): a request that can never fit
+  (no tokens, longer than the model's context, more MM tokens than an encode instance's or
+  the prefill instance's MM pool) raises :class:`CapacityExceeded`, or -- with
+  ``admission_control`` -- is recorded as rejected with the reference's reason and dropped;
+
 * ``assign_instance`` / ``_arrival_load`` (engine.py:65-78, 277-286): with several encode
   instances (the ranks split into equal groups, each one IRP instance), every arriving
   request goes to the instance the reference's policy picks -- round robin, or least
@@ -43,7 +48,7 @@ from dataclasses import dataclass, field
 import torch
 import torch.distributed as dist
 
-from ._lib import call
+from ._lib import CapacityExceeded, call
 from .blockpool import BlockManager, CacheKind
 from .routing import assign_instance, form_batch, plan_batch, shard_ranges
 
@@ -95,6 +100,7 @@ class RequestRecord:
     completion_time: float | None = None
     first_token: int | None = None
     ep_waited: bool = False
+    rejected: str | None = None     # admission: "empty" / "context" / "mm_capacity" / "kv_capacity"
 
 
 class TraceInvariantError(ValueError):
@@ -102,7 +108,10 @@ class TraceInvariantError(ValueError):
 
 
 def check_causality(r: RequestRecord) -> None:
-    """SimTrace._check_causality (trace.py:119-148) without the decode token times."""
+    """SimTrace._check_causality (trace.py:119-148) without the decode token times; a rejected
+    request has no times to order."""
+    if r.rejected is not None:
+        return
     def ordered(label, a, b):
         if a is not None and b is not None and a > b + 1e-12:
             raise TraceInvariantError(f"request {r.rid}: {label} out of order ({a} > {b})")
@@ -264,7 +273,7 @@ class EPDRuntime:
 
     def __init__(self, stage, prefiller, max_batch: int = 4, e_mm_tokens: int = 48_000, p_mm_tokens: int = 48_000,
                  block_size: int = 16, group=None, instances: int = 1, policy: str = "round_robin",
-                 pool=None, stamps=None):
+                 pool=None, stamps=None, admission_control: bool = False, max_context_tokens: int | None = None):
         """``pool`` / ``stamps`` replace the device MM pool transport and the %globaltimer stamps
         (the gloo CPU tier injects host stand-ins; production uses MMPool and _Stamps)."""
         self.stage, self.pf = stage, prefiller
@@ -292,6 +301,11 @@ class EPDRuntime:
         self.p = pool(self, nblocks) if pool is not None else MMPool(self.device, self.rank, self.world, nblocks,
                                                                      block_size, self.cfg.out_dim, group)
         self.stamps = stamps if stamps is not None else _Stamps(self.device)
+        self.admission_control = admission_control
+        if max_context_tokens is None and prefiller is not None:
+            geo = getattr(getattr(prefiller, "cfg", None), "geometry", None)
+            max_context_tokens = getattr(geo, "max_context_tokens", None)
+        self.max_context = max_context_tokens
         self.seq = 0
         self.keep_mm = False  # tests: keep a copy of each request's MM tokens as prefill read them
 
@@ -352,11 +366,19 @@ class EPDRuntime:
                 nonlocal rr
                 while pending and pending[0].arrival <= now:
                     r = pending.popleft()
+                    mm = r.tiles.shape[0] * T
+                    reason = self._admission_reason(mm, mm + int(r.prompt.numel()))
+                    if reason is not None:
+                        if not self.admission_control:
+                            raise CapacityExceeded(f"request {r.rid} can never fit: {reason}")
+                        recs[r.rid] = RequestRecord(r.rid, r.arrival, int(r.prompt.numel()), mm,
+                                                    mm + int(r.prompt.numel()), r.output_tokens, e_instance=None,
+                                                    p_instance=None, rejected=reason)
+                        continue
                     iid, rr = assign_instance(self.policy, [(i, float(load[i])) for i in range(self.instances)], rr)
                     inst_of[r.rid] = iid
                     queues[iid].append(r.rid)
                     load[iid] += r.tiles.shape[0]
-                    mm = r.tiles.shape[0] * T
                     recs[r.rid] = RequestRecord(r.rid, r.arrival, int(r.prompt.numel()), mm,
                                                 mm + int(r.prompt.numel()), r.output_tokens, e_instance=iid)
         first_tok, kept = {}, {}
@@ -365,46 +387,51 @@ class EPDRuntime:
             # ---- coordinator: _retry_waits first, then a new encode batch (engine.py:680-700)
             cmd = None
             if self.is_coord:
-                if open_loop:
-                    # a new batch starts once the encode instance finished its previous one
-                    # (engine.py: one running batch per instance); meanwhile requests arrive
-                    if enc_done is not None:
-                        enc_done.synchronize()
-                    admit(time.perf_counter() - t_wall0)
-                    if pending and not any(queues) and not ep_wait:
-                        time.sleep(max(0.0, pending[0].arrival - (time.perf_counter() - t_wall0)))
+                try:
+                    if open_loop:
+                        # a new batch starts once the encode instance finished its previous one
+                        # (engine.py: one running batch per instance); meanwhile requests arrive
+                        if enc_done is not None:
+                            enc_done.synchronize()
                         admit(time.perf_counter() - t_wall0)
-                else:
-                    admit(float("inf"))
-                pre = []
-                while ep_wait:
-                    rid = ep_wait[0]
-                    if not self.p.manager.can_allocate(recs[rid].mm_tokens):
-                        break
-                    ep_wait.popleft()
-                    p_blocks[rid] = self.p.manager.allocate(rid, recs[rid].mm_tokens)
-                    pre.append((rid, p_blocks[rid]))
+                        if pending and not any(queues) and not ep_wait:
+                            time.sleep(max(0.0, pending[0].arrival - (time.perf_counter() - t_wall0)))
+                            admit(time.perf_counter() - t_wall0)
+                    else:
+                        admit(float("inf"))
+                    pre = []
+                    while ep_wait:
+                        rid = ep_wait[0]
+                        if not self.p.manager.can_allocate(recs[rid].mm_tokens):
+                            break
+                        ep_wait.popleft()
+                        p_blocks[rid] = self.p.manager.allocate(rid, recs[rid].mm_tokens)
+                        pre.append((rid, p_blocks[rid]))
 
-                batch = []
-                for iid, queue in enumerate(queues):  # every idle encode instance starts a batch
-                    e_mm = self.e_mms[iid]
+                    batch = []
+                    for iid, queue in enumerate(queues):  # every idle encode instance starts a batch
+                        e_mm = self.e_mms[iid]
 
-                    def fits(rid, e_mm=e_mm):
-                        mm = recs[rid].mm_tokens
-                        if not e_mm.can_allocate(mm):
-                            return False
-                        e_mm.allocate(rid, mm)
-                        return True
-                    b = form_batch(list(queue), self.max_batch, fits)
-                    for _ in b:
-                        queue.popleft()
-                    batch += [(rid, reqs[rid].tiles.shape[0], iid) for rid in b]
-                done = not (any(queues) or ep_wait or batch or pre or pending)
-                if not done and not batch and not pre and not pending:
-                    # nothing in flight and nothing can start: a request larger than an MM pool
-                    raise RuntimeError("the MM blocks cannot hold the head request (mm_capacity)")
-                cmd = {"pre": [(rid, blocks, inst_of[rid]) for rid, blocks in pre], "batch": batch, "done": done}
+                        def fits(rid, e_mm=e_mm):
+                            mm = recs[rid].mm_tokens
+                            if not e_mm.can_allocate(mm):
+                                return False
+                            e_mm.allocate(rid, mm)
+                            return True
+                        b = form_batch(list(queue), self.max_batch, fits)
+                        for _ in b:
+                            queue.popleft()
+                        batch += [(rid, reqs[rid].tiles.shape[0], iid) for rid in b]
+                    done = not (any(queues) or ep_wait or batch or pre or pending)
+                    if not done and not batch and not pre and not pending:
+                        # nothing in flight and nothing can start (admission lets no such request in)
+                        raise CapacityExceeded("the MM blocks cannot hold the head request (mm_capacity)")
+                    cmd = {"pre": [(rid, blocks, inst_of[rid]) for rid, blocks in pre], "batch": batch, "done": done}
+                except CapacityExceeded as e:  # every rank raises it (no rank left in a collective)
+                    cmd = {"error": str(e)}
             cmd = self._bcast(cmd)
+            if "error" in cmd:
+                raise CapacityExceeded(cmd["error"])
             if cmd["done"]:
                 break
             self._send(cmd["pre"], held, marks, s)
@@ -466,6 +493,8 @@ class EPDRuntime:
         def sec(ns):
             return (ns - base) / 1e9
         for rid, rec in recs.items():
+            if rec.rejected is not None:
+                continue
             # arrivals are host seconds after the calibration stamp's completion, so they trail
             # the device clock slightly: arrival <= encode start holds by construction
             n = reqs[rid].tiles.shape[0]
@@ -492,6 +521,19 @@ class EPDRuntime:
         self.stamps.n = 0
         return {"records": recs, "ep_wait": waited, "wall_s": wall, "mm": kept,
                 "plans": plan_batch([reqs[r].tiles.shape[0] for r in reqs], self.width)[0]}
+
+    def _admission_reason(self, mm_tokens: int, total_tokens: int) -> str | None:
+        """_admission_reason (engine.py:319-344) for this path's pools: the encode instances'
+        MM blocks and the prefill instance's MM blocks (its KV is the handoff's concern)."""
+        if total_tokens == 0:
+            return "empty"
+        if self.max_context is not None and total_tokens > self.max_context:
+            return "context"
+        if self.e_mms[0].blocks_needed(mm_tokens) > self.e_mms[0].total_blocks:
+            return "mm_capacity"
+        if self.p.manager.blocks_needed(mm_tokens) > self.p.manager.total_blocks:
+            return "kv_capacity"  # the reference's prefill-instance check (MM and KV together)
+        return None
 
     # ---------------------------------------------------------------- per-rank work
     def _encode(self, batch, held, marks, s) -> None:

@@ -132,11 +132,33 @@ def _run(rank, world, scenario):
     from paper_2501_05460_b200.runtime import EPDRuntime, check_causality
     kw = {"plain": {}, "pwait": {"p_mm_tokens": 6 * T}, "ewait": {"e_mm_tokens": 6 * T},
           "inst_rr": {"instances": world, "policy": "round_robin"},
-          "inst_ll": {"instances": world, "policy": "least_loaded"}, "poisson": {}}[scenario]
+          "inst_ll": {"instances": world, "policy": "least_loaded"}, "poisson": {},
+          "admit": {"e_mm_tokens": 6 * T, "admission_control": True, "max_context_tokens": 150},
+          "admit_raise": {"e_mm_tokens": 6 * T}}[scenario]
     stage, pf = _Stage(rank, world), (_Prefiller() if rank == 0 else None)
     rt = EPDRuntime(stage, pf, max_batch=3, block_size=BS, pool=_HostPool, stamps=_Stamps(), **kw)
     rt.keep_mm = True
     reqs = _requests()
+    rejected = {}
+    if scenario.startswith("admit"):
+        # _admission_reason (engine.py:319-344): 7 tiles never fit a 6-tile encode pool; no
+        # tokens at all is "empty"; 12 tiles x 16 + 3 prompt tokens exceed a 150-token context
+        from paper_2501_05460_b200.runtime import ServeRequest
+        extra = [(100, 7, 3, "mm_capacity"), (101, 0, 0, "empty")]
+        if scenario == "admit":
+            extra.append((102, 12, 3, "context"))
+        for rid, n, np_, why in extra:
+            g = torch.Generator().manual_seed(rid)
+            tiles = torch.randint(0, 256, (n, 4, 4, 3), dtype=torch.uint8, generator=g)
+            reqs.insert(2, ServeRequest(rid, tiles, torch.arange(np_, dtype=torch.int32)))
+            rejected[rid] = why
+        if scenario == "admit_raise":
+            from paper_2501_05460_b200._lib import CapacityExceeded
+            try:
+                rt.serve(reqs)
+            except CapacityExceeded as e:
+                return ([] if "can never fit" in str(e) else [f"unexpected message {e}"]), stage.enc.calls
+            return ["admission_control=False must raise CapacityExceeded on every rank"], stage.enc.calls
     if scenario == "poisson":  # open loop: generate_poisson arrivals at 150 requests/s
         from paper_2501_05460_b200.routing import poisson_arrivals
         for r, t in zip(reqs, poisson_arrivals(150.0, len(reqs), 3)):
@@ -144,6 +166,10 @@ def _run(rank, world, scenario):
     out = rt.serve(reqs)
     errs = []
     if rank == 0:
+        for rid, why in rejected.items():
+            if out["records"][rid].rejected != why or out["records"][rid].shards:
+                errs.append(f"request {rid}: rejected {out['records'][rid].rejected!r}, expected {why!r}")
+        reqs = [r for r in reqs if r.rid not in rejected]
         for r in reqs:
             rec = out["records"][r.rid]
             want = _Encoder().encode(r.tiles, torch.empty(r.tiles.shape[0], T, D, dtype=torch.bfloat16))
@@ -169,7 +195,7 @@ def _run(rank, world, scenario):
                 rec = out["records"][r.rid]
                 if rec.arrival != r.arrival or rec.encode_start < r.arrival:
                     errs.append(f"request {r.rid}: arrival {rec.arrival} / encode start {rec.encode_start}")
-        starts = {round(rec.encode_start, 9) for rec in out["records"].values()}
+        starts = {round(rec.encode_start, 9) for rec in out["records"].values() if rec.rejected is None}
         if scenario == "ewait" and len(starts) < 4 * rt.instances:
             errs.append(f"ewait: {len(starts)} batches")
         if scenario.startswith("inst"):
@@ -200,7 +226,7 @@ def _worker(rank, world, port, scenario, q):
 
 @pytest.mark.parametrize("world,scenario", [(1, "plain"), (1, "pwait"), (2, "plain"), (2, "pwait"),
                                             (2, "ewait"), (2, "inst_rr"), (2, "inst_ll"), (1, "poisson"),
-                                            (2, "poisson")])
+                                            (2, "poisson"), (2, "admit"), (2, "admit_raise")])
 def test_runtime_control_logic_gloo(world, scenario):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
