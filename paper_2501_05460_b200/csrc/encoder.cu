@@ -21,8 +21,10 @@
 
 namespace epd {
 
-// Largest chunk whose forward is launched with PDL in auto mode (launch.h).
-constexpr int kPdlMaxTiles = 3;
+// Largest chunk whose forward is launched with PDL in auto mode (launch.h): every chunk size
+// since round 2 (same-box A/B, profiles/r02/ab.txt: 1-3 tile shards 4-6 % faster, C5 +0.9 %,
+// C2 +0.2 %; round 1's erratic C5 under PDL was the attention barrier-region overlap, since fixed).
+constexpr int kPdlMaxTiles = 1 << 30;
 
 namespace {
 
@@ -662,7 +664,7 @@ int Encoder::prof_read(double* ms, double* flops, double* bytes, int64_t* count,
 }
 
 int Encoder::forward_chunk(const uint8_t* tiles, int nt, bf16* out, cudaStream_t s) {
-  // PDL (auto mode) for small IRP shards only; scheduling only, results are identical
+  // PDL (auto mode); scheduling only, results are identical
   PdlScope pdl(nt <= kPdlMaxTiles);
   const int M = nt * T;
   const float eps = d.ln_eps;

@@ -5,9 +5,9 @@
 // kernel executes griddepcontrol.wait (pdl_wait) before it touches memory the previous
 // kernel produced or consumes. Because every kernel waits before completing, the
 // ordering is transitive along the stream. EPD_PDL=1 forces it on, EPD_PDL=0 off; by default
-// (auto) the encoder turns it on only for small chunks (PdlScope), where launch ramps are a
-// large share of every kernel: a 1-3 tile IRP shard runs 4-6 % faster, while on 10-tile
-// chunks it cost 6 % on the power-capped C2 step and made C5 erratic (671-900 vs 1135 tiles/s).
+// (auto) the encoder turns it on for its forward (PdlScope): a 1-3 tile IRP shard runs 4-6 %
+// faster, a 13-tile C5 request ~1 %. (Round 1 measured 10-tile chunks slower and C5 erratic
+// under PDL; that was the attention kernel's barrier region overlapping its TMEM holder.)
 #pragma once
 
 #include <cuda_runtime.h>
